@@ -1,0 +1,6 @@
+"""CPU oracle for the WFST decode path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its ``cpu_baseline`` leg and
+``--impl reference``) may import this package, and only as the checker / CPU baseline.  The
+product package ``paper_1808_00687_b200`` never imports it.
+"""
