@@ -1,0 +1,144 @@
+/*
+ * wfst_b200.h -- C ABI of the B200-native WFST Viterbi decoder (libwfstb200.so).
+ *
+ * Drop-in boundary for the reference decode path (`lsd_wfst`, a pure-Python package).  The
+ * reference has no C ABI of its own; each entry point below replaces the Python call named
+ * beside it (paths relative to /root/reference/pkg/src/lsd_wfst):
+ *
+ *   wb_graph_create      Wfst.__init__ arc layout (wfst.py:163-206) + epsilon_cycle() cache
+ *                        (wfst.py:242-247) + _check_compatible's max-ilabel scan (decoder.py:294)
+ *   wb_decode            decode / decode_fsd / decode_lsd (decoder.py:349-367) and
+ *                        parallel_decode (parallel.py:205-355) -- whole batches of utterances
+ *   wb_lattice_*         LatticeRecorder + build_lattice (lattice.py:96-249) and
+ *                        prune_lattice (lattice.py:359-501)
+ *
+ * Plain pointers and sizes only; no torch types.  Status convention: every function returns
+ * an int status, WB_OK == 0; the text of the last failure on the calling thread is available
+ * from wb_last_error().  The Python shim maps WB_ERR_VALUE -> ValueError, WB_ERR_WFST ->
+ * WfstError, WB_ERR_LATTICE -> LatticeError, others -> RuntimeError.
+ *
+ * Threading: graph handles are immutable after creation and may be shared by threads using
+ * the same device.  A decoder handle owns mutable device workspace: one call at a time.
+ */
+#ifndef WFST_B200_H
+#define WFST_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WB_OK 0
+#define WB_ERR_CUDA 1
+#define WB_ERR_VALUE 2
+#define WB_ERR_LATTICE 3
+#define WB_ERR_WFST 4
+#define WB_ERR_CAPACITY 5  /* a device workspace capacity was exceeded; retry with a larger one */
+#define WB_ERR_NOMEM 6
+
+#define WB_MEM_DEVICE 0    /* all batch pointers are device pointers; the call is asynchronous */
+#define WB_MEM_HOST 1      /* all batch pointers are host pointers; the call copies and syncs */
+
+typedef struct wb_graph_s *wb_graph_t;
+typedef struct wb_decoder_s *wb_decoder_t;
+
+/* Host-side CSR description (arrays are read during wb_graph_create only). */
+typedef struct {
+    int32_t num_states;
+    int32_t num_arcs;
+    int32_t start;
+    int32_t _pad;
+    const int32_t *row_ptr;  /* [S+1] arc_offsets               (wfst.py:185-190) */
+    const int32_t *eps_end;  /* [S]   eps_split                 (wfst.py:192-198) */
+    const int32_t *dst;      /* [A]   arcs sorted by (src, ilabel, dst, olabel, weight) */
+    const int32_t *ilabel;   /* [A] */
+    const int32_t *olabel;   /* [A] */
+    const double *weight;    /* [A] */
+    const double *final_w;   /* [S]   +inf = not final          (wfst.py:183) */
+} wb_graph_desc;
+
+/* Search configuration (DecodeConfig, decoder.py:78-94). */
+typedef struct {
+    double beam;             /* +inf allowed */
+    double blank_threshold;  /* LSD: a frame is blank iff blank_prob > threshold */
+    int32_t max_active;      /* 0 = None */
+    int32_t mode;            /* 0 = fsd, 1 = lsd */
+    int32_t lattice;         /* 1 = record the raw lattice (LatticeRecorder) */
+    int32_t _pad;
+} wb_config;
+
+/* Per-utterance result (DecodeResult, decoder.py:97-105) plus device counters. */
+typedef struct {
+    double total_cost;
+    int64_t tokens_expanded;
+    int32_t search_steps;
+    int32_t reached_final;
+    int32_t died_at_step;    /* -1 = None */
+    int32_t final_state;     /* state of the winning token */
+    int32_t final_step;      /* node step of the winning token (lattice finals) */
+    int32_t n_olabels;
+    int32_t n_ilabels;
+    int32_t status;          /* WB_OK or WB_ERR_CAPACITY */
+    int64_t best_trace;      /* backpointer-arena index of the winning token */
+    /* counters for the roofline: summed over the utterance's steps */
+    int64_t n_tok;           /* live tokens expanded */
+    int64_t a_emit;          /* emitting arcs scanned */
+    int64_t a_fin;           /* emitting relaxations with finite acoustic cost */
+    int64_t e_eps;           /* epsilon relaxations (self-loops excluded) */
+    int64_t n_cand;          /* recombined candidates */
+    int64_t n_surv;          /* survivors */
+    int64_t n_rec;           /* backpointer records written */
+    int64_t lat_arcs;        /* raw lattice arcs recorded (lattice mode) */
+} wb_utt_result;
+
+/* Decoder workspace options (0 = automatic). */
+typedef struct {
+    int32_t max_utts_in_flight;  /* concurrent utterances = persistent CTAs */
+    int32_t cand_capacity;       /* per-step candidate capacity per utterance */
+    int64_t arena_capacity;      /* backpointer records per wb_decode call */
+    int32_t max_frames;          /* longest utterance a call may contain */
+    int32_t block_threads;       /* 256, 512 or 1024 */
+    int64_t lattice_capacity;    /* raw lattice arcs per call (lattice mode) */
+} wb_decoder_opts;
+
+const char *wb_last_error(void);
+int wb_version(void);
+int wb_device_count(int32_t *n);
+
+int wb_graph_create(const wb_graph_desc *desc, int32_t device, wb_graph_t *out);
+int wb_graph_destroy(wb_graph_t g);
+int wb_graph_device_bytes(wb_graph_t g, int64_t *bytes);
+
+int wb_decoder_create(wb_graph_t g, const wb_decoder_opts *opts, wb_decoder_t *out);
+int wb_decoder_destroy(wb_decoder_t d);
+int wb_decoder_device_bytes(wb_decoder_t d, int64_t *bytes);
+
+/*
+ * Decode a batch of independent utterances in one persistent kernel launch.
+ *
+ *   costs       [R, num_cols] float64 rows; column 0 must be +inf (frame_costs, posteriors.py:136)
+ *   row_offset  [n_utts] first row of each utterance in `costs`
+ *   num_frames  [n_utts] T of each utterance
+ *   blank       [R] blank probability of each row (LSD pre-pass input)
+ *   results     [n_utts]
+ *   olabels / ilabels [n_utts * label_capacity]; an utterance whose path is longer than
+ *               label_capacity reports its true n_*labels and status WB_ERR_CAPACITY.
+ *
+ * memory_kind WB_MEM_DEVICE: pointers are device pointers, work is enqueued on `stream`
+ * (a cudaStream_t, may be NULL) and the call returns without synchronising.
+ * memory_kind WB_MEM_HOST: pointers are host pointers (pinned for full copy bandwidth); the
+ * call copies inputs in, decodes, copies results out and synchronises.
+ */
+int wb_decode(wb_decoder_t d, int32_t n_utts, const double *costs, const int64_t *row_offset,
+              const int32_t *num_frames, int32_t num_cols, const double *blank,
+              const wb_config *cfg, wb_utt_result *results, int32_t *olabels, int32_t *ilabels,
+              int32_t label_capacity, int32_t memory_kind, void *stream);
+
+/* Device time (ms) of the decode kernel of the last wb_decode call (CUDA events on its stream). */
+int wb_last_kernel_ms(wb_decoder_t d, float *ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WFST_B200_H */

@@ -1,1 +1,26 @@
-"""B200-native WFST Viterbi decoder (arXiv 1808.00687), drop-in for ``lsd_wfst``'s decode path."""
+"""B200-native WFST Viterbi decoder (arXiv 1808.00687), drop-in for ``lsd_wfst``'s decode path.
+
+Public names mirror ``lsd_wfst`` (reference ``pkg/src/lsd_wfst/__init__.py``) for the decode
+path: graph + per-frame acoustic scores in; best path, cost and lattices out.  The search
+itself runs in hand-written sm_100a CUDA kernels (``csrc/``) behind the C ABI declared in
+``include/wfst_b200.h``.
+"""
+__version__ = "0.1.0"
+
+from .decoder import (BatchDecoder, BatchOutput, DecodeConfig, DecodeResult, DeviceGraph,
+                      SearchDied, as_wfst, decode, decode_batch, decode_fsd, decode_lsd,
+                      parallel_decode)
+from .lattice import LatticeError, LatticeRecorder
+from .posteriors import (BlankMask, PosteriorFormatError, PosteriorMatrix, acoustic_cost,
+                         classify_blank_frames, cost_table, frame_costs)
+from .wfst import (Arc, EpsilonCycle, ParseError, Wfst, WfstError, parse_wfst_text,
+                   validate_epsilon_acyclic)
+
+__all__ = [
+    "Arc", "BatchDecoder", "BatchOutput", "BlankMask", "DecodeConfig", "DecodeResult",
+    "DeviceGraph", "EpsilonCycle", "LatticeError", "LatticeRecorder", "ParseError",
+    "PosteriorFormatError", "PosteriorMatrix", "SearchDied", "Wfst", "WfstError",
+    "acoustic_cost", "as_wfst", "classify_blank_frames", "cost_table", "decode",
+    "decode_batch", "decode_fsd", "decode_lsd", "frame_costs", "parallel_decode",
+    "parse_wfst_text", "validate_epsilon_acyclic",
+]

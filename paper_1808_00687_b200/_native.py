@@ -1,0 +1,114 @@
+"""ctypes binding of ``libwfstb200.so`` (the C ABI in ``include/wfst_b200.h``).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (nvcc, sm_100a).  There is
+no fallback: if the library is missing, or no CUDA device is visible, every decode call
+raises -- the product path never silently runs on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libwfstb200.so")
+
+WB_OK, WB_ERR_CUDA, WB_ERR_VALUE, WB_ERR_LATTICE, WB_ERR_WFST, WB_ERR_CAPACITY, WB_ERR_NOMEM = range(7)
+WB_MEM_DEVICE, WB_MEM_HOST = 0, 1
+
+
+class NativeError(RuntimeError):
+    """A CUDA / native failure reported by libwfstb200."""
+
+
+class CapacityError(NativeError):
+    """A device workspace capacity was exceeded (the caller may retry larger)."""
+
+
+class GraphDesc(C.Structure):
+    _fields_ = [("num_states", C.c_int32), ("num_arcs", C.c_int32), ("start", C.c_int32),
+                ("_pad", C.c_int32),
+                ("row_ptr", C.c_void_p), ("eps_end", C.c_void_p), ("dst", C.c_void_p),
+                ("ilabel", C.c_void_p), ("olabel", C.c_void_p), ("weight", C.c_void_p),
+                ("final_w", C.c_void_p)]
+
+
+class Config(C.Structure):
+    _fields_ = [("beam", C.c_double), ("blank_threshold", C.c_double),
+                ("max_active", C.c_int32), ("mode", C.c_int32), ("lattice", C.c_int32),
+                ("_pad", C.c_int32)]
+
+
+class DecoderOpts(C.Structure):
+    _fields_ = [("max_utts_in_flight", C.c_int32), ("cand_capacity", C.c_int32),
+                ("arena_capacity", C.c_int64), ("max_frames", C.c_int32),
+                ("block_threads", C.c_int32), ("lattice_capacity", C.c_int64)]
+
+
+UTT_RESULT_DTYPE = np.dtype([
+    ("total_cost", np.float64), ("tokens_expanded", np.int64), ("search_steps", np.int32),
+    ("reached_final", np.int32), ("died_at_step", np.int32), ("final_state", np.int32),
+    ("final_step", np.int32), ("n_olabels", np.int32), ("n_ilabels", np.int32),
+    ("status", np.int32), ("best_trace", np.int64), ("n_tok", np.int64), ("a_emit", np.int64),
+    ("a_fin", np.int64), ("e_eps", np.int64), ("n_cand", np.int64), ("n_surv", np.int64),
+    ("n_rec", np.int64), ("lat_arcs", np.int64)])
+
+_lib = None
+
+# Every symbol include/wfst_b200.h declares (checked by tests/test_native_abi.py).
+EXPORTED = ("wb_last_error", "wb_version", "wb_device_count", "wb_graph_create",
+            "wb_graph_destroy", "wb_graph_device_bytes", "wb_decoder_create",
+            "wb_decoder_destroy", "wb_decoder_device_bytes", "wb_decode", "wb_last_kernel_ms")
+
+
+def load():
+    """Load and prototype the library (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeError(f"{LIB_PATH} is missing: run __graft_entry__.build() first "
+                          "(the decoder has no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    L.wb_last_error.restype = C.c_char_p
+    L.wb_version.restype = C.c_int
+    L.wb_device_count.argtypes = [C.POINTER(C.c_int32)]
+    L.wb_graph_create.argtypes = [C.POINTER(GraphDesc), C.c_int32, C.POINTER(C.c_void_p)]
+    L.wb_graph_destroy.argtypes = [C.c_void_p]
+    L.wb_graph_device_bytes.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
+    L.wb_decoder_create.argtypes = [C.c_void_p, C.POINTER(DecoderOpts), C.POINTER(C.c_void_p)]
+    L.wb_decoder_destroy.argtypes = [C.c_void_p]
+    L.wb_decoder_device_bytes.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
+    L.wb_decode.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                            C.c_void_p, C.POINTER(Config), C.c_void_p, C.c_void_p, C.c_void_p,
+                            C.c_int32, C.c_int32, C.c_void_p]
+    L.wb_last_kernel_ms.argtypes = [C.c_void_p, C.POINTER(C.c_float)]
+    _lib = L
+    return L
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == WB_OK:
+        return
+    msg = (load().wb_last_error() or b"").decode(errors="replace")
+    text = f"{what}: {msg}" if what else msg
+    if rc == WB_ERR_VALUE:
+        raise ValueError(text)
+    if rc == WB_ERR_WFST:
+        from .wfst import WfstError
+        raise WfstError(text)
+    if rc == WB_ERR_LATTICE:
+        from .lattice import LatticeError
+        raise LatticeError(text)
+    if rc == WB_ERR_CAPACITY:
+        raise CapacityError(text)
+    raise NativeError(text)
+
+
+def device_count() -> int:
+    n = C.c_int32(0)
+    rc = load().wb_device_count(C.byref(n))
+    if rc != WB_OK:
+        return 0
+    return int(n.value)

@@ -1,0 +1,147 @@
+// device_common.cuh -- small sm_100a building blocks shared by the decoder kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace wb {
+
+typedef unsigned long long u64;
+typedef unsigned int u32;
+
+constexpr u64 EMPTY_KEY = 0xFFFFFFFFFFFFFFFFull;
+constexpr u64 SIGN64 = 0x8000000000000000ull;
+constexpr u32 EPS_BIT = 0x80000000u;   // payload tag: winner came through an epsilon arc
+constexpr u32 ROOT_PREV = 0xFFFFFFFFu; // trace root (decoder.py:27 ROOT_TRACE)
+constexpr u32 FULL = 0xFFFFFFFFu;
+
+// Order-preserving map from float64 cost to u64, with -0.0 folded onto +0.0 so that the two
+// compare equal exactly as Python floats do (frame_costs yields -0.0 for p = 1).
+__device__ __forceinline__ u64 cost_key(double c) {
+    c = __dadd_rn(c, 0.0);  // -0.0 + 0.0 == +0.0 under round-to-nearest
+    u64 b = (u64)__double_as_longlong(c);
+    return (b & SIGN64) ? ~b : (b | SIGN64);
+}
+__device__ __forceinline__ double key_cost(u64 k) {
+    u64 b = (k & SIGN64) ? (k & ~SIGN64) : ~k;
+    return __longlong_as_double((long long)b);
+}
+
+// Recombination slot: (cost key, arc index + 1, payload).  Ordered by (key, arcp1); since arcs
+// are sorted by source state, arc order == (src state, arc) order of decoder.py:131.
+struct __align__(16) Slot {
+    u64 key;
+    u32 arcp1;
+    u32 pay;
+};
+
+__device__ __forceinline__ Slot ld_slot(const Slot *p) {
+    // L2-coherent read (slots are updated by L2 atomics from other warps)
+    ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2 *>(p));
+    Slot s;
+    s.key = v.x;
+    s.arcp1 = (u32)v.y;
+    s.pay = (u32)(v.y >> 32);
+    return s;
+}
+__device__ __forceinline__ void st_slot_empty(Slot *p) {
+    __stcg(reinterpret_cast<ulonglong2 *>(p), make_ulonglong2(EMPTY_KEY, EMPTY_KEY));
+}
+
+// 128-bit compare-and-swap (ATOMG.E.CAS.128).  Returns the previous value.
+__device__ __forceinline__ Slot cas_slot(Slot *p, const Slot &expect, const Slot &desired) {
+    u64 elo = expect.key, ehi = ((u64)expect.pay << 32) | expect.arcp1;
+    u64 dlo = desired.key, dhi = ((u64)desired.pay << 32) | desired.arcp1;
+    u64 olo, ohi;
+    asm volatile(
+        "{\n\t.reg .b128 e, d, o;\n\t"
+        "mov.b128 e, {%2, %3};\n\t"
+        "mov.b128 d, {%4, %5};\n\t"
+        "atom.relaxed.gpu.global.cas.b128 o, [%6], e, d;\n\t"
+        "mov.b128 {%0, %1}, o;\n\t}"
+        : "=l"(olo), "=l"(ohi)
+        : "l"(elo), "l"(ehi), "l"(dlo), "l"(dhi), "l"(p)
+        : "memory");
+    Slot o;
+    o.key = olo;
+    o.arcp1 = (u32)ohi;
+    o.pay = (u32)(ohi >> 32);
+    return o;
+}
+
+__device__ __forceinline__ bool slot_better(u64 key, u32 arcp1, const Slot &cur) {
+    return key < cur.key || (key == cur.key && arcp1 < cur.arcp1);
+}
+
+// Min-recombination under the (cost, src, arc) total order with equal keys rejected
+// (_relax, decoder.py:121-135; StateSlots.relax, parallel.py:106-128).
+// Returns true when this candidate was installed; *first = slot was empty before,
+// *decreased = the slot's cost strictly dropped (so epsilon successors must be re-relaxed).
+__device__ __forceinline__ bool relax_slot(Slot *p, u64 key, u32 arcp1, u32 pay, bool *first,
+                                           bool *decreased) {
+    Slot cur = ld_slot(p);
+    Slot want;
+    want.key = key;
+    want.arcp1 = arcp1;
+    want.pay = pay;
+    while (slot_better(key, arcp1, cur)) {
+        Slot prev = cas_slot(p, cur, want);
+        if (prev.key == cur.key && prev.arcp1 == cur.arcp1 && prev.pay == cur.pay) {
+            *first = cur.key == EMPTY_KEY;
+            *decreased = key < cur.key;
+            return true;
+        }
+        cur = prev;
+    }
+    return false;
+}
+
+__device__ __forceinline__ u32 lanemask_lt() {
+    u32 m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ int warp_incl_scan(int v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int n = __shfl_up_sync(FULL, v, o);
+        if (lane >= o) v += n;
+    }
+    return v;
+}
+
+// Largest lane k with excl[k] <= j (excl non-decreasing, excl[0] == 0).
+__device__ __forceinline__ int warp_owner(int excl, int j) {
+    int k = 0;
+#pragma unroll
+    for (int b = 16; b >= 1; b >>= 1) {
+        int e = __shfl_sync(FULL, excl, k + b);
+        if (e <= j) k += b;
+    }
+    return k;
+}
+
+__device__ __forceinline__ u64 warp_min_u64(u64 v) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        u64 n = __shfl_xor_sync(FULL, v, o);
+        v = n < v ? n : v;
+    }
+    return v;
+}
+__device__ __forceinline__ u64 warp_max_u64(u64 v) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        u64 n = __shfl_xor_sync(FULL, v, o);
+        v = n > v ? n : v;
+    }
+    return v;
+}
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+
+}  // namespace wb

@@ -1,0 +1,50 @@
+"""GPU decode vs the CPU oracle on seeded instances (bit-exact DecodeResult)."""
+import math
+
+import numpy as np
+import pytest
+
+import paper_1808_00687_b200 as P
+from paper_1808_00687_b200 import synth
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+INF = math.inf
+
+
+def _fields(r):
+    return (r.total_cost, r.olabels, r.ilabels, r.search_steps, r.tokens_expanded,
+            r.reached_final, r.died_at_step)
+
+
+def _check_batch(g, posts, cfg, canonical=False):
+    got = P.decode_batch(g, posts, cfg)
+    for i, (p, r) in enumerate(zip(posts, got)):
+        o = O.decode(g, P.cost_table(p, cfg.acoustic_scale), p.rows[:, p.blank_col],
+                     beam=cfg.beam, max_active=cfg.max_active, mode=cfg.mode,
+                     blank_threshold=cfg.blank_threshold, canonical=canonical)
+        assert _fields(r) == o.astuple(), (i, r, o)
+
+
+@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("mode", ["fsd", "lsd"])
+def test_random_small(cuda, seed, mode):
+    rng = np.random.default_rng(seed)
+    S = int(rng.integers(2, 60))
+    g = synth.random_wfst(seed, S, int(S * rng.uniform(1, 4)), int(rng.integers(1, 6)),
+                          eps_fraction=[0.0, 0.15, 0.3][seed % 3], selfloops=seed % 2 == 0,
+                          final_fraction=0.3)
+    L = int(g.max_ilabel) or 1
+    posts = [synth.random_posteriors(seed * 100 + k, int(rng.integers(0, 12)), L,
+                                     blank_fraction=0.3) for k in range(5)]
+    for beam, ma in ((INF, None), (4.0, None), (INF, 3), (6.0, 5)):
+        _check_batch(g, posts, P.DecodeConfig(beam=beam, max_active=ma, mode=mode))
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_medium_graph(cuda, seed):
+    g = synth.random_wfst(seed, 5000, 16000, 50, eps_fraction=0.05, selfloops=True,
+                          final_fraction=0.05)
+    posts = [synth.random_posteriors(seed * 7 + k, 120, 50, blank_fraction=0.2) for k in range(8)]
+    _check_batch(g, posts, P.DecodeConfig(beam=10.0, max_active=300, mode="fsd"))
+    _check_batch(g, posts, P.DecodeConfig(beam=7.0, mode="lsd"))
