@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 WFST decode path (BASELINE.json metric, config 2 by default).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl b200|reference]
+
+A step = one persistent-kernel decode of one batch (64 utterances x 1000 frames of the
+config-2 synthetic HCLG-like graph per GPU; utterances are sharded by rank -> weak scaling).
+Prints ONE JSON line on rank 0:
+
+  value      decoded frames/s over all ranks, inputs (float64 cost table + blank column)
+             already resident in HBM, device time from CUDA events (max over ranks)
+  e2e        the same metric through the C ABI with HOST (pinned) buffers: H2D of the cost
+             table, decode, D2H of results + labels inside every timed step
+  roofline   algorithmic bytes of the decode kernel (SURVEY 8d convention, from device
+             counters) / its CUDA-event time, against MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline  the C oracle port of the reference serial decoder on all host cores, on a
+             bounded sample of the same workload (rank 0, N=1)
+
+``--impl reference`` times the reference algorithm's CPU port (oracle/, all host threads) on
+the same config, metric and unit, and prints its own line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "decoded frames/sec & arcs/sec per GPU (1/2/4/8 B200), RTF, HBM-roofline frac vs CPU"
+FRAME_SHIFT_S = 0.010  # RTF assumes a 10 ms frame shift (stated)
+
+CONFIGS = {
+    "1": dict(name="config1: toy synthetic WFST 1k states/10k arcs/50 pdfs, 1 utt x 200 frames, "
+                   "beam 10, FSD", states=1000, arcs=10000, labels=50, utts=1, frames=200,
+              beam=10.0, max_active=None, mode="fsd", blank_fraction=0.0, eps=0.05,
+              selfloops=True, final_fraction=0.05),
+    "2": dict(name="config2: synthetic HCLG-like graph 1M states/3M arcs/3k pdfs, 64 utt x 1000 "
+                   "frames, beam 13, max-active 7000, FSD", states=1_000_000, arcs=3_000_000,
+              labels=3000, utts=64, frames=1000, beam=13.0, max_active=7000, mode="fsd",
+              blank_fraction=0.0, eps=0.015, selfloops=False, final_fraction=0.01),
+    "4": dict(name="config4: CTC LSD, 5k-label synthetic TLG-like graph (self-loops), 256 utt x "
+                   "1500 frames, 80% blank frames, blank-skip threshold 0.98, beam 13, "
+                   "max-active 7000", states=100_000, arcs=300_000, labels=5000, utts=256,
+              frames=1500, beam=13.0, max_active=7000, mode="lsd", blank_fraction=0.8,
+              eps=0.015, selfloops=True, final_fraction=0.01),
+}
+
+# SURVEY 8d algorithmic bytes per step and utterance
+def algorithmic_bytes(r) -> int:
+    return int(24 * r["n_tok"].sum() + 24 * r["a_emit"].sum() + 16 * r["a_fin"].sum()
+               + 32 * r["e_eps"].sum() + 24 * r["n_cand"].sum() + 16 * r["n_surv"].sum())
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.idx = device_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        for r in self.rows:
+            for name, v in zip(self.NAMES, r[3:]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_workload(cfg: dict, rank: int, utts: int, frames: int):
+    from paper_1808_00687_b200 import synth
+    from paper_1808_00687_b200.posteriors import cost_table
+    g = synth.random_wfst(0, cfg["states"], cfg["arcs"], cfg["labels"], eps_fraction=cfg["eps"],
+                          selfloops=cfg["selfloops"], final_fraction=cfg["final_fraction"])
+    L1 = cfg["labels"] + 1
+    T = np.full(utts, frames, dtype=np.int32)
+    off = np.zeros(utts, dtype=np.int64)
+    np.cumsum(T[:-1], out=off[1:])
+    R = int(T.sum())
+    return g, L1, T, off, R
+
+
+def fill_inputs(cfg, rank, T, off, L1, costs_out, blank_out):
+    from paper_1808_00687_b200 import synth
+    from paper_1808_00687_b200.posteriors import PosteriorMatrix, cost_table
+    for i, (o, t) in enumerate(zip(off, T)):
+        rows = synth.random_posterior_rows(1000 * rank + i + 1, int(t), cfg["labels"],
+                                           blank_fraction=cfg["blank_fraction"])
+        p = PosteriorMatrix(rows, 0, validate=False)
+        cost_table(p, 1.0, out=costs_out[o:o + t])
+        blank_out[o:o + t] = rows[:, 0]
+
+
+def cpu_sample(g, cfg, L1, n_threads: int, frames: int):
+    """The oracle (C port of decoder.py) on one full utterance per host thread."""
+    from oracle import oracle as O
+    from paper_1808_00687_b200 import synth
+    from paper_1808_00687_b200.posteriors import PosteriorMatrix, cost_table
+    n = n_threads
+    costs, blanks = [], []
+    for i in range(n):
+        rows = synth.random_posterior_rows(i + 1, frames, cfg["labels"],
+                                           blank_fraction=cfg["blank_fraction"])
+        costs.append(cost_table(PosteriorMatrix(rows, 0, validate=False)))
+        blanks.append(np.ascontiguousarray(rows[:, 0]))
+    og = O.OracleGraph(g)
+    t0 = time.perf_counter()
+    res = O.decode_batch(og, costs, blanks, beam=cfg["beam"], max_active=cfg["max_active"],
+                         mode=cfg["mode"], n_threads=n_threads)
+    wall = time.perf_counter() - t0
+    return wall, n * frames, res
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the reference algorithm's CPU port on all host threads."""
+    if rank != 0:
+        return
+    frames = args.frames or cfg["frames"]
+    g, L1, *_ = make_workload(cfg, 0, 1, frames)
+    threads = len(os.sched_getaffinity(0))
+    n_thr = max(1, min(threads, args.utts or cfg["utts"]))
+    for _ in range(args.warmup):
+        cpu_sample(g, cfg, L1, n_thr, min(frames, 50))
+    walls = []
+    nfr = 0
+    for _ in range(args.steps):
+        w, nf, _ = cpu_sample(g, cfg, L1, n_thr, frames)
+        walls.append(w)
+        nfr += nf
+    value = nfr / sum(walls)
+    sample = (f"{n_thr} utterances x {frames} frames per step on {n_thr} threads "
+              f"(one full utterance per thread)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * sum(walls) / len(walls), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["name"], "parallelism": f"{n_thr} host threads"},
+            "cpu_baseline": {"value": value, "unit": "frames/s", "cores": n_thr, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--utts", type=int, default=0, help="utterances per GPU (default: config)")
+    ap.add_argument("--frames", type=int, default=0, help="frames per utterance (default: config)")
+    ap.add_argument("--block", type=int, default=0, help="threads per CTA (0 = auto)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu)")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.warmup < 0 or args.steps < 1:
+        raise SystemExit("need --steps >= 1")
+
+    if args.impl == "reference":
+        import __graft_entry__
+        __graft_entry__.build()
+        run_reference(args, cfg, rank, world)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_1808_00687_b200 import _native as N
+    from paper_1808_00687_b200.decoder import BatchDecoder, DecodeConfig
+
+    utts = args.utts or cfg["utts"]
+    frames = args.frames or cfg["frames"]
+    g, L1, T, off, R = make_workload(cfg, rank, utts, frames)
+    # pinned host inputs (the e2e path copies from these every step)
+    costs_h = torch.empty((R, L1), dtype=torch.float64, pin_memory=True)
+    blank_h = torch.empty(R, dtype=torch.float64, pin_memory=True)
+    fill_inputs(cfg, rank, T, off, L1, costs_h.numpy(), blank_h.numpy())
+    dcfg = DecodeConfig(beam=cfg["beam"], max_active=cfg["max_active"], mode=cfg["mode"])
+
+    block = args.block or (1024 if utts <= 148 else 512)
+    dec = BatchDecoder(g, local, max_utts_in_flight=min(utts, 148 * (1024 // block)),
+                       block_threads=block)
+    dec.reserve(int(T.sum()) + utts, cfg["max_active"], int(T.max()))
+    cap = frames + 64
+
+    dev = torch.device(f"cuda:{local}")
+    costs_d = costs_h.to(dev)
+    blank_d = blank_h.to(dev)
+    off_d = torch.from_numpy(off).to(dev)
+    T_d = torch.from_numpy(T).to(dev)
+    itemsize = N.UTT_RESULT_DTYPE.itemsize
+    res_d = torch.empty(utts * itemsize, dtype=torch.uint8, device=dev)
+    ol_d = torch.empty((utts, cap), dtype=torch.int32, device=dev)
+    il_d = torch.empty((utts, cap), dtype=torch.int32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step():
+        dec.decode_device(costs_d, off_d, T_d, blank_d, dcfg, cfg["mode"], res_d, ol_d, il_d, cap)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    res = np.frombuffer(res_d.cpu().numpy().tobytes(), dtype=N.UTT_RESULT_DTYPE)
+    if (res["status"] != 0).any():
+        raise SystemExit(f"decode reported status {np.unique(res['status'])}")
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    sampler = ClockSampler(local) if rank == 0 else None
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    kernel_ms = []
+    barrier()
+    if sampler:
+        sampler.start()
+    for k in range(args.steps):
+        flush.zero_()                       # evict L2 between timed steps
+        ev[k][0].record()
+        step()
+        ev[k][1].record()
+        torch.cuda.synchronize()
+        kernel_ms.append(dec.last_kernel_ms())
+    barrier()
+    clocks = sampler.stop() if sampler else None
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    if dist is not None:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    frames_step = int(T.sum())
+    res = np.frombuffer(res_d.cpu().numpy().tobytes(), dtype=N.UTT_RESULT_DTYPE)
+    relax = int(res["a_fin"].sum() + res["e_eps"].sum())
+    nbytes = algorithmic_bytes(res)
+    avg_kernel_ms = sum(kernel_ms) / len(kernel_ms)
+    peak, peak_src = peaks()
+    achieved = nbytes / (avg_kernel_ms * 1e-3) / 1e9
+
+    # ---------------- e2e through the C ABI with host buffers
+    e2e = None
+    if not (args.no_e2e or args.profile):
+        costs_np, blank_np = costs_h.numpy(), blank_h.numpy()
+        dec.decode_host(costs_np, off, T, blank_np, dcfg, cfg["mode"], cap)  # warm
+        e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in range(args.steps)]
+        barrier()
+        for k in range(args.steps):
+            flush.zero_()
+            e_ev[k][0].record()
+            out = dec.decode_host(costs_np, off, T, blank_np, dcfg, cfg["mode"], cap)
+            e_ev[k][1].record()
+            torch.cuda.synchronize()
+        barrier()
+        e_ms = sum(a.elapsed_time(b) for a, b in e_ev)
+        if dist is not None:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        h2d = costs_np.nbytes + blank_np.nbytes + off.nbytes + T.nbytes
+        d2h = out.results.nbytes + out.olabels.nbytes + out.ilabels.nbytes
+        e2e = {"value": frames_step * world * args.steps / (e_ms / 1e3), "unit": "frames/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": e_ms / args.steps}
+
+    # ---------------- CPU baseline (oracle port, rank 0, N = 1)
+    cpu = None
+    if rank == 0 and world == 1 and not (args.no_cpu or args.profile):
+        n_thr = max(1, min(len(os.sched_getaffinity(0)), utts))
+        wall, nfr, _ = cpu_sample(g, cfg, L1, n_thr, frames)
+        cpu = {"value": nfr / wall, "unit": "frames/s", "cores": n_thr, "kind": "port",
+               "sample": f"{n_thr} utterances x {frames} frames (one full utterance per host "
+                         f"thread) of the same workload, oracle/ C port of decoder.py"}
+
+    if rank == 0:
+        value = frames_step * world * args.steps / (total_ms / 1e3)
+        traffic = None
+        tfile = os.path.join(ROOT, "profiles", "decode_traffic.json")
+        if os.path.exists(tfile):
+            try:
+                with open(tfile) as fh:
+                    traffic = json.load(fh).get(cfg["name"])
+            except Exception:
+                traffic = None
+        line = {
+            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded random graph + posteriors, reference fixture semantics)",
+            "config": {"workload": cfg["name"], "utts_per_gpu": utts, "frames_per_utt": frames,
+                       "graph": {"states": g.num_states, "arcs": g.num_arcs,
+                                 "labels": cfg["labels"]},
+                       "parallelism": f"utterance-sharded x{world}, one persistent kernel/GPU",
+                       "block_threads": block,
+                       "l2": "flushed between timed steps (256 MiB write); cost table 1.5 GB > L2"},
+            "arcs_per_s": relax * world * args.steps / (total_ms / 1e3),
+            "rtf": (total_ms / args.steps / 1e3) / (frames_step * FRAME_SHIFT_S),
+            "rtf_note": "per-GPU batch wall / batch audio at an assumed 10 ms frame shift",
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "decode_kernel", "kernel_ms": avg_kernel_ms,
+                         "algorithmic_bytes": nbytes, "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clocks,
+            "gpu_launches": 2 * args.steps,
+            "counters_per_step": {k: int(res[k].sum()) for k in
+                                  ("n_tok", "a_emit", "a_fin", "e_eps", "n_cand", "n_surv", "n_rec")},
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
