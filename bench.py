@@ -48,6 +48,10 @@ CONFIGS = {
                    "frames, beam 13, max-active 7000, FSD", states=1_000_000, arcs=3_000_000,
               labels=3000, utts=64, frames=1000, beam=13.0, max_active=7000, mode="fsd",
               blank_fraction=0.0, eps=0.015, selfloops=False, final_fraction=0.01),
+    "2s": dict(name="config2-small-graph (L2-resident probe): 30k states/90k arcs/3k pdfs, 64 utt x "
+                    "1000 frames, beam 13, max-active 7000, FSD", states=30_000, arcs=90_000,
+               labels=3000, utts=64, frames=1000, beam=13.0, max_active=7000, mode="fsd",
+               blank_fraction=0.0, eps=0.015, selfloops=False, final_fraction=0.01),
     "4": dict(name="config4: CTC LSD, 5k-label synthetic TLG-like graph (self-loops), 256 utt x "
                    "1500 frames, 80% blank frames, blank-skip threshold 0.98, beam 13, "
                    "max-active 7000", states=100_000, arcs=300_000, labels=5000, utts=256,
@@ -251,9 +255,8 @@ def main():
     fill_inputs(cfg, rank, T, off, L1, costs_h.numpy(), blank_h.numpy())
     dcfg = DecodeConfig(beam=cfg["beam"], max_active=cfg["max_active"], mode=cfg["mode"])
 
-    block = args.block or (1024 if utts <= 148 else 512)
-    dec = BatchDecoder(g, local, max_utts_in_flight=min(utts, 148 * (1024 // block)),
-                       block_threads=block)
+    block = args.block or 512
+    dec = BatchDecoder(g, local, max_utts_in_flight=min(utts, 148), block_threads=block)
     dec.reserve(int(T.sum()) + utts, cfg["max_active"], int(T.max()))
     cap = frames + 64
 
@@ -382,6 +385,10 @@ def main():
             "gpu_launches": 2 * args.steps,
             "counters_per_step": {k: int(res[k].sum()) for k in
                                   ("n_tok", "a_emit", "a_fin", "e_eps", "n_cand", "n_surv", "n_rec")},
+            "phase_share": dict(zip(["stage_row", "expand", "eps_closure", "gather", "select",
+                                     "flags", "compact", "other"],
+                                    [round(float(x), 4) for x in
+                                     res["phase_cycles"].sum(0) / max(1, res["phase_cycles"].sum())])),
         }
         print(json.dumps(line), flush=True)
     if dist is not None:

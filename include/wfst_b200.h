@@ -90,6 +90,11 @@ typedef struct {
     int64_t n_surv;          /* survivors */
     int64_t n_rec;           /* backpointer records written */
     int64_t lat_arcs;        /* raw lattice arcs recorded (lattice mode) */
+    /* SM clock cycles spent per phase (CTA thread 0, measured after each phase barrier):
+     * [0] cost-row staging, [1] emitting expansion, [2] epsilon closure, [3] candidate
+     * gather + min/max, [4] max-active histogram/select, [5] survivor flags + chain marks,
+     * [6] compaction + records + next tokens, [7] utterance prologue/epilogue */
+    int64_t phase_cycles[8];
 } wb_utt_result;
 
 /* Decoder workspace options (0 = automatic). */

@@ -52,7 +52,7 @@ UTT_RESULT_DTYPE = np.dtype([
     ("final_step", np.int32), ("n_olabels", np.int32), ("n_ilabels", np.int32),
     ("status", np.int32), ("best_trace", np.int64), ("n_tok", np.int64), ("a_emit", np.int64),
     ("a_fin", np.int64), ("e_eps", np.int64), ("n_cand", np.int64), ("n_surv", np.int64),
-    ("n_rec", np.int64), ("lat_arcs", np.int64)])
+    ("n_rec", np.int64), ("lat_arcs", np.int64), ("phase_cycles", np.int64, (8,))])
 
 _lib = None
 

@@ -37,8 +37,12 @@ constexpr int GCAP = 1024;           // boundary-bucket members ranked in shared
 constexpr int ROW_SMEM_MAX = 16384;  // cost-row columns staged in shared memory (128 KB)
 constexpr u32 F_SURV = 1u, F_MARK = 2u, CA_NONE = 0xFFFFFFFFu;
 constexpr int MAX_EPS_ROUNDS = 1 << 20;
-constexpr int UNROLL = 4;
-constexpr int GATHER = 4;
+// relaxations in flight per lane (expand) / gathers per thread (prune): halved for 1024-thread
+// CTAs, whose register budget is 64 per thread
+template <int BLOCK> struct Tune {
+    static constexpr int UNROLL = BLOCK >= 1024 ? 2 : 4;
+    static constexpr int GATHER = 4;
+};
 
 struct GraphDev {
     int S, A, start, has_eps;
@@ -92,6 +96,8 @@ struct Smem {
     u64 thr_key;
     u32 thr_state;
     u64 arena_base;
+    long long pc[8];   // phase cycle counters (thread 0)
+    long long t_mark;  // last phase boundary (thread 0)
     union {
         u32 hist[NB];
         struct {
@@ -101,9 +107,40 @@ struct Smem {
     } u;
 };
 
+// Dynamic shared memory: [Smem header | cost row (expansion) / candidate keys + flags (prune)]
+__device__ __forceinline__ unsigned char *dyn_smem() {
+    extern __shared__ __align__(128) unsigned char s_dyn[];
+    return s_dyn;
+}
+template <int BLOCK>
+__host__ __device__ constexpr size_t smem_hdr() { return (sizeof(Smem<BLOCK>) + 127) & ~(size_t)127; }
+template <int BLOCK>
+__device__ __forceinline__ Smem<BLOCK> &SH() { return *reinterpret_cast<Smem<BLOCK> *>(dyn_smem()); }
+template <int BLOCK>
+__device__ __forceinline__ double *s_row() { return reinterpret_cast<double *>(dyn_smem() + smem_hdr<BLOCK>()); }
+template <int BLOCK>
+__device__ __forceinline__ u64 *s_key() { return reinterpret_cast<u64 *>(dyn_smem() + smem_hdr<BLOCK>()); }
+template <int BLOCK>
+__device__ __forceinline__ u32 *s_ca(const WorkDev &ws) {
+    return reinterpret_cast<u32 *>(dyn_smem() + smem_hdr<BLOCK>() + sizeof(u64) * (size_t)ws.smem_cands);
+}
+
+// Phase timing: thread 0 charges the cycles since the previous mark to phase `ph`.  Called
+// right after a barrier, so the time is the CTA's wall time for the phase.
+template <int BLOCK>
+__device__ __forceinline__ void tick(int ph) {
+    Smem<BLOCK> &sh = SH<BLOCK>();
+    if (threadIdx.x == 0) {
+        long long t = clock64();
+        sh.pc[ph] += t - sh.t_mark;
+        sh.t_mark = t;
+    }
+}
+
 // ------------------------------------------------------------------ block primitives
 template <int BLOCK>
-__device__ __forceinline__ void block_minmax(u64 &mn, u64 &mx, Smem<BLOCK> &sh) {
+__device__ __forceinline__ void block_minmax(u64 &mn, u64 &mx) {
+    Smem<BLOCK> &sh = SH<BLOCK>();
     constexpr int NW = BLOCK / 32;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     mn = warp_min_u64(mn);
@@ -123,7 +160,8 @@ __device__ __forceinline__ void block_minmax(u64 &mn, u64 &mx, Smem<BLOCK> &sh) 
 }
 
 template <int BLOCK>
-__device__ __forceinline__ long long block_sum(long long v, Smem<BLOCK> &sh) {
+__device__ __forceinline__ long long block_sum(long long v) {
+    Smem<BLOCK> &sh = SH<BLOCK>();
     constexpr int NW = BLOCK / 32;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     v = warp_sum_ll(v);
@@ -161,135 +199,202 @@ __device__ __forceinline__ int warp_offsets(int v, u32 *buf, int *tot) {
 
 // ------------------------------------------------------------------ per-utterance lane state
 struct Lane {
-    Slot *slot;
-    u32 *cand_of, *qtag;
-    u32 *cand_state, *cand_arc, *cand_pay, *cand_ca;
-    int4 *cand_rng;
-    u64 *cand_key;
-    u32 *front[2];
-    int4 *tok_info[2];
-    double *tok_cost[2];
-    int *frames;
-    const double *row;  // current cost row (shared or global)
-    u64 *s_key;         // shared-memory candidate keys
-    u32 *s_ca;          // shared-memory candidate flags / arena indices
-    u32 tag;
-    long long a_emit, a_fin, e_eps;  // per-thread counters
+    // Stateless accessor: pointers into this CTA's workspace are recomputed from the kernel
+    // parameters on use (constant-bank loads + one IMAD) instead of living in registers or
+    // on the stack across the persistent loop.
+    const WorkDev &ws;
+    __device__ __forceinline__ size_t so() const { return (size_t)blockIdx.x * (size_t)ws.S; }
+    __device__ __forceinline__ size_t co() const { return (size_t)blockIdx.x * (size_t)ws.cap; }
+    __device__ __forceinline__ Slot *slot() const { return ws.slot + so(); }
+    __device__ __forceinline__ u32 *cand_of() const { return ws.cand_of + so(); }
+    __device__ __forceinline__ u32 *qtag() const { return ws.qtag + so(); }
+    __device__ __forceinline__ u32 *cand_state() const { return ws.cand_state + co(); }
+    __device__ __forceinline__ int4 *cand_rng() const { return ws.cand_rng + co(); }
+    __device__ __forceinline__ u32 *cand_arc() const { return ws.cand_arc + co(); }
+    __device__ __forceinline__ u32 *cand_pay() const { return ws.cand_pay + co(); }
+    __device__ __forceinline__ u64 *cand_key() const { return ws.cand_key + co(); }
+    __device__ __forceinline__ u32 *cand_ca() const { return ws.cand_ca + co(); }
+    __device__ __forceinline__ u32 *front(int k) const { return ws.front + 2 * co() + (size_t)k * ws.cap; }
+    __device__ __forceinline__ int4 *tok_info(int k) const {
+        return ws.tok_info + 2 * co() + (size_t)k * ws.cap;
+    }
+    __device__ __forceinline__ double *tok_cost(int k) const {
+        return ws.tok_cost + 2 * co() + (size_t)k * ws.cap;
+    }
+    __device__ __forceinline__ int *frames() const { return ws.frames + (size_t)blockIdx.x * ws.T_cap; }
 };
 
-// First touch of a state in this step: register it as a candidate.  `rng` = the state's
-// {eps_lo, emit_lo, emit_hi} taken from the arc record.  Epsilon graphs: remember the
-// state -> candidate map and, if asked, queue the state for the epsilon closure.
+
+
+// Warp-cooperative candidate registration (call with the whole warp converged).  Lanes with
+// `first` set installed the first entry of state `d` this step; they get consecutive
+// candidate indices from one shared-memory atomic per warp.  `rng` = the state's
+// {eps_lo, emit_lo, emit_hi} from the arc record.  Epsilon graphs: states with epsilon arcs
+// record their candidate index (frontier lookups) and, if `push`, join the frontier.
 template <int BLOCK>
-__device__ __forceinline__ void append_cand(u32 d, int4 rng, const GraphDev &g, const WorkDev &ws,
-                                            Lane &c, Smem<BLOCK> &sh, u32 *front_out,
-                                            bool push_front) {
-    int idx = atomicAdd(&sh.n_cand, 1);
-    if (idx < ws.cap) {
-        c.cand_state[idx] = d;
-        c.cand_rng[idx] = make_int4(rng.x, rng.y, rng.z, 0);
-        if (g.has_eps) {
-            c.cand_of[d] = (u32)idx;
-            if (push_front && rng.x < rng.y) {
-                int f = atomicAdd(&sh.n_front, 1);
-                front_out[f] = d;
+__device__ __forceinline__ void warp_append(bool first, u32 d, int4 rng, bool push,
+                                            const GraphDev &g, const WorkDev &ws,
+                                            u32 *front_out) {
+    Smem<BLOCK> &sh = SH<BLOCK>();
+    const Lane c{ws};
+    const u32 m = __ballot_sync(FULL, first);
+    if (!m) return;
+    const int l = threadIdx.x & 31;
+    const int leader = __ffs(m) - 1;
+    int base = 0;
+    if (l == leader) base = atomicAdd(&sh.n_cand, __popc(m));
+    base = __shfl_sync(FULL, base, leader);
+    const int idx = base + __popc(m & lanemask_lt());
+    bool pf = false;
+    if (first) {
+        if (idx < ws.cap) {
+            c.cand_state()[idx] = d;
+            c.cand_rng()[idx] = make_int4(rng.x, rng.y, rng.z, 0);
+            if (g.has_eps && rng.x < rng.y) {
+                c.cand_of()[d] = (u32)idx;
+                pf = push;
             }
+        } else {
+            sh.overflow = 1;
         }
-    } else {
-        sh.overflow = 1;
+    }
+    if (g.has_eps && push) {
+        const u32 mf = __ballot_sync(FULL, pf);
+        if (mf) {
+            const int lf = __ffs(mf) - 1;
+            int fb = 0;
+            if (l == lf) fb = atomicAdd(&sh.n_front, __popc(mf));
+            fb = __shfl_sync(FULL, fb, lf);
+            if (pf) front_out[fb + __popc(mf & lanemask_lt())] = d;
+        }
     }
 }
 
+// Install `want` in *p under the (cost, arc) total order, optimistic first attempt already
+// made (prev = value returned by a CAS that expected EMPTY).  Returns true if installed;
+// *first = the slot was empty.
+__device__ __forceinline__ bool finish_relax(Slot *p, const Slot &want, Slot prev, bool *first,
+                                             bool *decreased) {
+    if (prev.key == EMPTY_KEY && prev.arcp1 == 0xFFFFFFFFu && prev.pay == 0xFFFFFFFFu) {
+        *first = true;
+        *decreased = true;
+        return true;
+    }
+    *first = false;
+    Slot cs = prev;
+    while (slot_better(want.key, want.arcp1, cs)) {
+        Slot got = cas_slot(p, cs, want);
+        if (got.key == cs.key && got.arcp1 == cs.arcp1 && got.pay == cs.pay) {
+            *decreased = want.key < cs.key;
+            return true;
+        }
+        cs = got;
+    }
+    *decreased = false;
+    return false;
+}
+
 // Emitting expansion of all live tokens (viterbi_step's emitting loop, decoder.py:212-225;
-// parallel form parallel.py:257-283).
+// parallel form parallel.py:257-283).  Per lane, UNROLL relaxations are in flight: their arc
+// loads, then their CAS attempts (optimistically expecting an empty slot -- most relaxations
+// are first touches), are issued back to back.
+struct ExpandCounts {
+    u32 a_emit, a_fin;
+};
+
 template <int BLOCK>
-__device__ void expand_emitting(int n_live, int cur, const GraphDev &g, const WorkDev &ws,
-                                Lane &c, Smem<BLOCK> &sh) {
+__noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const double *row,
+                                                     const GraphDev &g, const WorkDev &ws) {
+    const Lane c{ws};
+    u32 a_emit = 0, a_fin = 0;
     constexpr int NW = BLOCK / 32;
+    constexpr int U = Tune<BLOCK>::UNROLL;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    const int4 *tinfo = c.tok_info[cur];
-    const double *tcost = c.tok_cost[cur];
-    u32 *front0 = c.front[0];
+    const int4 *__restrict__ tinfo = c.tok_info(cur);
+    const double *__restrict__ tcost = c.tok_cost(cur);
+    Slot *slot = c.slot();
+    u32 *front0 = c.front(0);
     const int nchunks = (n_live + 31) >> 5;
+    const Slot empty = {EMPTY_KEY, 0xFFFFFFFFu, 0xFFFFFFFFu};
     for (int ch = w; ch < nchunks; ch += NW) {
         int t = (ch << 5) + l;
         int4 ti = make_int4(0, 0, 0, 0);
         double tc = 0.0;
         if (t < n_live) { ti = tinfo[t]; tc = tcost[t]; }
         int deg = t < n_live ? ti.w - ti.z : 0;
-        c.a_emit += deg;
+        a_emit += deg;
         int incl = warp_incl_scan(deg);
         int total = __shfl_sync(FULL, incl, 31);
         int excl = incl - deg;
-        for (int j0 = 0; j0 < total; j0 += 32 * UNROLL) {
-            int4 rec[UNROLL];
-            double cst[UNROLL];
-            u32 pay[UNROLL];
-            int arc[UNROLL];
-            bool ok[UNROLL];
+        for (int j0 = 0; j0 < total; j0 += 32 * U) {
+            int4 rec[U];
+            Slot want[U];
+            bool act[U];
 #pragma unroll
-            for (int u = 0; u < UNROLL; ++u) {
+            for (int u = 0; u < U; ++u) {
                 int j = j0 + u * 32 + l;
                 int k = warp_owner(excl, j);
                 int lo_k = __shfl_sync(FULL, ti.z, k);
                 int ex_k = __shfl_sync(FULL, excl, k);
-                cst[u] = __shfl_sync(FULL, tc, k);
-                pay[u] = (u32)__shfl_sync(FULL, ti.y, k);
-                ok[u] = j < total;
-                arc[u] = lo_k + j - ex_k;
-                if (ok[u]) rec[u] = __ldg(&g.arcs[2 * arc[u]]);
-            }
-            Slot cur_s[UNROLL];
-            u64 key[UNROLL];
-#pragma unroll
-            for (int u = 0; u < UNROLL; ++u) {
-                if (ok[u]) {
-                    double ac = c.row[rec[u].y];
-                    if (ac == INFINITY) {  // decoder.py:219-220: no relaxation, no record
-                        ok[u] = false;
-                    } else {
-                        double wgt = __hiloint2double(rec[u].w, rec[u].z);
-                        double cc = __dadd_rn(__dadd_rn(cst[u], wgt), ac);
-                        key[u] = cost_key(cc);
-                        cur_s[u] = ld_slot(&c.slot[rec[u].x]);
-                    }
-                }
+                double cst = __shfl_sync(FULL, tc, k);
+                want[u].pay = (u32)__shfl_sync(FULL, ti.y, k);
+                act[u] = j < total;
+                int arc = lo_k + j - ex_k;
+                want[u].arcp1 = (u32)arc + 1u;
+                if (act[u]) rec[u] = __ldg(&g.arcs[2 * arc]);
+                want[u].key = __double_as_longlong(cst);  // carry the token cost
             }
 #pragma unroll
-            for (int u = 0; u < UNROLL; ++u) {
-                if (!ok[u]) continue;
-                c.a_fin++;
-                Slot *p = &c.slot[rec[u].x];
-                Slot want;
-                want.key = key[u];
-                want.arcp1 = (u32)arc[u] + 1u;
-                want.pay = pay[u];
-                Slot cs = cur_s[u];
-                while (slot_better(want.key, want.arcp1, cs)) {
-                    Slot prev = cas_slot(p, cs, want);
-                    if (prev.key == cs.key && prev.arcp1 == cs.arcp1 && prev.pay == cs.pay) {
-                        if (cs.key == EMPTY_KEY) {
-                            int4 r1 = __ldg(&g.arcs[2 * arc[u] + 1]);
-                            append_cand<BLOCK>((u32)rec[u].x, r1, g, ws, c, sh, front0, true);
-                        }
-                        break;
-                    }
-                    cs = prev;
+            for (int u = 0; u < U; ++u) {
+                if (!act[u]) continue;
+                double ac = row[rec[u].y];
+                if (ac == INFINITY) {  // decoder.py:219-220: no relaxation, no record
+                    act[u] = false;
+                    continue;
                 }
+                double wgt = __hiloint2double(rec[u].w, rec[u].z);
+                double cst = __longlong_as_double((long long)want[u].key);
+                want[u].key = cost_key(__dadd_rn(__dadd_rn(cst, wgt), ac));
+            }
+            Slot prev[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (act[u]) prev[u] = cas_slot(&slot[rec[u].x], empty, want[u]);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                bool first = false, dec = false;
+                if (act[u]) {
+                    a_fin++;
+                    finish_relax(&slot[rec[u].x], want[u], prev[u], &first, &dec);
+                }
+                int4 r1 = make_int4(0, 0, 0, 0);
+                if (first) r1 = __ldg(&g.arcs[2 * (want[u].arcp1 - 1u) + 1]);
+                warp_append<BLOCK>(first, (u32)rec[u].x, r1, true, g, ws, front0);
             }
         }
     }
+    return ExpandCounts{a_emit, a_fin};
 }
 
 // Epsilon closure to a fixpoint by frontier rounds (decoder.py:138-171; parallel.py:287-325).
 // Self-loops are skipped (decoder.py:162-163).  An epsilon winner's payload is the candidate
 // index of its source | EPS_BIT.  Frontier entries are states; their candidate index is looked
 // up one round later, after the barrier has published it.
+struct EpsOut {
+    u32 tag, e_eps;
+    int status;
+};
+
 template <int BLOCK>
-__device__ void epsilon_closure(const GraphDev &g, const WorkDev &ws, Lane &c, Smem<BLOCK> &sh,
-                                int &status) {
+__noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev &ws, u32 tag_in) {
+    Smem<BLOCK> &sh = SH<BLOCK>();
+    const Lane c{ws};
+    u32 tag_cur = tag_in, e_eps = 0;
+    int status = WB_OK;
     constexpr int NW = BLOCK / 32;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    Slot *slot = c.slot();
+    const Slot empty = {EMPTY_KEY, 0xFFFFFFFFu, 0xFFFFFFFFu};
     int which = 0;
     int rounds = 0;
     for (;;) {
@@ -299,13 +404,13 @@ __device__ void epsilon_closure(const GraphDev &g, const WorkDev &ws, Lane &c, S
         if (++rounds > MAX_EPS_ROUNDS) { status = WB_ERR_CAPACITY; break; }
         if (threadIdx.x == 0) {
             sh.n_front = 0;
-            sh.tag_round = (int)(c.tag + 1u);
+            sh.tag_round = (int)(tag_cur + 1u);
         }
         __syncthreads();
         const u32 tag = (u32)sh.tag_round;
-        c.tag = tag;
-        const u32 *fin = c.front[which];
-        u32 *fout = c.front[which ^ 1];
+        tag_cur = tag;
+        const u32 *fin = c.front(which);
+        u32 *fout = c.front(which ^ 1);
         const int nchunks = (n_front + 31) >> 5;
         for (int ch = w; ch < nchunks; ch += NW) {
             int i = (ch << 5) + l;
@@ -314,9 +419,9 @@ __device__ void epsilon_closure(const GraphDev &g, const WorkDev &ws, Lane &c, S
             double ucost = 0.0;
             if (i < n_front) {
                 uu = fin[i];
-                ui = c.cand_of[uu];
-                Slot us = ld_slot(&c.slot[uu]);
-                int4 rg = c.cand_rng[ui];
+                Slot us = ld_slot(&slot[uu]);
+                ui = c.cand_of()[uu];
+                int4 rg = c.cand_rng()[ui];
                 lo = rg.x;
                 deg = rg.y - rg.x;
                 ucost = key_cost(us.key);
@@ -332,25 +437,36 @@ __device__ void epsilon_closure(const GraphDev &g, const WorkDev &ws, Lane &c, S
                 double uc_k = __shfl_sync(FULL, ucost, k);
                 u32 u_k = __shfl_sync(FULL, uu, k);
                 u32 ui_k = __shfl_sync(FULL, ui, k);
-                if (j >= total) continue;
+                bool act = j < total;
                 int a = lo_k + j - ex_k;
-                int4 rec = __ldg(&g.arcs[2 * a]);
-                if ((u32)rec.x == u_k) continue;  // a positive self-loop never improves its state
-                c.e_eps++;
-                double wgt = __hiloint2double(rec.w, rec.z);
-                u64 key = cost_key(__dadd_rn(uc_k, wgt));
+                int4 rec = make_int4(0, 0, 0, 0);
+                if (act) {
+                    rec = __ldg(&g.arcs[2 * a]);
+                    if ((u32)rec.x == u_k) act = false;  // a positive self-loop never improves its state
+                }
                 bool first = false, dec = false;
-                if (relax_slot(&c.slot[rec.x], key, (u32)a + 1u, ui_k | EPS_BIT, &first, &dec)) {
-                    int4 r1 = make_int4(0, 0, 0, 0);
-                    if (first) {
-                        r1 = __ldg(&g.arcs[2 * a + 1]);
-                        append_cand<BLOCK>((u32)rec.x, r1, g, ws, c, sh, fout, false);
-                    } else if (dec) {
-                        r1 = __ldg(&g.arcs[2 * a + 1]);
-                    }
-                    if ((first || dec) && r1.x < r1.y &&
-                        atomicExch(&c.qtag[rec.x], tag) != tag) {
-                        int f = atomicAdd(&sh.n_front, 1);
+                if (act) {
+                    e_eps++;
+                    Slot want;
+                    want.key = cost_key(__dadd_rn(uc_k, __hiloint2double(rec.w, rec.z)));
+                    want.arcp1 = (u32)a + 1u;
+                    want.pay = ui_k | EPS_BIT;
+                    Slot prev = cas_slot(&slot[rec.x], empty, want);
+                    finish_relax(&slot[rec.x], want, prev, &first, &dec);
+                }
+                int4 r1 = make_int4(0, 0, 0, 0);
+                if (dec) r1 = __ldg(&g.arcs[2 * a + 1]);
+                warp_append<BLOCK>(first, (u32)rec.x, r1, false, g, ws, fout);
+                // states whose cost dropped (or that are new) re-relax their epsilon arcs
+                bool push = dec && r1.x < r1.y && atomicExch(&c.qtag()[rec.x], tag) != tag;
+                const u32 mp = __ballot_sync(FULL, push);
+                if (mp) {
+                    const int lp = __ffs(mp) - 1;
+                    int fb = 0;
+                    if (l == lp) fb = atomicAdd(&sh.n_front, __popc(mp));
+                    fb = __shfl_sync(FULL, fb, lp);
+                    int f = fb + __popc(mp & lanemask_lt());
+                    if (push) {
                         if (f < ws.cap) fout[f] = (u32)rec.x;
                         else sh.overflow = 1;
                     }
@@ -360,6 +476,7 @@ __device__ void epsilon_closure(const GraphDev &g, const WorkDev &ws, Lane &c, S
         __syncthreads();
         which ^= 1;
     }
+    return EpsOut{tag_cur, e_eps, status};
 }
 
 __device__ __forceinline__ int bucket_of(double cst, double best, double scale) {
@@ -371,8 +488,10 @@ __device__ __forceinline__ int bucket_of(double cst, double best, double scale) 
 // Exact max-active cut: K* = the max_active-th smallest (cost, state) among kept candidates
 // (decoder.py:188-191).  Expects sh.u.hist filled; sets sh.thr_bucket / thr_key / thr_state.
 template <int BLOCK>
-__device__ void select_threshold(int n_cand, int max_active, double best, double cutoff,
-                                 double scale, const u64 *ckey, Lane &c, Smem<BLOCK> &sh) {
+__noinline__ __device__ void select_threshold(int n_cand, int max_active, double best, double cutoff,
+                                 double scale, const u64 *ckey, const WorkDev &ws) {
+    Smem<BLOCK> &sh = SH<BLOCK>();
+    const Lane c{ws};
     constexpr int PER = NB / BLOCK;
     u32 loc[PER];
     u32 s = 0;
@@ -413,7 +532,7 @@ __device__ void select_threshold(int n_cand, int max_active, double best, double
             if (cst <= cutoff && bucket_of(cst, best, scale) == bstar) {
                 int j = atomicAdd(&sh.ng, 1);
                 sh.u.g.key[j] = k;
-                sh.u.g.st[j] = c.cand_state[i];
+                sh.u.g.st[j] = c.cand_state()[i];
             }
         }
         __syncthreads();
@@ -443,7 +562,7 @@ __device__ void select_threshold(int n_cand, int max_active, double best, double
             u64 k = ckey[i];
             double cst = key_cost(k);
             if (!(cst <= cutoff) || bucket_of(cst, best, scale) != bstar) continue;
-            u32 st = c.cand_state[i];
+            u32 st = c.cand_state()[i];
             if ((k & kmask) != kpre || (st & smask) != spre) continue;
             u32 d = in_key ? (u32)((k >> shift) & 0xFF) : ((st >> shift) & 0xFF);
             atomicAdd(&sh.u.hist[d], 1u);
@@ -472,47 +591,54 @@ __device__ void select_threshold(int n_cand, int max_active, double best, double
 
 // Finish a step: gather candidates, beam/max-active prune, backpointer records, next tokens.
 // Returns the number of survivors (0 = search death).
+struct StepOut {
+    int n_surv, n_keep, status;
+};
+
 template <int BLOCK>
-__device__ int finish_step(int nxt, const GraphDev &g, const WorkDev &ws, const CfgDev &cfg,
-                           Lane &c, Smem<BLOCK> &sh, int &status, long long &n_rec) {
+__noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const WorkDev &ws,
+                                            const CfgDev &cfg) {
+    Smem<BLOCK> &sh = SH<BLOCK>();
+    const Lane c{ws};
     const int n_cand = min(sh.n_cand, ws.cap);
-    if (sh.overflow) status = WB_ERR_CAPACITY;
+    int status = sh.overflow ? WB_ERR_CAPACITY : WB_OK;
     const bool in_smem = n_cand <= ws.smem_cands;
-    u64 *ckey = in_smem ? c.s_key : c.cand_key;
-    u32 *ca = in_smem ? c.s_ca : c.cand_ca;
+    u64 *ckey = in_smem ? s_key<BLOCK>() : c.cand_key();
+    u32 *ca = in_smem ? s_ca<BLOCK>(ws) : c.cand_ca();
     volatile u32 *vca = ca;
 
     // P1: gather slot contents (batched loads), reset slots, min / max
     u64 mn = EMPTY_KEY, mx = 0;
-    for (int i0 = threadIdx.x; i0 < n_cand; i0 += BLOCK * GATHER) {
-        u32 st[GATHER];
-        Slot v[GATHER];
+    for (int i0 = threadIdx.x; i0 < n_cand; i0 += BLOCK * Tune<BLOCK>::GATHER) {
+        u32 st[Tune<BLOCK>::GATHER];
+        Slot v[Tune<BLOCK>::GATHER];
 #pragma unroll
-        for (int q = 0; q < GATHER; ++q) {
+        for (int q = 0; q < Tune<BLOCK>::GATHER; ++q) {
             int i = i0 + q * BLOCK;
-            if (i < n_cand) st[q] = c.cand_state[i];
+            if (i < n_cand) st[q] = c.cand_state()[i];
         }
 #pragma unroll
-        for (int q = 0; q < GATHER; ++q) {
+        for (int q = 0; q < Tune<BLOCK>::GATHER; ++q) {
             int i = i0 + q * BLOCK;
-            if (i < n_cand) v[q] = ld_slot(&c.slot[st[q]]);
+            if (i < n_cand) v[q] = ld_slot(&c.slot()[st[q]]);
         }
 #pragma unroll
-        for (int q = 0; q < GATHER; ++q) {
+        for (int q = 0; q < Tune<BLOCK>::GATHER; ++q) {
             int i = i0 + q * BLOCK;
             if (i < n_cand) {
                 ckey[i] = v[q].key;
-                c.cand_arc[i] = v[q].arcp1;
-                c.cand_pay[i] = v[q].pay;
+                c.cand_arc()[i] = v[q].arcp1;
+                c.cand_pay()[i] = v[q].pay;
                 ca[i] = 0u;
-                st_slot_empty(&c.slot[st[q]]);
+                st_slot_empty(&c.slot()[st[q]]);
                 mn = v[q].key < mn ? v[q].key : mn;
                 mx = v[q].key > mx ? v[q].key : mx;
             }
         }
     }
-    block_minmax<BLOCK>(mn, mx, sh);
-    if (n_cand == 0) return 0;
+    block_minmax<BLOCK>(mn, mx);
+    tick<BLOCK>(3);
+    if (n_cand == 0) return StepOut{0, 0, status};
     const double best = key_cost(mn);
     const double cutoff = __dadd_rn(best, cfg.beam);  // cutoff = best + beam (decoder.py:186)
 
@@ -534,11 +660,12 @@ __device__ int finish_step(int nxt, const GraphDev &g, const WorkDev &ws, const 
                 atomicAdd(&sh.u.hist[bucket_of(cst, best, scale)], 1u);
             }
         }
-        kept = block_sum<BLOCK>(kept, sh);
+        kept = block_sum<BLOCK>(kept);
         need_select = kept > cfg.max_active;
         if (need_select)
-            select_threshold<BLOCK>(n_cand, cfg.max_active, best, cutoff, scale, ckey, c, sh);
+            select_threshold<BLOCK>(n_cand, cfg.max_active, best, cutoff, scale, ckey, ws);
     }
+    tick<BLOCK>(4);
     const int bstar = need_select ? sh.thr_bucket : 0;
     const u64 tkey = need_select ? sh.thr_key : 0;
     const u32 tst = need_select ? sh.thr_state : 0;
@@ -551,14 +678,14 @@ __device__ int finish_step(int nxt, const GraphDev &g, const WorkDev &ws, const 
         if (surv && need_select) {
             int b = bucket_of(cst, best, scale);
             surv = b < bstar ||
-                   (b == bstar && (k < tkey || (k == tkey && c.cand_state[i] <= tst)));
+                   (b == bstar && (k < tkey || (k == tkey && c.cand_state()[i] <= tst)));
         }
         if (!surv) continue;
         atomicOr(&ca[i], F_SURV);
         if (!g.has_eps) continue;
         int v = i;
         for (;;) {
-            u32 a = c.cand_arc[v], p = c.cand_pay[v];
+            u32 a = c.cand_arc()[v], p = c.cand_pay()[v];
             if (a == 0u || !(p & EPS_BIT)) break;
             int uix = (int)(p & ~EPS_BIT);
             u32 old = atomicOr(&ca[uix], F_MARK);
@@ -567,6 +694,7 @@ __device__ int finish_step(int nxt, const GraphDev &g, const WorkDev &ws, const 
         }
     }
     __syncthreads();
+    tick<BLOCK>(5);
 
     // P4: order-preserving compaction of kept candidates (arena records) and survivors
     // (next tokens).  Warps own contiguous segments; ballots count; one scan.
@@ -598,12 +726,14 @@ __device__ int finish_step(int nxt, const GraphDev &g, const WorkDev &ws, const 
     }
     __syncthreads();
     const int n_keep = (int)sh.wa[NW], n_surv = (int)sh.wb[NW];
-    if (sh.overflow == 2) { status = WB_ERR_CAPACITY; __syncthreads(); return 0; }
+    if (sh.overflow == 2) { __syncthreads(); return StepOut{0, 0, WB_ERR_CAPACITY}; }
     const u64 base = sh.arena_base;
-    int4 *tinfo = c.tok_info[nxt];
-    double *tcost = c.tok_cost[nxt];
-    u32 *pend = c.front[0];
+    int4 *tinfo = c.tok_info(nxt);
+    double *tcost = c.tok_cost(nxt);
+    u32 *pend = c.front(0);
+    u32 *tokidx = c.front(1);  // survivor -> next-token slot (frontier buffers are free here)
     {
+        // E1: indices from the shared-memory flags only (ballot ranks within warp segments)
         int ra = (int)sh.wa[w], rb = (int)sh.wb[w];
         const u32 lt = lanemask_lt();
         for (int i0 = lo; i0 < hi; i0 += 32) {
@@ -612,46 +742,73 @@ __device__ int finish_step(int nxt, const GraphDev &g, const WorkDev &ws, const 
             bool keep = f != 0u, surv = (f & F_SURV) != 0u;
             u32 mk = __ballot_sync(FULL, keep), ms = __ballot_sync(FULL, surv);
             if (i < hi) {
-                u32 rec = keep ? (u32)(base + (u64)(ra + __popc(mk & lt))) : CA_NONE;
-                ca[i] = rec;
-                if (surv) {
-                    int j = rb + __popc(ms & lt);
-                    int4 rg = c.cand_rng[i];
-                    tinfo[j] = make_int4((int)c.cand_state[i], (int)rec, rg.y, rg.z);
-                    tcost[j] = key_cost(ckey[i]);
-                }
-                if (keep) {
-                    u32 a = c.cand_arc[i], p = c.cand_pay[i];
-                    if (a != 0u && (p & EPS_BIT)) {
-                        int q = atomicAdd(&sh.n_pend, 1);
-                        pend[q] = (u32)i;  // epsilon winner: needs its source's record index
-                    } else {
-                        u32 prev = a == 0u ? ROOT_PREV : p;
-                        ws.arena[rec] = (u64)a | ((u64)prev << 32);
-                    }
-                }
+                ca[i] = keep ? (u32)(base + (u64)(ra + __popc(mk & lt))) : CA_NONE;
+                tokidx[i] = surv ? (u32)(rb + __popc(ms & lt)) : CA_NONE;
             }
             ra += __popc(mk);
             rb += __popc(ms);
         }
     }
     __syncthreads();
+    {
+        // E2: records + next tokens, G candidates per thread with their loads in flight
+        constexpr int G = Tune<BLOCK>::GATHER;
+        const u32 *__restrict__ cst_ = c.cand_state();
+        const int4 *__restrict__ rng_ = c.cand_rng();
+        const u32 *__restrict__ arc_ = c.cand_arc();
+        const u32 *__restrict__ pay_ = c.cand_pay();
+        for (int i0 = threadIdx.x; i0 < n_cand; i0 += BLOCK * G) {
+            u32 rec[G], tj[G], a[G], p[G];
+#pragma unroll
+            for (int q = 0; q < G; ++q) {
+                int i = i0 + q * BLOCK;
+                rec[q] = CA_NONE;
+                tj[q] = CA_NONE;
+                if (i < n_cand) {
+                    rec[q] = vca[i];
+                    tj[q] = tokidx[i];
+                    a[q] = arc_[i];
+                    p[q] = pay_[i];
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < G; ++q) {
+                int i = i0 + q * BLOCK;
+                if (tj[q] != CA_NONE) {
+                    int4 rg = rng_[i];
+                    tinfo[tj[q]] = make_int4((int)cst_[i], (int)rec[q], rg.y, rg.z);
+                    tcost[tj[q]] = key_cost(ckey[i]);
+                }
+                if (rec[q] != CA_NONE) {
+                    if (a[q] != 0u && (p[q] & EPS_BIT)) {
+                        int qq = atomicAdd(&sh.n_pend, 1);
+                        pend[qq] = (u32)i;  // epsilon winner: needs its source's record index
+                    } else {
+                        u32 prev = a[q] == 0u ? ROOT_PREV : p[q];
+                        ws.arena[rec[q]] = (u64)a[q] | ((u64)prev << 32);
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
     const int n_pend = sh.n_pend;
     for (int q = threadIdx.x; q < n_pend; q += BLOCK) {
         int i = (int)pend[q];
-        u32 a = c.cand_arc[i], p = c.cand_pay[i];
+        u32 a = c.cand_arc()[i], p = c.cand_pay()[i];
         ws.arena[vca[i]] = (u64)a | ((u64)vca[p & ~EPS_BIT] << 32);
     }
-    n_rec += n_keep;
     __syncthreads();
-    return n_surv;
+    tick<BLOCK>(6);
+    return StepOut{n_surv, n_keep, status};
 }
 
 // LSD pre-pass (classify_blank_frames + nonblank_frames, posteriors.py:116-125,109-110): a
 // frame is blank iff its blank probability strictly exceeds the threshold; non-blank frame
 // ids are compacted in order.
 template <int BLOCK>
-__device__ int lsd_prepass(const double *bl, int T, double thr, int *fr, Smem<BLOCK> &sh) {
+__device__ int lsd_prepass(const double *bl, int T, double thr, int *fr) {
+    Smem<BLOCK> &sh = SH<BLOCK>();
     constexpr int NW = BLOCK / 32;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     const int seg = ((T + NW - 1) / NW + 31) & ~31;
@@ -677,7 +834,8 @@ __device__ int lsd_prepass(const double *bl, int T, double thr, int *fr, Smem<BL
 
 // argmin over tokens by (key, state); returns the token index (-1 if none)
 template <int BLOCK>
-__device__ int block_argmin_tok(u64 key, u32 st, int idx, Smem<BLOCK> &sh) {
+__device__ int block_argmin_tok(u64 key, u32 st, int idx) {
+    Smem<BLOCK> &sh = SH<BLOCK>();
     constexpr int NW = BLOCK / 32;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
 #pragma unroll
@@ -709,44 +867,28 @@ __device__ int block_argmin_tok(u64 key, u32 st, int idx, Smem<BLOCK> &sh) {
 }
 
 template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
-decode_kernel(GraphDev g, WorkDev ws, BatchDev b, CfgDev cfg, wb_utt_result *res) {
-    extern __shared__ __align__(16) unsigned char s_dyn[];
-    __shared__ Smem<BLOCK> sh;
+__global__ void __launch_bounds__(BLOCK, 1)
+decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDev ws,
+              const __grid_constant__ BatchDev b, const __grid_constant__ CfgDev cfg,
+              wb_utt_result *res) {
+    Smem<BLOCK> &sh = SH<BLOCK>();
+    const Lane c{ws};
     const int slot_id = blockIdx.x;
-    const size_t S = (size_t)ws.S, cap = (size_t)ws.cap;
-    Lane c;
-    c.slot = ws.slot + slot_id * S;
-    c.cand_of = ws.cand_of + slot_id * S;
-    c.qtag = ws.qtag + slot_id * S;
-    c.cand_state = ws.cand_state + slot_id * cap;
-    c.cand_rng = ws.cand_rng + slot_id * cap;
-    c.cand_arc = ws.cand_arc + slot_id * cap;
-    c.cand_pay = ws.cand_pay + slot_id * cap;
-    c.cand_key = ws.cand_key + slot_id * cap;
-    c.cand_ca = ws.cand_ca + slot_id * cap;
-    c.front[0] = ws.front + (size_t)slot_id * 2 * cap;
-    c.front[1] = c.front[0] + cap;
-    c.tok_info[0] = ws.tok_info + (size_t)slot_id * 2 * cap;
-    c.tok_info[1] = c.tok_info[0] + cap;
-    c.tok_cost[0] = ws.tok_cost + (size_t)slot_id * 2 * cap;
-    c.tok_cost[1] = c.tok_cost[0] + cap;
-    c.frames = ws.frames + (size_t)slot_id * ws.T_cap;
-    c.s_key = reinterpret_cast<u64 *>(s_dyn);
-    c.s_ca = reinterpret_cast<u32 *>(s_dyn + sizeof(u64) * (size_t)ws.smem_cands);
-    c.tag = ws.tag_ctr[slot_id];
+    u32 tag = ws.tag_ctr[slot_id];
     const bool row_in_smem = ws.row_in_smem != 0;
-    double *s_row = reinterpret_cast<double *>(s_dyn);
+    double *srow = s_row<BLOCK>();
 
     for (;;) {
         if (threadIdx.x == 0) sh.utt = (int)atomicAdd(ws.utt_ctr, 1u);
         __syncthreads();
         const int u = sh.utt;
         if (u >= b.n) break;
+        if (threadIdx.x < 8) sh.pc[threadIdx.x] = 0;
+        if (threadIdx.x == 0) sh.t_mark = clock64();
         const int T = b.T[u];
         const long long row0 = b.row_off[u];
         int status = WB_OK;
-        c.a_emit = c.a_fin = c.e_eps = 0;
+        u32 a_emit = 0, a_fin = 0, e_eps = 0;  // per-thread counters
         long long n_tok = 0, n_cand_tot = 0, n_surv_tot = 0, n_rec = 0;
         int nf = T;
         if (cfg.mode == 1) {
@@ -754,64 +896,83 @@ decode_kernel(GraphDev g, WorkDev ws, BatchDev b, CfgDev cfg, wb_utt_result *res
                 status = WB_ERR_CAPACITY;
                 nf = 0;
             } else {
-                nf = lsd_prepass<BLOCK>(b.blank + row0, T, cfg.thr, c.frames, sh);
+                nf = lsd_prepass<BLOCK>(b.blank + row0, T, cfg.thr, c.frames());
             }
         }
 
         // ---- initial tokens: start entry + epsilon closure + prune (decoder.py:236-249)
         if (threadIdx.x == 0) {
             u64 k0 = cost_key(0.0);
-            __stcg(reinterpret_cast<ulonglong2 *>(&c.slot[g.start]),
+            __stcg(reinterpret_cast<ulonglong2 *>(&c.slot()[g.start]),
                    make_ulonglong2(k0, (u64)0u | ((u64)ROOT_PREV << 32)));
-            c.cand_state[0] = (u32)g.start;
-            c.cand_rng[0] = g.start_rng;
-            if (g.has_eps) c.cand_of[g.start] = 0u;
+            c.cand_state()[0] = (u32)g.start;
+            c.cand_rng()[0] = g.start_rng;
+            if (g.has_eps) c.cand_of()[g.start] = 0u;
             sh.n_cand = 1;
             sh.overflow = 0;
             sh.n_front = 0;
             if (g.has_eps && g.start_rng.x < g.start_rng.y) {
-                c.front[0][0] = (u32)g.start;
+                c.front(0)[0] = (u32)g.start;
                 sh.n_front = 1;
             }
         }
         __syncthreads();
-        if (g.has_eps) epsilon_closure<BLOCK>(g, ws, c, sh, status);
+        if (g.has_eps) {
+            EpsOut eo = epsilon_closure<BLOCK>(g, ws, tag);
+            tag = eo.tag;
+            e_eps += eo.e_eps;
+            if (eo.status) status = eo.status;
+        }
         n_cand_tot += min(sh.n_cand, ws.cap);
         int cur = 0;
-        int n_live = finish_step<BLOCK>(cur, g, ws, cfg, c, sh, status, n_rec);
+        StepOut so = finish_step<BLOCK>(cur, g, ws, cfg);
+        if (so.status) status = so.status;
+        n_rec += so.n_keep;
+        int n_live = so.n_surv;
         n_surv_tot += n_live;
         int steps_run = 0, died_at = -1;
         long long expanded = 0;
         for (int s = 0; s < nf && status == WB_OK; ++s) {
-            const int f = cfg.mode == 1 ? c.frames[s] : s;
+            const int f = cfg.mode == 1 ? c.frames()[s] : s;
             const double *grow = b.costs + (size_t)(row0 + f) * b.L1;
+            const double *row = grow;
             if (row_in_smem) {
-                for (int q = threadIdx.x; q < b.L1; q += BLOCK) s_row[q] = __ldg(&grow[q]);
-                c.row = s_row;
-            } else {
-                c.row = grow;
+                for (int q = threadIdx.x; q < b.L1; q += BLOCK) srow[q] = __ldg(&grow[q]);
+                row = srow;
             }
             if (threadIdx.x == 0) { sh.n_cand = 0; sh.n_front = 0; sh.overflow = 0; }
             __syncthreads();
+            tick<BLOCK>(0);
             expanded += n_live;
             n_tok += n_live;
-            expand_emitting<BLOCK>(n_live, cur, g, ws, c, sh);
+            ExpandCounts ec = expand_emitting<BLOCK>(n_live, cur, row, g, ws);
+            a_emit += ec.a_emit;
+            a_fin += ec.a_fin;
             __syncthreads();
-            if (g.has_eps) epsilon_closure<BLOCK>(g, ws, c, sh, status);
+            tick<BLOCK>(1);
+            if (g.has_eps) {
+                EpsOut eo = epsilon_closure<BLOCK>(g, ws, tag);
+                tag = eo.tag;
+                e_eps += eo.e_eps;
+                if (eo.status) status = eo.status;
+            }
+            tick<BLOCK>(2);
             n_cand_tot += min(sh.n_cand, ws.cap);
-            int m = finish_step<BLOCK>(cur ^ 1, g, ws, cfg, c, sh, status, n_rec);
+            so = finish_step<BLOCK>(cur ^ 1, g, ws, cfg);
+            if (so.status) status = so.status;
+            n_rec += so.n_keep;
             steps_run++;
-            if (m == 0) {
+            if (so.n_surv == 0) {
                 died_at = s;
                 break;
             }
-            n_surv_tot += m;
+            n_surv_tot += so.n_surv;
             cur ^= 1;
-            n_live = m;
+            n_live = so.n_surv;
         }
         // ---- final transition / death fallback (decoder.py:252-273, 327-333)
-        const int4 *tinfo = c.tok_info[cur];
-        const double *tcost = c.tok_cost[cur];
+        const int4 *tinfo = c.tok_info(cur);
+        const double *tcost = c.tok_cost(cur);
         int best_t = -1;
         int reached = 0;
         double best_cost = 0.0;
@@ -826,7 +987,7 @@ decode_kernel(GraphDev g, WorkDev ws, BatchDev b, CfgDev cfg, wb_utt_result *res
                 u64 kk = cost_key(__dadd_rn(tcost[t], fw));
                 if (kk < k || (kk == k && (u32)s < st)) { k = kk; st = (u32)s; idx = t; }
             }
-            best_t = block_argmin_tok<BLOCK>(k, st, idx, sh);
+            best_t = block_argmin_tok<BLOCK>(k, st, idx);
             if (best_t >= 0) {
                 reached = 1;
                 best_cost = __dadd_rn(tcost[best_t], __ldg(&g.final_w[tinfo[best_t].x]));
@@ -841,15 +1002,17 @@ decode_kernel(GraphDev g, WorkDev ws, BatchDev b, CfgDev cfg, wb_utt_result *res
                 u32 s = (u32)tinfo[t].x;
                 if (kk < k || (kk == k && s < st)) { k = kk; st = s; idx = t; }
             }
-            best_t = block_argmin_tok<BLOCK>(k, st, idx, sh);
+            best_t = block_argmin_tok<BLOCK>(k, st, idx);
             if (best_t >= 0) best_cost = tcost[best_t];
         }
-        long long a_emit = block_sum<BLOCK>(c.a_emit, sh);
-        long long a_fin = block_sum<BLOCK>(c.a_fin, sh);
-        long long e_eps = block_sum<BLOCK>(c.e_eps, sh);
+        long long t_emit = block_sum<BLOCK>(a_emit);
+        long long t_fin = block_sum<BLOCK>(a_fin);
+        long long t_eps = block_sum<BLOCK>(e_eps);
+        tick<BLOCK>(7);
         if (threadIdx.x == 0) {
             wb_utt_result r;
             memset(&r, 0, sizeof(r));
+            for (int q = 0; q < 8; ++q) r.phase_cycles[q] = sh.pc[q];
             r.total_cost = best_cost;
             r.tokens_expanded = expanded;
             r.search_steps = steps_run;
@@ -860,9 +1023,9 @@ decode_kernel(GraphDev g, WorkDev ws, BatchDev b, CfgDev cfg, wb_utt_result *res
             r.status = status;
             r.best_trace = best_t >= 0 ? (long long)(u32)tinfo[best_t].y : -1;
             r.n_tok = n_tok;
-            r.a_emit = a_emit;
-            r.a_fin = a_fin;
-            r.e_eps = e_eps;
+            r.a_emit = t_emit;
+            r.a_fin = t_fin;
+            r.e_eps = t_eps;
             r.n_cand = n_cand_tot;
             r.n_surv = n_surv_tot;
             r.n_rec = n_rec;
@@ -870,7 +1033,7 @@ decode_kernel(GraphDev g, WorkDev ws, BatchDev b, CfgDev cfg, wb_utt_result *res
         }
         __syncthreads();
     }
-    if (threadIdx.x == 0) ws.tag_ctr[slot_id] = c.tag;
+    if (threadIdx.x == 0) ws.tag_ctr[slot_id] = tag;
 }
 
 // Backtrace (decoder.py:276-291): one thread per utterance walks the arena from the winner;

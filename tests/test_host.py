@@ -1,0 +1,143 @@
+"""Host-side logic (CPU-only): graph layout, cost table, epsilon-cycle validation, config
+validation, synthetic generators, API error behaviour before any device call."""
+import dataclasses
+import math
+import random
+
+import numpy as np
+import pytest
+
+import refutil
+from paper_1808_00687_b200 import synth
+from paper_1808_00687_b200.decoder import DecodeConfig
+from paper_1808_00687_b200.posteriors import PosteriorMatrix, cost_table, frame_costs
+from paper_1808_00687_b200.wfst import Arc, Wfst, WfstError, parse_wfst_text, validate_epsilon_acyclic
+
+needs_ref = pytest.mark.skipif(not refutil.HAVE_REF, reason="reference not present")
+
+
+@needs_ref
+def test_wfst_layout_matches_reference():
+    """Arc order, arc_offsets, eps_split, final weights (wfst.py:182-198)."""
+    L = refutil.ref()
+    for seed in range(60):
+        rng = random.Random(seed)
+        w = L.fixtures.make_random_wfst(rng, rng.randrange(2, 40), rng.randrange(1, 120),
+                                        rng.randrange(1, 6), eps_fraction=0.3,
+                                        selfloops=seed % 2 == 0,
+                                        weight_grid=[0.0, 0.5] if seed % 5 == 0 else None)
+        arcs = [Arc(a.src, a.dst, a.ilabel, a.olabel, a.weight) for a in w.arcs]
+        random.Random(seed + 1).shuffle(arcs)
+        g = Wfst(w.num_states, w.start, arcs, w.final_weights)
+        assert [(a.src, a.dst, a.ilabel, a.olabel, a.weight) for a in g.arcs] == \
+               [(a.src, a.dst, a.ilabel, a.olabel, a.weight) for a in w.arcs]
+        assert g.arc_offsets == w.arc_offsets
+        assert g.eps_split == w.eps_split
+        assert g.final_weights == w.final_weights
+        assert g.has_epsilon_arcs == w.has_epsilon_arcs
+
+
+@needs_ref
+def test_cost_table_bit_exact_vs_frame_costs():
+    """The vectorised (and thread-blocked) table equals frame_costs row by row, bit for bit."""
+    L = refutil.ref()
+    for seed in range(20):
+        rng = random.Random(seed)
+        labels = rng.randrange(1, 80)
+        p = L.fixtures.make_random_posteriors(rng, rng.randrange(0, 40), labels,
+                                              blank_fraction=0.3, blank_col=seed % (labels + 1))
+        mine = PosteriorMatrix(p.rows, p.blank_col)
+        for scale in (1.0, 0.7):
+            t = cost_table(mine, scale)
+            for f in range(p.num_frames):
+                ref = L.posteriors.frame_costs(p, f, scale)
+                assert t[f].tobytes() == np.asarray(ref).tobytes()
+
+
+def test_cost_table_large_threaded_equals_rowwise():
+    rows = synth.random_posterior_rows(3, 700, 3000, blank_fraction=0.2)
+    p = PosteriorMatrix(rows, 0, validate=False)
+    t = cost_table(p)
+    for f in (0, 1, 350, 699):
+        assert t[f].tobytes() == np.asarray(frame_costs(p, f)).tobytes()
+
+
+def test_zero_probability_is_infinite_cost():
+    p = PosteriorMatrix(np.array([[0.5, 0.5, 0.0], [1.0, 0.0, 0.0]]), 0)
+    t = cost_table(p)
+    assert math.isinf(t[0, 2]) and math.isinf(t[1, 1]) and math.isinf(t[0, 0])
+    assert t[1, 1] > 0
+
+
+@needs_ref
+def test_epsilon_cycle_detection_matches_reference():
+    L = refutil.ref()
+    texts = ["0 1 0 0 0.0\n1 0 0 0 0.0\n0 2 1 1 0.5\n2 0.0",      # zero-weight cycle
+             "0 1 0 0 0.5\n1 0 0 0 0.5\n0 2 1 1 0.5\n2 0.0",      # positive cycle: accepted
+             "0 0 0 0 0.0\n0 1 1 1 1\n1",                          # zero self-loop
+             "0 0 0 0 0.3\n0 1 1 1 1\n1",                          # positive self-loop
+             "0 1 1 1 0.5\n1 0.0"]
+    for t in texts:
+        ref = L.wfst.parse_wfst_text(t).epsilon_cycle()
+        mine = parse_wfst_text(t).epsilon_cycle()
+        assert (ref is None) == (mine is None), t
+        if ref is not None:
+            assert mine.total_weight == ref.total_weight
+    for t in ["0 1 0 0 -1.0\n1 0 0 0 0.5\n0 2 1 1 0.5\n2 0.0"]:
+        ref = L.wfst.parse_wfst_text(t, allow_negative_weights=True).epsilon_cycle()
+        mine = parse_wfst_text(t, allow_negative_weights=True).epsilon_cycle()
+        assert (ref is None) == (mine is None)
+
+
+def test_epsilon_validation_fast_path_on_large_graph():
+    g = synth.random_wfst(1, 200_000, 600_000, 100, eps_fraction=0.05)
+    assert validate_epsilon_acyclic(g) is None
+
+
+def test_decode_config_validation():
+    with pytest.raises(ValueError):
+        DecodeConfig(beam=-1.0)
+    with pytest.raises(ValueError):
+        DecodeConfig(max_active=0)
+    with pytest.raises(ValueError):
+        DecodeConfig(acoustic_scale=0.0)
+    with pytest.raises(ValueError):
+        DecodeConfig(mode="nonsense")
+
+
+def test_api_errors_raise_before_device_work():
+    """WfstError for a non-positive epsilon cycle, ValueError for an alphabet mismatch
+    (decoder.py:304-308, 294-299) -- raised on the host, like the reference."""
+    import paper_1808_00687_b200 as P
+    w = parse_wfst_text("0 1 0 0 0.0\n1 0 0 0 0.0\n0 2 1 1 0.5\n2 0.0")
+    p = PosteriorMatrix(np.array([[0.1, 0.9]]), 0)
+    with pytest.raises(WfstError):
+        P.decode_fsd(w, p, DecodeConfig(mode="fsd"))
+    w2 = parse_wfst_text("0 1 7 7 0.5\n1 0.0")
+    with pytest.raises(ValueError):
+        P.decode_fsd(w2, PosteriorMatrix(np.array([[0.1, 0.45, 0.45]]), 0), DecodeConfig(mode="fsd"))
+    with pytest.raises(ValueError):
+        P.parallel_decode(w2, p, DecodeConfig(), workers=0)
+
+
+def test_synth_generators_deterministic_and_well_formed():
+    a = synth.random_wfst(5, 1000, 4000, 20, eps_fraction=0.1, selfloops=True)
+    b = synth.random_wfst(5, 1000, 4000, 20, eps_fraction=0.1, selfloops=True)
+    for f in ("row_ptr", "eps_end", "dst", "ilabel", "olabel", "weight", "final_w"):
+        assert np.array_equal(getattr(a, f), getattr(b, f))
+    assert a.num_arcs == 4000 and validate_epsilon_acyclic(a) is None
+    eps = a.ilabel == 0
+    assert (a.src[eps] < a.dst[eps]).all()           # forward-only epsilon arcs
+    rows = synth.random_posterior_rows(1, 500, 30, blank_fraction=0.4)
+    assert np.allclose(rows.sum(1), 1.0) and (rows > 0).all()
+    assert int((rows[:, 0] > 0.98).sum()) == 200
+
+
+@needs_ref
+def test_reference_graph_conversion_roundtrip():
+    L = refutil.ref()
+    from paper_1808_00687_b200.decoder import as_wfst
+    w, _ = refutil.random_instance(3)
+    g = as_wfst(w)
+    assert as_wfst(w) is g
+    assert g.arc_offsets == w.arc_offsets and g.eps_split == w.eps_split
