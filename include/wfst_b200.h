@@ -105,6 +105,7 @@ typedef struct {
     int32_t max_frames;          /* longest utterance a call may contain */
     int32_t block_threads;       /* 256, 512 or 1024 */
     int64_t lattice_capacity;    /* raw lattice arcs per call (lattice mode) */
+    int64_t hash_entries;        /* per-utterance recombination table size (power of two) */
 } wb_decoder_opts;
 
 const char *wb_last_error(void);

@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libwfstb200.so")
+LIB_PATH = os.environ.get("WB_LIB") or os.path.join(_HERE, "_lib", "libwfstb200.so")
 
 WB_OK, WB_ERR_CUDA, WB_ERR_VALUE, WB_ERR_LATTICE, WB_ERR_WFST, WB_ERR_CAPACITY, WB_ERR_NOMEM = range(7)
 WB_MEM_DEVICE, WB_MEM_HOST = 0, 1
@@ -43,7 +43,8 @@ class Config(C.Structure):
 class DecoderOpts(C.Structure):
     _fields_ = [("max_utts_in_flight", C.c_int32), ("cand_capacity", C.c_int32),
                 ("arena_capacity", C.c_int64), ("max_frames", C.c_int32),
-                ("block_threads", C.c_int32), ("lattice_capacity", C.c_int64)]
+                ("block_threads", C.c_int32), ("lattice_capacity", C.c_int64),
+                ("hash_entries", C.c_int64)]
 
 
 UTT_RESULT_DTYPE = np.dtype([

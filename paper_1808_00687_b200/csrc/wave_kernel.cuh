@@ -38,7 +38,7 @@ namespace cg = cooperative_groups;
 constexpr int NB = 4096;       // max-active histogram buckets per lane
 constexpr int GCAP = 2048;     // boundary-bucket members ranked in shared memory
 constexpr int MAXW = 1024;     // lanes per wave (shared-memory prefix arrays)
-constexpr u32 F_MARK = 1u;
+constexpr u32 CA_NONE = 0xFFFFFFFFu, CA_CLAIM = 0xFFFFFFFEu;
 constexpr int MAX_EPS_ROUNDS = 1 << 20;
 constexpr int U = 4;           // relaxations in flight per lane (expand)
 
@@ -83,14 +83,18 @@ struct LaneG {
 };
 
 struct WaveDev {
-    Slot *slot;          // [W][S]
-    u32 *cand_of;        // [W][S] (epsilon graphs)
-    u32 *qtag;           // [W][S] (epsilon graphs)
+    // Per-lane recombination table, open addressing with linear probing (identity mapping when
+    // the whole state space fits): compact, so it stays L2-resident and is reused every step.
+    u32 *hst;            // [W][H] state of an entry (EMPTY_STATE = free)
+    Slot *hslot;         // [W][H] {cost key, arc+1, payload}
+    u32 *hcand;          // [W][H] candidate index of an entry (this step)
+    u32 *hqtag;          // [W][H] epsilon frontier dedup tags (epsilon graphs)
+    u32 *cand_ent;       // [W][cap] table entry of a candidate (append order)
     u32 *cand_state;     // [W][cap]
-    int4 *cand_rng;      // [W][cap]
-    u32 *cand_arc, *cand_pay, *ca_flag, *ca_idx;  // [W][cap]
+    u32 *cand_arc, *cand_pay;  // [W][cap] winner arc + 1, payload (after the gather)
+    u32 *ca_idx;         // [W][cap] backpointer record of a kept candidate (CA_NONE = dropped)
     u64 *cand_key;       // [W][cap]
-    u32 *front;          // [W][2][cap]
+    u32 *front;          // [W][2][cap] frontier entries
     int4 *tok_info;      // [W][2][cap] {state, trace, emit_lo, emit_hi}
     double *tok_cost;    // [W][2][cap]
     int *frames;         // [W][T_cap]
@@ -104,9 +108,15 @@ struct WaveDev {
     u64 *arena_ctr;
     long long S;
     int cap, T_cap, W, first_utt;
+    int hlog2, dense;    // table size 2^hlog2; dense = identity mapping (S <= H)
 };
 
-__device__ __forceinline__ size_t lso(const WaveDev &ws, int w) { return (size_t)w * (size_t)ws.S; }
+constexpr u32 EMPTY_STATE = 0xFFFFFFFFu;
+
+__device__ __forceinline__ size_t lho(const WaveDev &ws, int w) { return (size_t)w << ws.hlog2; }
+__device__ __forceinline__ u32 hhash(const WaveDev &ws, u32 d) {
+    return ws.dense ? d : (d * 0x9E3779B1u) >> (32 - ws.hlog2);
+}
 __device__ __forceinline__ size_t lco(const WaveDev &ws, int w) { return (size_t)w * (size_t)ws.cap; }
 
 __device__ __forceinline__ int bucket_of(double cst, double best, double scale) {
@@ -241,8 +251,10 @@ __device__ __forceinline__ u64 warp_reserve64(u64 *ctr, bool want) {
     return base + __popc(m & lanemask_lt());
 }
 
-// Register candidates installed for the first time this step (warp-converged call).
-__device__ __forceinline__ void warp_append(bool first, u32 d, int4 rng, bool push, int w,
+// Register states whose table entry was claimed this step (warp-converged call): candidate
+// index from one atomic per warp; `rng` = the state's {eps_lo, emit_lo, emit_hi} from the arc
+// record; states with epsilon arcs join the frontier when `push`.
+__device__ __forceinline__ void warp_append(bool first, u32 ent, int4 rng, bool push, int w,
                                             const GraphDev &g, const WaveDev &ws, LaneG &L,
                                             int par, u32 *front_out, u32 *front_ctr) {
     u32 m;
@@ -251,13 +263,9 @@ __device__ __forceinline__ void warp_append(bool first, u32 d, int4 rng, bool pu
     bool pf = false;
     if (first) {
         if ((int)idx < ws.cap) {
-            size_t co = lco(ws, w);
-            ws.cand_state[co + idx] = d;
-            ws.cand_rng[co + idx] = make_int4(rng.x, rng.y, rng.z, 0);
-            if (g.has_eps && rng.x < rng.y) {
-                ws.cand_of[lso(ws, w) + d] = idx;
-                pf = push;
-            }
+            ws.cand_ent[lco(ws, w) + idx] = ent;
+            ws.hcand[lho(ws, w) + ent] = idx;
+            pf = push && g.has_eps && rng.x < rng.y;
         } else {
             L.status = WB_ERR_CAPACITY;
         }
@@ -267,9 +275,22 @@ __device__ __forceinline__ void warp_append(bool first, u32 d, int4 rng, bool pu
         u32 f = warp_reserve(front_ctr, pf, &mf);
         if (mf && (threadIdx.x & 31) == (u32)(__ffs(mf) - 1)) atomicAdd(&ws.gctr[0], (u32)__popc(mf));
         if (pf) {
-            if ((int)f < ws.cap) front_out[f] = d;
+            if ((int)f < ws.cap) front_out[f] = ent;
             else L.status = WB_ERR_CAPACITY;
         }
+    }
+}
+
+// Find or claim the table entry of state d (first probe already attempted: `old` = value the
+// probe CAS at h returned).  Returns the entry, or -1 when the table is full.
+__device__ __forceinline__ int table_resolve(u32 *hst, u32 mask, u32 h, u32 d, u32 old,
+                                             bool *claimed) {
+    for (u32 probe = 0;; ++probe) {
+        if (old == EMPTY_STATE) { *claimed = true; return (int)h; }
+        if (old == d) { *claimed = false; return (int)h; }
+        if (probe >= mask) return -1;
+        h = (h + 1) & mask;
+        old = atomicCAS(&hst[h], EMPTY_STATE, d);
     }
 }
 
@@ -286,8 +307,9 @@ __device__ __forceinline__ void warp_minmax(LaneCnt &cn, bool ok, u64 key) {
 
 // ------------------------------------------------------------------ P1: emitting expansion
 template <int BLOCK>
-__device__ void phase_expand(const GraphDev &g, const WaveDev &ws, const BatchDev &b,
-                             const CfgDev &cfg, int par, Smem<BLOCK> &sh) {
+__noinline__ __device__ void phase_expand(const GraphDev &g, const WaveDev &ws,
+                                          const BatchDev &b, const CfgDev &cfg, int par,
+                                          Smem<BLOCK> &sh) {
     constexpr int NW = BLOCK / 32;
     const int W = ws.W, l = threadIdx.x & 31;
     const int total = lane_chunks<BLOCK>(W, [&](int w) {
@@ -295,6 +317,7 @@ __device__ void phase_expand(const GraphDev &g, const WaveDev &ws, const BatchDe
         return L.done ? 0 : L.n_live;
     }, sh);
     const Slot empty = {EMPTY_KEY, 0xFFFFFFFFu, 0xFFFFFFFFu};
+    const u32 mask = (1u << ws.hlog2) - 1u;
     for (int ch = blockIdx.x * NW + (threadIdx.x >> 5); ch < total; ch += gridDim.x * NW) {
         const int w = chunk_lane(sh.pre, W, (u32)ch);
         LaneG &L = ws.lane[w];
@@ -303,7 +326,8 @@ __device__ void phase_expand(const GraphDev &g, const WaveDev &ws, const BatchDe
         const int f = cfg.mode == 1 ? ws.frames[(size_t)w * ws.T_cap + L.s] : L.s;
         const double *row = b.costs + (size_t)(L.row0 + f) * b.L1;
         const size_t co2 = 2 * lco(ws, w) + (size_t)cur * ws.cap;
-        Slot *slot = ws.slot + lso(ws, w);
+        u32 *hst = ws.hst + lho(ws, w);
+        Slot *hslot = ws.hslot + lho(ws, w);
         u32 *front0 = ws.front + 2 * lco(ws, w);
         const int t = (int)(ch - sh.pre[w]) * 32 + l;
         int4 ti = make_int4(0, 0, 0, 0);
@@ -332,6 +356,7 @@ __device__ void phase_expand(const GraphDev &g, const WaveDev &ws, const BatchDe
                 if (act[u]) rec[u] = __ldg(&g.arcs[2 * arc]);
                 want[u].key = (u64)__double_as_longlong(cst);  // carry the token cost
             }
+            u32 hq[U], oq[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 if (!act[u]) continue;
@@ -343,22 +368,31 @@ __device__ void phase_expand(const GraphDev &g, const WaveDev &ws, const BatchDe
                 double wgt = __hiloint2double(rec[u].w, rec[u].z);
                 double cst = __longlong_as_double((long long)want[u].key);
                 want[u].key = cost_key(__dadd_rn(__dadd_rn(cst, wgt), ac));
+                hq[u] = hhash(ws, (u32)rec[u].x);
+                oq[u] = atomicCAS(&hst[hq[u]], EMPTY_STATE, (u32)rec[u].x);  // probe / claim
             }
+            bool claimed[U];
             Slot prev[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (act[u]) prev[u] = cas_slot(&slot[rec[u].x], empty, want[u]);
+            for (int u = 0; u < U; ++u) {
+                claimed[u] = false;
+                if (!act[u]) continue;
+                int e = table_resolve(hst, mask, hq[u], (u32)rec[u].x, oq[u], &claimed[u]);
+                if (e < 0) { L.status = WB_ERR_CAPACITY; act[u] = false; continue; }
+                hq[u] = (u32)e;
+                prev[u] = cas_slot(&hslot[e], empty, want[u]);
+            }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 bool first = false, dec = false, ok = false;
                 if (act[u]) {
                     ++nfin;
-                    ok = finish_relax(&slot[rec[u].x], want[u], prev[u], &first, &dec);
+                    ok = finish_relax(&hslot[hq[u]], want[u], prev[u], &first, &dec);
                 }
                 warp_minmax(cn, ok, want[u].key);
                 int4 r1 = make_int4(0, 0, 0, 0);
-                if (first) r1 = __ldg(&g.arcs[2 * (want[u].arcp1 - 1u) + 1]);
-                warp_append(first, (u32)rec[u].x, r1, true, w, g, ws, L, par, front0,
+                if (g.has_eps && claimed[u]) r1 = __ldg(&g.arcs[2 * (want[u].arcp1 - 1u) + 1]);
+                warp_append(claimed[u], hq[u], r1, true, w, g, ws, L, par, front0,
                             (u32 *)&cn.nfront[0]);
             }
         }
@@ -372,10 +406,11 @@ __device__ void phase_expand(const GraphDev &g, const WaveDev &ws, const BatchDe
 
 // ------------------------------------------------------------------ P2: epsilon closure round
 // Round r reads frontier buffer r&1 (size nfront[r%3]) and pushes into buffer (r+1)&1
-// (nfront[(r+1)%3]); nfront[(r+2)%3] and gctr[(r+2)%3] are zeroed for round r+1.
+// (nfront[(r+1)%3]); nfront[(r+2)%3] and gctr[(r+2)%3] are zeroed for round r+1.  Frontier
+// entries are table entries; an epsilon winner's payload is its source entry | EPS_BIT.
 template <int BLOCK>
-__device__ void phase_eps_round(const GraphDev &g, const WaveDev &ws, int par, int r, u32 tag,
-                                Smem<BLOCK> &sh) {
+__noinline__ __device__ void phase_eps_round(const GraphDev &g, const WaveDev &ws, int par,
+                                             int r, u32 tag, Smem<BLOCK> &sh) {
     constexpr int NW = BLOCK / 32;
     const int W = ws.W, l = threadIdx.x & 31;
     const int rin = r % 3, rout = (r + 1) % 3, rzero = (r + 2) % 3;
@@ -388,24 +423,26 @@ __device__ void phase_eps_round(const GraphDev &g, const WaveDev &ws, int par, i
         return L.done ? 0 : min(L.cnt[par].nfront[rin], ws.cap);
     }, sh);
     const Slot empty = {EMPTY_KEY, 0xFFFFFFFFu, 0xFFFFFFFFu};
+    const u32 mask = (1u << ws.hlog2) - 1u;
     for (int ch = blockIdx.x * NW + (threadIdx.x >> 5); ch < total; ch += gridDim.x * NW) {
         const int w = chunk_lane(sh.pre, W, (u32)ch);
         LaneG &L = ws.lane[w];
         LaneCnt &cn = L.cnt[par];
         const int nfr = min(cn.nfront[rin], ws.cap);
-        Slot *slot = ws.slot + lso(ws, w);
+        u32 *hst = ws.hst + lho(ws, w);
+        Slot *hslot = ws.hslot + lho(ws, w);
         const size_t co = lco(ws, w);
         const u32 *fin = ws.front + 2 * co + (size_t)(r & 1) * ws.cap;
         u32 *fout = ws.front + 2 * co + (size_t)((r + 1) & 1) * ws.cap;
         const int i = (int)(ch - sh.pre[w]) * 32 + l;
-        u32 uu = 0, ui = 0;
+        u32 ue = 0, uu = 0;
         int lo = 0, deg = 0;
         double ucost = 0.0;
         if (i < nfr) {
-            uu = fin[i];
-            Slot us = ld_slot(&slot[uu]);
-            ui = ws.cand_of[lso(ws, w) + uu];
-            int4 rg = ws.cand_rng[co + ui];
+            ue = fin[i];
+            uu = __ldcg(&hst[ue]);
+            Slot us = ld_slot(&hslot[ue]);
+            int4 rg = us.arcp1 == 0u ? g.start_rng : __ldg(&g.arcs[2 * (us.arcp1 - 1u) + 1]);
             lo = rg.x;
             deg = rg.y - rg.x;
             ucost = key_cost(us.key);
@@ -421,7 +458,7 @@ __device__ void phase_eps_round(const GraphDev &g, const WaveDev &ws, int par, i
             int ex_k = __shfl_sync(FULL, excl, k);
             double uc_k = __shfl_sync(FULL, ucost, k);
             u32 u_k = __shfl_sync(FULL, uu, k);
-            u32 ui_k = __shfl_sync(FULL, ui, k);
+            u32 ue_k = __shfl_sync(FULL, ue, k);
             bool act = j < tot;
             int a = lo_k + j - ex_k;
             int4 rec = make_int4(0, 0, 0, 0);
@@ -429,28 +466,38 @@ __device__ void phase_eps_round(const GraphDev &g, const WaveDev &ws, int par, i
                 rec = __ldg(&g.arcs[2 * a]);
                 if ((u32)rec.x == u_k) act = false;  // a positive self-loop never improves its state
             }
-            bool first = false, dec = false, ok = false;
+            bool first = false, dec = false, ok = false, claimed = false;
+            int e = 0;
             Slot want;
             want.key = EMPTY_KEY;
             if (act) {
                 ++neps;
                 want.key = cost_key(__dadd_rn(uc_k, __hiloint2double(rec.w, rec.z)));
                 want.arcp1 = (u32)a + 1u;
-                want.pay = ui_k | EPS_BIT;
-                Slot prev = cas_slot(&slot[rec.x], empty, want);
-                ok = finish_relax(&slot[rec.x], want, prev, &first, &dec);
+                want.pay = ue_k | EPS_BIT;  // epsilon winner: payload = source entry
+                u32 h = hhash(ws, (u32)rec.x);
+                u32 old = atomicCAS(&hst[h], EMPTY_STATE, (u32)rec.x);
+                e = table_resolve(hst, mask, h, (u32)rec.x, old, &claimed);
+                if (e < 0) {
+                    L.status = WB_ERR_CAPACITY;
+                    claimed = false;
+                } else {
+                    Slot prev = cas_slot(&hslot[e], empty, want);
+                    ok = finish_relax(&hslot[e], want, prev, &first, &dec);
+                }
             }
             warp_minmax(cn, ok, want.key);
             int4 r1 = make_int4(0, 0, 0, 0);
-            if (dec) r1 = __ldg(&g.arcs[2 * a + 1]);
-            warp_append(first, (u32)rec.x, r1, false, w, g, ws, L, par, fout, nullptr);
-            // states that are new or got cheaper re-relax their epsilon arcs next round
-            bool push = dec && r1.x < r1.y && atomicExch(&ws.qtag[lso(ws, w) + rec.x], tag) != tag;
+            if (ok && dec) r1 = __ldg(&g.arcs[2 * a + 1]);
+            warp_append(claimed, (u32)e, r1, false, w, g, ws, L, par, fout, nullptr);
+            // entries that are new or got cheaper re-relax their epsilon arcs next round
+            bool push = ok && dec && r1.x < r1.y &&
+                        atomicExch(&ws.hqtag[lho(ws, w) + e], tag) != tag;
             u32 mp;
             u32 fidx = warp_reserve((u32 *)&cn.nfront[rout], push, &mp);
             if (mp && l == __ffs(mp) - 1) atomicAdd(&ws.gctr[rout], (u32)__popc(mp));
             if (push) {
-                if ((int)fidx < ws.cap) fout[fidx] = (u32)rec.x;
+                if ((int)fidx < ws.cap) fout[fidx] = (u32)e;
                 else L.status = WB_ERR_CAPACITY;
             }
         }
@@ -460,8 +507,10 @@ __device__ void phase_eps_round(const GraphDev &g, const WaveDev &ws, int par, i
 }
 
 // ------------------------------------------------------------------ P3: gather + histogram
+constexpr int GC = 4;  // chunks per warp iteration in the per-candidate phases (loads in flight)
+
 template <int BLOCK>
-__device__ void phase_gather(const GraphDev &g, const WaveDev &ws, const CfgDev &cfg, int par,
+__noinline__ __device__ void phase_gather(const GraphDev &g, const WaveDev &ws, const CfgDev &cfg, int par,
                              Smem<BLOCK> &sh) {
     constexpr int NW = BLOCK / 32;
     const int W = ws.W, l = threadIdx.x & 31;
@@ -469,41 +518,64 @@ __device__ void phase_gather(const GraphDev &g, const WaveDev &ws, const CfgDev 
         const LaneG &L = ws.lane[w];
         return L.done ? 0 : min(L.cnt[par].n_cand, ws.cap);
     }, sh);
-    for (int ch = blockIdx.x * NW + (threadIdx.x >> 5); ch < total; ch += gridDim.x * NW) {
-        const int w = chunk_lane(sh.pre, W, (u32)ch);
-        LaneG &L = ws.lane[w];
-        LaneCnt &cn = L.cnt[par];
-        const int n = min(cn.n_cand, ws.cap);
-        const int loc = (int)(ch - sh.pre[w]);
-        const int i = loc * 32 + l;
-        const size_t co = lco(ws, w);
-        Slot *slot = ws.slot + lso(ws, w);
-        const Beam bm = lane_beam(cn, cfg, n);
-        bool in = false;
-        if (i < n) {
-            u32 s = ws.cand_state[co + i];
-            Slot v = ld_slot(&slot[s]);
-            ws.cand_key[co + i] = v.key;
-            ws.cand_arc[co + i] = v.arcp1;
-            ws.cand_pay[co + i] = v.pay;
-            ws.ca_flag[co + i] = 0u;
-            st_slot_empty(&slot[s]);
-            double cst = key_cost(v.key);
-            in = cst <= bm.cutoff;
-            if (bm.may_cut && in)
-                atomicAdd(&ws.hist[(size_t)w * NB + bucket_of(cst, bm.best, bm.scale)], 1u);
+    const int gw = blockIdx.x * NW + (threadIdx.x >> 5), nwarps = gridDim.x * NW;
+    for (int c0 = gw * GC; c0 < total; c0 += nwarps * GC) {
+        int wq[GC], iq[GC];
+        u32 eq[GC], st[GC];
+        Slot v[GC];
+#pragma unroll
+        for (int q = 0; q < GC; ++q) {
+            const int ch = c0 + q;
+            wq[q] = -1;
+            iq[q] = 0;
+            if (ch < total) {
+                const int w = chunk_lane(sh.pre, W, (u32)ch);
+                const int i = (int)(ch - sh.pre[w]) * 32 + l;
+                if (i < min(ws.lane[w].cnt[par].n_cand, ws.cap)) {
+                    wq[q] = w;
+                    iq[q] = i;
+                    eq[q] = ws.cand_ent[lco(ws, w) + i];
+                }
+            }
         }
-        if (bm.may_cut) {
-            u32 kept = (u32)__popc(__ballot_sync(FULL, in));
-            if (l == 0 && kept) atomicAdd(&cn.kept, (unsigned long long)kept);
-            if (loc == 0 && l == 0) atomicAdd(&ws.gctr[3 + par], 1u);
+#pragma unroll
+        for (int q = 0; q < GC; ++q)
+            if (wq[q] >= 0) {
+                st[q] = __ldcg(&ws.hst[lho(ws, wq[q]) + eq[q]]);
+                v[q] = ld_slot(&ws.hslot[lho(ws, wq[q]) + eq[q]]);
+            }
+#pragma unroll
+        for (int q = 0; q < GC; ++q) {
+            const int ch = c0 + q;
+            if (ch >= total) break;  // warp-uniform
+            const int w = chunk_lane(sh.pre, W, (u32)ch);
+            LaneCnt &cn = ws.lane[w].cnt[par];
+            const Beam bm = lane_beam(cn, cfg, min(cn.n_cand, ws.cap));
+            bool in = false;
+            if (wq[q] >= 0) {
+                const size_t co = lco(ws, w) + iq[q];
+                ws.cand_state[co] = st[q];
+                ws.cand_key[co] = v[q].key;
+                ws.cand_arc[co] = v[q].arcp1;
+                ws.cand_pay[co] = v[q].pay;
+                ws.ca_idx[co] = CA_NONE;
+                double cst = key_cost(v[q].key);
+                in = cst <= bm.cutoff;
+                if (bm.may_cut && in)
+                    atomicAdd(&ws.hist[(size_t)w * NB + bucket_of(cst, bm.best, bm.scale)], 1u);
+            }
+            if (bm.may_cut) {
+                u32 kept = (u32)__popc(__ballot_sync(FULL, in));
+                if (l == 0 && kept) atomicAdd(&cn.kept, (unsigned long long)kept);
+                if (ch == (int)sh.pre[w] && l == 0) atomicAdd(&ws.gctr[3 + par], 1u);
+            }
         }
     }
 }
 
 // ------------------------------------------------------------------ P5: max-active threshold
 template <int BLOCK>
-__device__ void lane_threshold(const WaveDev &ws, const CfgDev &cfg, int w, int par,
+__noinline__ __device__ void lane_threshold(const WaveDev &ws, const CfgDev &cfg, int w, int par,
                                Smem<BLOCK> &sh) {
     LaneG &L = ws.lane[w];
     LaneCnt &cn = L.cnt[par];
@@ -640,8 +712,11 @@ __device__ __forceinline__ bool survives(u64 k, u32 st, const Beam &bm, const La
 }
 
 // ------------------------------------------------------------------ P6: survivors + records
+// Survivors get a backpointer record and a next-step token.  An epsilon winner's record links
+// to its source candidate's record (written in P8); sources that are not survivors themselves
+// are claimed here (CAS on their record slot) so exactly one thread records each.
 template <int BLOCK>
-__device__ void phase_survive(const GraphDev &g, const WaveDev &ws, const CfgDev &cfg, int par,
+__noinline__ __device__ void phase_survive(const GraphDev &g, const WaveDev &ws, const CfgDev &cfg, int par,
                               Smem<BLOCK> &sh) {
     constexpr int NW = BLOCK / 32;
     const int W = ws.W, l = threadIdx.x & 31;
@@ -649,90 +724,125 @@ __device__ void phase_survive(const GraphDev &g, const WaveDev &ws, const CfgDev
         const LaneG &L = ws.lane[w];
         return L.done ? 0 : min(L.cnt[par].n_cand, ws.cap);
     }, sh);
-    for (int ch = blockIdx.x * NW + (threadIdx.x >> 5); ch < total; ch += gridDim.x * NW) {
-        const int w = chunk_lane(sh.pre, W, (u32)ch);
-        LaneG &L = ws.lane[w];
-        LaneCnt &cn = L.cnt[par];
-        const int n = min(cn.n_cand, ws.cap);
-        const int i = (int)(ch - sh.pre[w]) * 32 + l;
-        const size_t co = lco(ws, w);
-        const Beam bm = lane_beam(cn, cfg, n);
-        const int need = cn.need;
-        bool surv = false;
-        u64 k = 0;
-        u32 st = 0, a = 0, p = 0;
-        if (i < n) {
-            k = ws.cand_key[co + i];
-            st = ws.cand_state[co + i];
-            surv = survives(k, st, bm, L, need);
-        }
-        const u64 rec = warp_reserve64(ws.arena_ctr, surv);
-        u32 mtok;
-        const u32 j = warp_reserve((u32 *)&cn.n_surv, surv, &mtok);
-        if (mtok && l == __ffs(mtok) - 1) atomicAdd(&cn.n_rec, (unsigned long long)__popc(mtok));
-        if (!surv) continue;
-        if (rec >= ws.arena_cap || rec >= (u64)EPS_BIT) { L.status = WB_ERR_CAPACITY; continue; }
-        ws.ca_idx[co + i] = (u32)rec;
-        a = ws.cand_arc[co + i];
-        p = ws.cand_pay[co + i];
-        const size_t nx = 2 * co + (size_t)(L.cur ^ 1) * ws.cap;
-        int4 rg = ws.cand_rng[co + i];
-        ws.tok_info[nx + j] = make_int4((int)st, (int)rec, rg.y, rg.z);
-        ws.tok_cost[nx + j] = key_cost(k);
-        if (a == 0u || !(p & EPS_BIT)) {
-            ws.arena[rec] = (u64)a | ((u64)(a == 0u ? ROOT_PREV : p) << 32);
-            continue;
-        }
-        // epsilon winner: claim the candidates of its epsilon chain that are not survivors
-        u32 v_pay = p;
-        for (;;) {
-            const int uix = (int)(v_pay & ~EPS_BIT);
-            u64 ku = ws.cand_key[co + uix];
-            u32 su = ws.cand_state[co + uix];
-            if (survives(ku, su, bm, L, need)) break;          // its own thread records it
-            if (atomicOr(&ws.ca_flag[co + uix], F_MARK) & F_MARK) break;
-            u64 ru = atomicAdd(ws.arena_ctr, 1ull);
-            atomicAdd(&cn.n_rec, 1ull);
-            if (ru >= ws.arena_cap || ru >= (u64)EPS_BIT) { L.status = WB_ERR_CAPACITY; break; }
-            ws.ca_idx[co + uix] = (u32)ru;
-            u32 au = ws.cand_arc[co + uix], pu = ws.cand_pay[co + uix];
-            if (au == 0u || !(pu & EPS_BIT)) {
-                ws.arena[ru] = (u64)au | ((u64)(au == 0u ? ROOT_PREV : pu) << 32);
-                break;
+    const int gw = blockIdx.x * NW + (threadIdx.x >> 5), nwarps = gridDim.x * NW;
+    for (int c0 = gw * GC; c0 < total; c0 += nwarps * GC) {
+        u64 kq[GC];
+        u32 sq[GC];
+        int iq[GC], wq[GC];
+#pragma unroll
+        for (int q = 0; q < GC; ++q) {
+            const int ch = c0 + q;
+            wq[q] = -1;
+            iq[q] = 0;
+            if (ch < total) {
+                const int w = chunk_lane(sh.pre, W, (u32)ch);
+                const int i = (int)(ch - sh.pre[w]) * 32 + l;
+                if (i < min(ws.lane[w].cnt[par].n_cand, ws.cap)) {
+                    const size_t co = lco(ws, w) + i;
+                    wq[q] = w;
+                    iq[q] = i;
+                    kq[q] = ws.cand_key[co];
+                    sq[q] = ws.cand_state[co];
+                }
             }
-            v_pay = pu;
+        }
+#pragma unroll
+        for (int q = 0; q < GC; ++q) {
+            const int ch = c0 + q;
+            if (ch >= total) break;  // warp-uniform
+            const int w = chunk_lane(sh.pre, W, (u32)ch);
+            LaneG &L = ws.lane[w];
+            LaneCnt &cn = L.cnt[par];
+            const int n = min(cn.n_cand, ws.cap);
+            const Beam bm = lane_beam(cn, cfg, n);
+            const int need = cn.need;
+            const bool surv = wq[q] >= 0 && survives(kq[q], sq[q], bm, L, need);
+            const u64 rec = warp_reserve64(ws.arena_ctr, surv);
+            u32 mtok;
+            const u32 j = warp_reserve((u32 *)&cn.n_surv, surv, &mtok);
+            if (mtok && l == __ffs(mtok) - 1) atomicAdd(&cn.n_rec, (unsigned long long)__popc(mtok));
+            if (!surv) continue;
+            if (rec >= ws.arena_cap || rec >= (u64)EPS_BIT) { L.status = WB_ERR_CAPACITY; continue; }
+            const size_t co = lco(ws, w);
+            const int i = iq[q];
+            ws.ca_idx[co + i] = (u32)rec;
+            const u32 a = ws.cand_arc[co + i], p = ws.cand_pay[co + i];
+            const int4 r1 = a == 0u ? g.start_rng : __ldg(&g.arcs[2 * (a - 1u) + 1]);
+            const size_t nx = 2 * co + (size_t)(L.cur ^ 1) * ws.cap;
+            ws.tok_info[nx + j] = make_int4((int)sq[q], (int)rec, r1.y, r1.z);
+            ws.tok_cost[nx + j] = key_cost(kq[q]);
+            if (a == 0u || !(p & EPS_BIT)) {
+                ws.arena[rec] = (u64)a | ((u64)(a == 0u ? ROOT_PREV : p) << 32);
+                continue;
+            }
+            // epsilon winner: claim the non-surviving candidates of its epsilon chain
+            u32 src = p & ~EPS_BIT;  // source table entry
+            for (;;) {
+                const u32 uc = ws.hcand[lho(ws, w) + src];
+                if (survives(ws.cand_key[co + uc], ws.cand_state[co + uc], bm, L, need)) break;
+                if (atomicCAS(&ws.ca_idx[co + uc], CA_NONE, CA_CLAIM) != CA_NONE) break;
+                const u64 ru = atomicAdd(ws.arena_ctr, 1ull);
+                atomicAdd(&cn.n_rec, 1ull);
+                if (ru >= ws.arena_cap || ru >= (u64)EPS_BIT) { L.status = WB_ERR_CAPACITY; break; }
+                ws.ca_idx[co + uc] = (u32)ru;
+                const u32 au = ws.cand_arc[co + uc], pu = ws.cand_pay[co + uc];
+                if (au == 0u || !(pu & EPS_BIT)) {
+                    ws.arena[ru] = (u64)au | ((u64)(au == 0u ? ROOT_PREV : pu) << 32);
+                    break;
+                }
+                src = pu & ~EPS_BIT;
+            }
         }
     }
 }
 
 // ------------------------------------------------------------------ P8: epsilon links + lanes
 template <int BLOCK>
-__device__ void phase_link(const GraphDev &g, const WaveDev &ws, const CfgDev &cfg, int k,
+__noinline__ __device__ void phase_link(const GraphDev &g, const WaveDev &ws, const CfgDev &cfg, int k,
                            Smem<BLOCK> &sh) {
+    constexpr int NW = BLOCK / 32;
     const int par = k & 1;
     const bool search_step = k > 0;
-    constexpr int NW = BLOCK / 32;
     const int W = ws.W, l = threadIdx.x & 31;
-    if (g.has_eps) {
+    {
+        // epsilon-winner records (their source's record index is final now) and the table
+        // reset O(touched) for the next step
         const int total = lane_chunks<BLOCK>(W, [&](int w) {
             const LaneG &L = ws.lane[w];
             return L.done ? 0 : min(L.cnt[par].n_cand, ws.cap);
         }, sh);
-        for (int ch = blockIdx.x * NW + (threadIdx.x >> 5); ch < total; ch += gridDim.x * NW) {
-            const int w = chunk_lane(sh.pre, W, (u32)ch);
-            const LaneG &L = ws.lane[w];
-            const LaneCnt &cn = L.cnt[par];
-            const int n = min(cn.n_cand, ws.cap);
-            const int i = (int)(ch - sh.pre[w]) * 32 + l;
-            if (i >= n) continue;
-            const size_t co = lco(ws, w);
-            u32 a = ws.cand_arc[co + i], p = ws.cand_pay[co + i];
-            if (a == 0u || !(p & EPS_BIT)) continue;
-            const Beam bm = lane_beam(cn, cfg, n);
-            bool kept = survives(ws.cand_key[co + i], ws.cand_state[co + i], bm, L, cn.need) ||
-                        (ws.ca_flag[co + i] & F_MARK);
-            if (!kept) continue;
-            ws.arena[ws.ca_idx[co + i]] = (u64)a | ((u64)ws.ca_idx[co + (p & ~EPS_BIT)] << 32);
+        const int gw = blockIdx.x * NW + (threadIdx.x >> 5), nwarps = gridDim.x * NW;
+        for (int c0 = gw * GC; c0 < total; c0 += nwarps * GC) {
+            u32 aq[GC], pq[GC], rq[GC], eq[GC];
+            int wq[GC];
+#pragma unroll
+            for (int q = 0; q < GC; ++q) {
+                const int ch = c0 + q;
+                wq[q] = -1;
+                if (ch < total) {
+                    const int w = chunk_lane(sh.pre, W, (u32)ch);
+                    const int i = (int)(ch - sh.pre[w]) * 32 + l;
+                    if (i < min(ws.lane[w].cnt[par].n_cand, ws.cap)) {
+                        const size_t co = lco(ws, w) + i;
+                        wq[q] = w;
+                        eq[q] = ws.cand_ent[co];
+                        rq[q] = ws.ca_idx[co];
+                        aq[q] = ws.cand_arc[co];
+                        pq[q] = ws.cand_pay[co];
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < GC; ++q) {
+                if (wq[q] < 0) continue;
+                const int w = wq[q];
+                if (rq[q] < CA_CLAIM && aq[q] != 0u && (pq[q] & EPS_BIT)) {
+                    const u32 uc = ws.hcand[lho(ws, w) + (pq[q] & ~EPS_BIT)];
+                    ws.arena[rq[q]] = (u64)aq[q] | ((u64)ws.ca_idx[lco(ws, w) + uc] << 32);
+                }
+                ws.hst[lho(ws, w) + eq[q]] = EMPTY_STATE;
+                st_slot_empty(&ws.hslot[lho(ws, w) + eq[q]]);
+            }
         }
     }
     // lane bookkeeping: one thread per lane; nothing else in this phase reads these fields
@@ -781,8 +891,8 @@ __device__ void phase_link(const GraphDev &g, const WaveDev &ws, const CfgDev &c
 }
 
 // ------------------------------------------------------------------ the persistent kernel
-template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK, 2)
+template <int BLOCK, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB)
 wave_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WaveDev ws,
             const __grid_constant__ BatchDev b, const __grid_constant__ CfgDev cfg,
             wb_utt_result *res) {
@@ -854,19 +964,20 @@ wave_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WaveDev 
                 cn.n_rec = 0;
             }
             if (real) {
-                // start entry (0.0, src -1, arc -1, ROOT) (decoder.py:241)
-                const size_t so = lso(ws, w), co = lco(ws, w);
+                // start entry (0.0, src -1, arc -1, ROOT) (decoder.py:241); tables are empty
+                const size_t ho = lho(ws, w), co = lco(ws, w);
+                const u32 e = hhash(ws, (u32)g.start);
                 const u64 k0 = cost_key(0.0);
-                __stcg(reinterpret_cast<ulonglong2 *>(&ws.slot[so + g.start]),
+                ws.hst[ho + e] = (u32)g.start;
+                __stcg(reinterpret_cast<ulonglong2 *>(&ws.hslot[ho + e]),
                        make_ulonglong2(k0, (u64)0u | ((u64)ROOT_PREV << 32)));
-                ws.cand_state[co] = (u32)g.start;
-                ws.cand_rng[co] = g.start_rng;
+                ws.hcand[ho + e] = 0u;
+                ws.cand_ent[co] = e;
                 L.cnt[0].n_cand = 1;
                 L.cnt[0].kmin = k0;
                 L.cnt[0].khi = k0;
                 if (g.has_eps && g.start_rng.x < g.start_rng.y) {
-                    ws.cand_of[so + g.start] = 0u;
-                    ws.front[2 * co] = (u32)g.start;
+                    ws.front[2 * co] = e;
                     L.cnt[0].nfront[0] = 1;
                     atomicAdd(&ws.gctr[0], 1u);
                 }

@@ -15,6 +15,10 @@
 using namespace wb;
 using wb::wave::LaneG;
 
+#ifndef WB_WAVE_MINB
+#define WB_WAVE_MINB 1  // CTAs per SM the wave kernel is register-budgeted for
+#endif
+
 static thread_local std::string g_err;
 
 static int set_err(int code, const std::string &msg) {
@@ -43,11 +47,11 @@ struct wb_decoder_s {
     wb_graph_s *g = nullptr;
     int W = 0, cap = 0, T_cap = 0, block = 512, num_sms = 0, grid = 0;
     u64 arena_cap = 0;
-    Slot *slot = nullptr;
-    u32 *cand_of = nullptr, *qtag = nullptr;
-    u32 *cand_state = nullptr, *cand_arc = nullptr, *cand_pay = nullptr, *ca_flag = nullptr,
+    int hlog2 = 0, dense = 0;
+    u32 *hst = nullptr, *hcand = nullptr, *hqtag = nullptr;
+    Slot *hslot = nullptr;
+    u32 *cand_ent = nullptr, *cand_state = nullptr, *cand_arc = nullptr, *cand_pay = nullptr,
         *ca_idx = nullptr;
-    int4 *cand_rng = nullptr;
     u64 *cand_key = nullptr;
     u32 *front = nullptr;
     int4 *tok_info = nullptr;
@@ -155,8 +159,8 @@ int wb_graph_device_bytes(wb_graph_t g, int64_t *bytes) {
 }  // extern "C"
 
 static void free_decoder(wb_decoder_s *d) {
-    void *ptrs[] = {d->slot, d->cand_of, d->qtag, d->cand_state, d->cand_rng, d->cand_arc,
-                    d->cand_pay, d->ca_flag, d->ca_idx, d->cand_key, d->front, d->tok_info,
+    void *ptrs[] = {d->hst, d->hslot, d->hcand, d->hqtag, d->cand_ent, d->cand_state, d->cand_arc,
+                    d->cand_pay, d->ca_idx, d->cand_key, d->front, d->tok_info,
                     d->tok_cost, d->frames, d->hist, d->lane, d->gctr, d->phase, d->arena,
                     d->arena_ctr, d->h_costs, d->h_blank, d->h_off, d->h_T, d->h_res, d->h_lab};
     for (void *p : ptrs) cudaFree(p);
@@ -219,24 +223,38 @@ int wb_decoder_create(wb_graph_t g, const wb_decoder_opts *o, wb_decoder_t *out)
     d->cap = opts.cand_capacity > 0 ? opts.cand_capacity : std::min(g->S, 1 << 18);
     d->cap = std::max(1, std::min(d->cap, g->S));
     int occ = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave::wave_kernel<512>, 512, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave::wave_kernel<512, WB_WAVE_MINB>, 512, 0);
     if (e != cudaSuccess || occ < 1) {
         delete d;
         return set_err(WB_ERR_CUDA, "wave kernel occupancy query failed");
     }
     d->grid = d->num_sms * std::min(occ, 2);
-    size_t S = (size_t)g->S, W = (size_t)d->W, cap = (size_t)d->cap;
+    // recombination table per lane: next power of two >= S (identity mapping, no probing)
+    // when that is at most hash_entries, else a hash table of hash_entries (load <= ~0.7)
+    const int64_t hmax = opts.hash_entries > 0 ? opts.hash_entries : 32768;
+    int hl = 0;
+    while ((1ll << hl) < (int64_t)g->S) ++hl;
+    if ((1ll << hl) <= hmax) {
+        d->dense = 1;
+    } else {
+        d->dense = 0;
+        hl = 0;
+        while ((1ll << hl) < hmax) ++hl;
+    }
+    d->hlog2 = std::max(hl, 1);
+    d->cap = std::min(d->cap, d->dense ? g->S : (int)((1ll << d->hlog2) * 7 / 8));
+    size_t H = (size_t)1 << d->hlog2, W = (size_t)d->W, cap = (size_t)d->cap;
     size_t acc = 0;
     e = cudaSuccess;
 #define DA(p, n) if (e == cudaSuccess) e = dalloc(&d->p, (n), acc)
-    DA(slot, W * S);
-    DA(cand_of, g->has_eps ? W * S : 1);
-    DA(qtag, g->has_eps ? W * S : 1);
+    DA(hst, W * H);
+    DA(hslot, W * H);
+    DA(hcand, W * H);
+    DA(hqtag, g->has_eps ? W * H : 1);
+    DA(cand_ent, W * cap);
     DA(cand_state, W * cap);
-    DA(cand_rng, W * cap);
     DA(cand_arc, W * cap);
     DA(cand_pay, W * cap);
-    DA(ca_flag, W * cap);
     DA(ca_idx, W * cap);
     DA(cand_key, W * cap);
     DA(front, W * 2 * cap);
@@ -248,8 +266,9 @@ int wb_decoder_create(wb_graph_t g, const wb_decoder_opts *o, wb_decoder_t *out)
     DA(phase, 8);
     DA(arena_ctr, 1);
 #undef DA
-    if (e == cudaSuccess) e = cudaMemset(d->slot, 0xFF, sizeof(Slot) * W * S);
-    if (e == cudaSuccess && g->has_eps) e = cudaMemset(d->qtag, 0, sizeof(u32) * W * S);
+    if (e == cudaSuccess) e = cudaMemset(d->hst, 0xFF, sizeof(u32) * W * H);
+    if (e == cudaSuccess) e = cudaMemset(d->hslot, 0xFF, sizeof(Slot) * W * H);
+    if (e == cudaSuccess && g->has_eps) e = cudaMemset(d->hqtag, 0, sizeof(u32) * W * H);
     if (e == cudaSuccess) e = cudaMemset(d->hist, 0, sizeof(u32) * W * wave::NB);
     if (e == cudaSuccess) e = cudaMemset(d->gctr, 0, sizeof(u32) * 16);
     if (e == cudaSuccess) e = cudaEventCreate(&d->ev0);
@@ -354,9 +373,10 @@ int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row
     wave::CfgDev cd{cfg->beam, cfg->blank_threshold, cfg->max_active, cfg->mode, cfg->lattice};
     wave::WaveDev wd;
     std::memset(&wd, 0, sizeof(wd));
-    wd.slot = d->slot; wd.cand_of = d->cand_of; wd.qtag = d->qtag;
-    wd.cand_state = d->cand_state; wd.cand_rng = d->cand_rng; wd.cand_arc = d->cand_arc;
-    wd.cand_pay = d->cand_pay; wd.ca_flag = d->ca_flag; wd.ca_idx = d->ca_idx;
+    wd.hst = d->hst; wd.hslot = d->hslot; wd.hcand = d->hcand; wd.hqtag = d->hqtag;
+    wd.hlog2 = d->hlog2; wd.dense = d->dense;
+    wd.cand_ent = d->cand_ent; wd.cand_state = d->cand_state; wd.cand_arc = d->cand_arc;
+    wd.cand_pay = d->cand_pay; wd.ca_idx = d->ca_idx;
     wd.cand_key = d->cand_key; wd.front = d->front; wd.tok_info = d->tok_info;
     wd.tok_cost = d->tok_cost; wd.frames = d->frames; wd.hist = d->hist; wd.lane = d->lane;
     wd.gctr = d->gctr; wd.phase = d->phase; wd.arena = d->arena; wd.arena_cap = d->arena_cap;
@@ -370,7 +390,7 @@ int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row
         CUDA_TRY(cudaMemsetAsync(d->phase, 0, sizeof(long long) * 8, st));
         CUDA_TRY(cudaMemsetAsync(d->arena_ctr, 0, sizeof(u64), st));
         void *args[] = {(void *)&gd, (void *)&wd, (void *)&bd, (void *)&cd, (void *)&dres};
-        CUDA_TRY(cudaLaunchCooperativeKernel((void *)wave::wave_kernel<512>, d->grid, 512, args, 0, st));
+        CUDA_TRY(cudaLaunchCooperativeKernel((void *)wave::wave_kernel<512, WB_WAVE_MINB>, d->grid, 512, args, 0, st));
         // backtrace (decoder.py:276-291) of this wave before its arena is reused
         wave::backtrace_kernel<<<(wd.W + 127) / 128, 128, 0, st>>>(d->arena, g->arcs, dres + first, wd.W,
                                                              dol + (size_t)first * lcap,

@@ -160,12 +160,12 @@ class BatchDecoder:
 
     def __init__(self, graph, device: int | None = None, *, max_utts_in_flight: int = 0,
                  cand_capacity: int = 0, arena_capacity: int = 0, max_frames: int = 0,
-                 block_threads: int = 0):
+                 block_threads: int = 0, hash_entries: int = 0):
         self.graph = graph if isinstance(graph, DeviceGraph) else DeviceGraph(graph, device)
         self.device = self.graph.device
         self.opts = dict(max_utts_in_flight=max_utts_in_flight, cand_capacity=cand_capacity,
                          arena_capacity=arena_capacity, max_frames=max_frames,
-                         block_threads=block_threads)
+                         block_threads=block_threads, hash_entries=hash_entries)
         self._h = None
         self._create()
 
@@ -174,7 +174,7 @@ class BatchDecoder:
             self._fin()
         o = self.opts
         opts = N.DecoderOpts(o["max_utts_in_flight"], o["cand_capacity"], o["arena_capacity"],
-                             o["max_frames"], o["block_threads"], 0)
+                             o["max_frames"], o["block_threads"], 0, o["hash_entries"])
         h = C.c_void_p()
         N.check(N.load().wb_decoder_create(self.graph.handle, C.byref(opts), C.byref(h)),
                 "decoder workspace")
@@ -187,6 +187,7 @@ class BatchDecoder:
         self.opts["cand_capacity"] = min(S, cap * 2)
         arena = self.opts["arena_capacity"] or (1 << 24)
         self.opts["arena_capacity"] = min(2**31 - 2, max(arena * 2, arena_need or 0))
+        self.opts["hash_entries"] = 2 * (self.opts["hash_entries"] or 32768)
         self._create()
 
     def device_bytes(self) -> int:
