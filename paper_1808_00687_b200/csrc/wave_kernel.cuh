@@ -4,22 +4,28 @@
 // step is spread over ALL SMs (one cooperative persistent launch, phases separated by grid
 // barriers), so one utterance's 15-20k relaxations per frame are processed by ~150 SMs
 // instead of one.  Work inside a phase is flattened over (utterance lane, chunk of 32 items);
-// chunks never straddle lanes, so per-lane counters can be updated with warp-aggregated
+// chunks never straddle lanes, so per-lane counters are updated with warp-aggregated
 // atomics.  Per step (decoder.py:197-233):
 //
-//   P1 expand   tokens x emitting arcs, warp-level load balancing by prefix-summed
+//   E1 expand   tokens x emitting arcs, warp-level load balancing by prefix-summed
 //               out-degree; 32-byte arc records {dst, ilabel, weight | dst ranges, olabel};
-//               recombination = optimistic 128-bit CAS on a dense per-lane slot
-//               {cost key, arc+1, payload} under the (cost, src, arc) total order
-//               (decoder.py:121-135); installs also maintain the lane's min / max cost key
-//   P2 closure  epsilon frontier rounds, epoch-tagged dedup (decoder.py:138-171)
-//   P3 gather   slot -> compact candidate arrays, slot reset O(touched), max-active
-//               histogram (4096 value buckets) when the cut can bind (decoder.py:174-194)
+//               each relaxation is a fire-and-forget 64-bit atomicMin (RED) of its
+//               order-preserving cost key into the destination's slot, and is logged
+//   E2 ties     logged relaxations whose key equals the slot minimum atomicMin their
+//               arc index + 1: the (cost, src state, arc) total order of decoder.py:121-135
+//               (arcs are sorted by source state, so arc order == (src, arc) order)
+//   E3 winners  the unique relaxation matching (key, arc) stores its payload and registers
+//               the state as a candidate -- no 128-bit CAS on the emitting hot path
+//   P2 closure  epsilon frontier rounds (128-bit CAS recombination, epoch-tagged dedup)
+//               (decoder.py:138-171)
+//   P3 gather   slot -> compact candidate arrays, max-active histogram (4096 value
+//               buckets) when the cut can bind (decoder.py:174-194)
 //   P5 select   per lane: exact (cost, state) threshold = max_active-th smallest, from the
 //               histogram + an exact rank inside the boundary bucket (radix-select fallback)
 //   P6 survive  survivors get arena backpointer records + next tokens; epsilon-chain
 //               candidates they trace through are claimed and recorded too
-//   P8 link     epsilon-winner records (need their source's record index); lane bookkeeping
+//   P8 link     epsilon-winner records (need their source's record index), slot reset
+//               O(touched), lane bookkeeping
 //
 // Arithmetic is float64 in the reference's association order; results are bit-identical to
 // decoder.py (labels: winner-consistent traces, identical on tie-free inputs).
@@ -41,6 +47,7 @@ constexpr int MAXW = 1024;     // lanes per wave (shared-memory prefix arrays)
 constexpr u32 CA_NONE = 0xFFFFFFFFu, CA_CLAIM = 0xFFFFFFFEu;
 constexpr int MAX_EPS_ROUNDS = 1 << 20;
 constexpr int U = 4;           // relaxations in flight per lane (expand)
+constexpr int GC = 4;          // chunks per warp iteration in the streaming phases
 
 struct GraphDev {
     int S, A, start, has_eps;
@@ -64,16 +71,20 @@ struct CfgDev {
 
 // Per-step counters of one lane, double-buffered by step parity.
 struct LaneCnt {
-    int n_cand;        // candidates appended this step
+    int n_cand;        // candidates registered this step
     int nfront[3];     // epsilon frontier sizes, rotating by round
     int n_surv;        // next-step tokens
     int need;          // max-active cut binds
+    int n_log;         // logged emitting relaxations
+    int _pad;
     unsigned long long kept;  // candidates within the beam (when the cut may bind)
     u64 kmin, khi;     // min / max of installed cost keys (min == min of final slot values)
     unsigned long long n_rec;  // backpointer records this step
 };
 
-struct LaneG {
+// Padded to 4 KB: lanes' hot counters (appends, min/max, logs) are hammered by warp-aggregated
+// atomics from every SM, and must not share L2 lines / slices with other lanes' counters.
+struct __align__(4096) LaneG {
     LaneCnt cnt[2];
     int utt, T, nf, s, cur, n_live, status, died_at, steps_run, done, tbucket;
     u32 tst;
@@ -83,18 +94,16 @@ struct LaneG {
 };
 
 struct WaveDev {
-    // Per-lane recombination table, open addressing with linear probing (identity mapping when
-    // the whole state space fits): compact, so it stays L2-resident and is reused every step.
-    u32 *hst;            // [W][H] state of an entry (EMPTY_STATE = free)
-    Slot *hslot;         // [W][H] {cost key, arc+1, payload}
-    u32 *hcand;          // [W][H] candidate index of an entry (this step)
-    u32 *hqtag;          // [W][H] epsilon frontier dedup tags (epsilon graphs)
-    u32 *cand_ent;       // [W][cap] table entry of a candidate (append order)
+    Slot *slot;          // [W][S] recombination slots {cost key, arc+1, payload} (EMPTY between steps)
+    u32 *cand_of;        // [W][S] candidate index of a state this step (epsilon graphs)
+    u32 *qtag;           // [W][S] epsilon frontier dedup tags (epsilon graphs)
+    u32 *log_dst, *log_arc, *log_pay;  // [W][logcap] emitting relaxations of the step
+    u64 *log_key;        // [W][logcap]
     u32 *cand_state;     // [W][cap]
     u32 *cand_arc, *cand_pay;  // [W][cap] winner arc + 1, payload (after the gather)
     u32 *ca_idx;         // [W][cap] backpointer record of a kept candidate (CA_NONE = dropped)
     u64 *cand_key;       // [W][cap]
-    u32 *front;          // [W][2][cap] frontier entries
+    u32 *front;          // [W][2][cap] frontier states
     int4 *tok_info;      // [W][2][cap] {state, trace, emit_lo, emit_hi}
     double *tok_cost;    // [W][2][cap]
     int *frames;         // [W][T_cap]
@@ -107,17 +116,12 @@ struct WaveDev {
     u64 arena_cap;
     u64 *arena_ctr;
     long long S;
-    int cap, T_cap, W, first_utt;
-    int hlog2, dense;    // table size 2^hlog2; dense = identity mapping (S <= H)
+    int cap, logcap, T_cap, W, first_utt;
 };
 
-constexpr u32 EMPTY_STATE = 0xFFFFFFFFu;
-
-__device__ __forceinline__ size_t lho(const WaveDev &ws, int w) { return (size_t)w << ws.hlog2; }
-__device__ __forceinline__ u32 hhash(const WaveDev &ws, u32 d) {
-    return ws.dense ? d : (d * 0x9E3779B1u) >> (32 - ws.hlog2);
-}
+__device__ __forceinline__ size_t lso(const WaveDev &ws, int w) { return (size_t)w * (size_t)ws.S; }
 __device__ __forceinline__ size_t lco(const WaveDev &ws, int w) { return (size_t)w * (size_t)ws.cap; }
+__device__ __forceinline__ size_t llo(const WaveDev &ws, int w) { return (size_t)w * (size_t)ws.logcap; }
 
 __device__ __forceinline__ int bucket_of(double cst, double best, double scale) {
     double v = __dmul_rn(__dsub_rn(cst, best), scale);
@@ -251,10 +255,11 @@ __device__ __forceinline__ u64 warp_reserve64(u64 *ctr, bool want) {
     return base + __popc(m & lanemask_lt());
 }
 
-// Register states whose table entry was claimed this step (warp-converged call): candidate
+// Register states installed for the first time this step (warp-converged call): candidate
 // index from one atomic per warp; `rng` = the state's {eps_lo, emit_lo, emit_hi} from the arc
-// record; states with epsilon arcs join the frontier when `push`.
-__device__ __forceinline__ void warp_append(bool first, u32 ent, int4 rng, bool push, int w,
+// record; states with epsilon arcs record their candidate index and, if `push`, join the
+// epsilon frontier.
+__device__ __forceinline__ void warp_append(bool first, u32 d, int4 rng, bool push, int w,
                                             const GraphDev &g, const WaveDev &ws, LaneG &L,
                                             int par, u32 *front_out, u32 *front_ctr) {
     u32 m;
@@ -263,9 +268,11 @@ __device__ __forceinline__ void warp_append(bool first, u32 ent, int4 rng, bool 
     bool pf = false;
     if (first) {
         if ((int)idx < ws.cap) {
-            ws.cand_ent[lco(ws, w) + idx] = ent;
-            ws.hcand[lho(ws, w) + ent] = idx;
-            pf = push && g.has_eps && rng.x < rng.y;
+            ws.cand_state[lco(ws, w) + idx] = d;
+            if (g.has_eps && rng.x < rng.y) {
+                ws.cand_of[lso(ws, w) + d] = idx;
+                pf = push;
+            }
         } else {
             L.status = WB_ERR_CAPACITY;
         }
@@ -275,22 +282,9 @@ __device__ __forceinline__ void warp_append(bool first, u32 ent, int4 rng, bool 
         u32 f = warp_reserve(front_ctr, pf, &mf);
         if (mf && (threadIdx.x & 31) == (u32)(__ffs(mf) - 1)) atomicAdd(&ws.gctr[0], (u32)__popc(mf));
         if (pf) {
-            if ((int)f < ws.cap) front_out[f] = ent;
+            if ((int)f < ws.cap) front_out[f] = d;
             else L.status = WB_ERR_CAPACITY;
         }
-    }
-}
-
-// Find or claim the table entry of state d (first probe already attempted: `old` = value the
-// probe CAS at h returned).  Returns the entry, or -1 when the table is full.
-__device__ __forceinline__ int table_resolve(u32 *hst, u32 mask, u32 h, u32 d, u32 old,
-                                             bool *claimed) {
-    for (u32 probe = 0;; ++probe) {
-        if (old == EMPTY_STATE) { *claimed = true; return (int)h; }
-        if (old == d) { *claimed = false; return (int)h; }
-        if (probe >= mask) return -1;
-        h = (h + 1) & mask;
-        old = atomicCAS(&hst[h], EMPTY_STATE, d);
     }
 }
 
@@ -305,7 +299,9 @@ __device__ __forceinline__ void warp_minmax(LaneCnt &cn, bool ok, u64 key) {
     }
 }
 
-// ------------------------------------------------------------------ P1: emitting expansion
+// ------------------------------------------------------------------ E1: emitting expansion
+// Fire-and-forget 64-bit atomicMin of every relaxation's cost key into its slot, plus a log
+// entry (dst, key, arc + 1, payload) per relaxation.
 template <int BLOCK>
 __noinline__ __device__ void phase_expand(const GraphDev &g, const WaveDev &ws,
                                           const BatchDev &b, const CfgDev &cfg, int par,
@@ -316,8 +312,6 @@ __noinline__ __device__ void phase_expand(const GraphDev &g, const WaveDev &ws,
         const LaneG &L = ws.lane[w];
         return L.done ? 0 : L.n_live;
     }, sh);
-    const Slot empty = {EMPTY_KEY, 0xFFFFFFFFu, 0xFFFFFFFFu};
-    const u32 mask = (1u << ws.hlog2) - 1u;
     for (int ch = blockIdx.x * NW + (threadIdx.x >> 5); ch < total; ch += gridDim.x * NW) {
         const int w = chunk_lane(sh.pre, W, (u32)ch);
         LaneG &L = ws.lane[w];
@@ -326,9 +320,8 @@ __noinline__ __device__ void phase_expand(const GraphDev &g, const WaveDev &ws,
         const int f = cfg.mode == 1 ? ws.frames[(size_t)w * ws.T_cap + L.s] : L.s;
         const double *row = b.costs + (size_t)(L.row0 + f) * b.L1;
         const size_t co2 = 2 * lco(ws, w) + (size_t)cur * ws.cap;
-        u32 *hst = ws.hst + lho(ws, w);
-        Slot *hslot = ws.hslot + lho(ws, w);
-        u32 *front0 = ws.front + 2 * lco(ws, w);
+        Slot *slot = ws.slot + lso(ws, w);
+        const size_t lo_ = llo(ws, w);
         const int t = (int)(ch - sh.pre[w]) * 32 + l;
         int4 ti = make_int4(0, 0, 0, 0);
         double tc = 0.0;
@@ -340,7 +333,8 @@ __noinline__ __device__ void phase_expand(const GraphDev &g, const WaveDev &ws,
         u32 nfin = 0;
         for (int j0 = 0; j0 < tot; j0 += 32 * U) {
             int4 rec[U];
-            Slot want[U];
+            u32 arcp1[U], pay[U];
+            double cst[U];
             bool act[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -348,17 +342,18 @@ __noinline__ __device__ void phase_expand(const GraphDev &g, const WaveDev &ws,
                 int k = warp_owner(excl, j);
                 int lo_k = __shfl_sync(FULL, ti.z, k);
                 int ex_k = __shfl_sync(FULL, excl, k);
-                double cst = __shfl_sync(FULL, tc, k);
-                want[u].pay = (u32)__shfl_sync(FULL, ti.y, k);
+                cst[u] = __shfl_sync(FULL, tc, k);
+                pay[u] = (u32)__shfl_sync(FULL, ti.y, k);
                 act[u] = j < tot;
                 int arc = lo_k + j - ex_k;
-                want[u].arcp1 = (u32)arc + 1u;
+                arcp1[u] = (u32)arc + 1u;
                 if (act[u]) rec[u] = __ldg(&g.arcs[2 * arc]);
-                want[u].key = (u64)__double_as_longlong(cst);  // carry the token cost
             }
-            u32 hq[U], oq[U];
+            u64 key[U];
+            u32 nact = 0;
 #pragma unroll
             for (int u = 0; u < U; ++u) {
+                key[u] = EMPTY_KEY;
                 if (!act[u]) continue;
                 double ac = __ldg(&row[rec[u].y]);
                 if (ac == INFINITY) {  // decoder.py:219-220: no relaxation, no record
@@ -366,34 +361,29 @@ __noinline__ __device__ void phase_expand(const GraphDev &g, const WaveDev &ws,
                     continue;
                 }
                 double wgt = __hiloint2double(rec[u].w, rec[u].z);
-                double cst = __longlong_as_double((long long)want[u].key);
-                want[u].key = cost_key(__dadd_rn(__dadd_rn(cst, wgt), ac));
-                hq[u] = hhash(ws, (u32)rec[u].x);
-                oq[u] = atomicCAS(&hst[hq[u]], EMPTY_STATE, (u32)rec[u].x);  // probe / claim
+                key[u] = cost_key(__dadd_rn(__dadd_rn(cst[u], wgt), ac));
+                atomicMin(&slot[rec[u].x].key, key[u]);  // RED.MIN.64: no return, no wait
+                ++nact;
             }
-            bool claimed[U];
-            Slot prev[U];
+            // log the relaxations: one reservation per warp iteration
+            const u32 wn = (u32)warp_sum_ll((long long)nact);
+            u32 base = 0;
+            if (l == 0 && wn) base = atomicAdd((u32 *)&cn.n_log, wn);
+            base = __shfl_sync(FULL, base, 0);
+            u32 off = (u32)(warp_incl_scan((int)nact) - (int)nact);
+            nfin += nact;
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                claimed[u] = false;
                 if (!act[u]) continue;
-                int e = table_resolve(hst, mask, hq[u], (u32)rec[u].x, oq[u], &claimed[u]);
-                if (e < 0) { L.status = WB_ERR_CAPACITY; act[u] = false; continue; }
-                hq[u] = (u32)e;
-                prev[u] = cas_slot(&hslot[e], empty, want[u]);
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                bool first = false, dec = false, ok = false;
-                if (act[u]) {
-                    ++nfin;
-                    ok = finish_relax(&hslot[hq[u]], want[u], prev[u], &first, &dec);
+                const u32 e = base + off++;
+                if ((int)e < ws.logcap) {
+                    ws.log_dst[lo_ + e] = (u32)rec[u].x;
+                    ws.log_key[lo_ + e] = key[u];
+                    ws.log_arc[lo_ + e] = arcp1[u];
+                    ws.log_pay[lo_ + e] = pay[u];
+                } else {
+                    L.status = WB_ERR_CAPACITY;
                 }
-                warp_minmax(cn, ok, want[u].key);
-                int4 r1 = make_int4(0, 0, 0, 0);
-                if (g.has_eps && claimed[u]) r1 = __ldg(&g.arcs[2 * (want[u].arcp1 - 1u) + 1]);
-                warp_append(claimed[u], hq[u], r1, true, w, g, ws, L, par, front0,
-                            (u32 *)&cn.nfront[0]);
             }
         }
         u32 tot_fin = (u32)warp_sum_ll((long long)nfin);
@@ -404,10 +394,77 @@ __noinline__ __device__ void phase_expand(const GraphDev &g, const WaveDev &ws,
     }
 }
 
+// ------------------------------------------------------------------ E2 / E3: exact ties + winners
+// E2 (tie): relaxations whose key equals the slot minimum atomicMin their arc + 1 into it.
+// E3 (win): the relaxation matching (key, arc + 1) is the unique winner: it stores its
+// payload and registers the state as a candidate (round-0 epsilon frontier if it has
+// epsilon arcs).  Lane min / max keys are taken over the winners.
+template <int BLOCK>
+__noinline__ __device__ void phase_emit_resolve(const GraphDev &g, const WaveDev &ws, int par,
+                                                bool win, Smem<BLOCK> &sh) {
+    constexpr int NW = BLOCK / 32;
+    const int W = ws.W, l = threadIdx.x & 31;
+    const int total = lane_chunks<BLOCK>(W, [&](int w) {
+        const LaneG &L = ws.lane[w];
+        return L.done ? 0 : min(L.cnt[par].n_log, ws.logcap);
+    }, sh);
+    const int gw = blockIdx.x * NW + (threadIdx.x >> 5), nwarps = gridDim.x * NW;
+    for (int c0 = gw * GC; c0 < total; c0 += nwarps * GC) {
+        int wq[GC];
+        u32 dq[GC], aq[GC];
+        u64 kq[GC];
+        Slot sq[GC];
+#pragma unroll
+        for (int q = 0; q < GC; ++q) {
+            const int ch = c0 + q;
+            wq[q] = -1;
+            if (ch < total) {
+                const int w = chunk_lane(sh.pre, W, (u32)ch);
+                const int i = (int)(ch - sh.pre[w]) * 32 + l;
+                if (i < min(ws.lane[w].cnt[par].n_log, ws.logcap)) {
+                    const size_t e = llo(ws, w) + i;
+                    wq[q] = w;
+                    dq[q] = ws.log_dst[e];
+                    kq[q] = ws.log_key[e];
+                    aq[q] = ws.log_arc[e];
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < GC; ++q)
+            if (wq[q] >= 0) sq[q] = ld_slot(&ws.slot[lso(ws, wq[q]) + dq[q]]);
+        if (!win) {
+#pragma unroll
+            for (int q = 0; q < GC; ++q)
+                if (wq[q] >= 0 && sq[q].key == kq[q] && aq[q] < sq[q].arcp1)
+                    atomicMin(&ws.slot[lso(ws, wq[q]) + dq[q]].arcp1, aq[q]);
+            continue;
+        }
+#pragma unroll
+        for (int q = 0; q < GC; ++q) {
+            const int ch = c0 + q;
+            if (ch >= total) break;  // warp-uniform
+            const int w = chunk_lane(sh.pre, W, (u32)ch);
+            LaneG &L = ws.lane[w];
+            LaneCnt &cn = L.cnt[par];
+            const bool first = wq[q] >= 0 && sq[q].key == kq[q] && sq[q].arcp1 == aq[q];
+            int4 r1 = make_int4(0, 0, 0, 0);
+            if (first) {
+                const size_t e = llo(ws, w) + (size_t)(ch - (int)sh.pre[w]) * 32 + l;
+                ws.slot[lso(ws, w) + dq[q]].pay = ws.log_pay[e];
+                if (g.has_eps) r1 = __ldg(&g.arcs[2 * (aq[q] - 1u) + 1]);
+            }
+            warp_minmax(cn, first, kq[q]);
+            warp_append(first, dq[q], r1, true, w, g, ws, L, par,
+                        ws.front + 2 * lco(ws, w), (u32 *)&cn.nfront[0]);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ P2: epsilon closure round
 // Round r reads frontier buffer r&1 (size nfront[r%3]) and pushes into buffer (r+1)&1
 // (nfront[(r+1)%3]); nfront[(r+2)%3] and gctr[(r+2)%3] are zeroed for round r+1.  Frontier
-// entries are table entries; an epsilon winner's payload is its source entry | EPS_BIT.
+// entries are states; an epsilon winner's payload is its source state | EPS_BIT.
 template <int BLOCK>
 __noinline__ __device__ void phase_eps_round(const GraphDev &g, const WaveDev &ws, int par,
                                              int r, u32 tag, Smem<BLOCK> &sh) {
@@ -423,25 +480,22 @@ __noinline__ __device__ void phase_eps_round(const GraphDev &g, const WaveDev &w
         return L.done ? 0 : min(L.cnt[par].nfront[rin], ws.cap);
     }, sh);
     const Slot empty = {EMPTY_KEY, 0xFFFFFFFFu, 0xFFFFFFFFu};
-    const u32 mask = (1u << ws.hlog2) - 1u;
     for (int ch = blockIdx.x * NW + (threadIdx.x >> 5); ch < total; ch += gridDim.x * NW) {
         const int w = chunk_lane(sh.pre, W, (u32)ch);
         LaneG &L = ws.lane[w];
         LaneCnt &cn = L.cnt[par];
         const int nfr = min(cn.nfront[rin], ws.cap);
-        u32 *hst = ws.hst + lho(ws, w);
-        Slot *hslot = ws.hslot + lho(ws, w);
+        Slot *slot = ws.slot + lso(ws, w);
         const size_t co = lco(ws, w);
         const u32 *fin = ws.front + 2 * co + (size_t)(r & 1) * ws.cap;
         u32 *fout = ws.front + 2 * co + (size_t)((r + 1) & 1) * ws.cap;
         const int i = (int)(ch - sh.pre[w]) * 32 + l;
-        u32 ue = 0, uu = 0;
+        u32 uu = 0;
         int lo = 0, deg = 0;
         double ucost = 0.0;
         if (i < nfr) {
-            ue = fin[i];
-            uu = __ldcg(&hst[ue]);
-            Slot us = ld_slot(&hslot[ue]);
+            uu = fin[i];
+            Slot us = ld_slot(&slot[uu]);
             int4 rg = us.arcp1 == 0u ? g.start_rng : __ldg(&g.arcs[2 * (us.arcp1 - 1u) + 1]);
             lo = rg.x;
             deg = rg.y - rg.x;
@@ -458,7 +512,6 @@ __noinline__ __device__ void phase_eps_round(const GraphDev &g, const WaveDev &w
             int ex_k = __shfl_sync(FULL, excl, k);
             double uc_k = __shfl_sync(FULL, ucost, k);
             u32 u_k = __shfl_sync(FULL, uu, k);
-            u32 ue_k = __shfl_sync(FULL, ue, k);
             bool act = j < tot;
             int a = lo_k + j - ex_k;
             int4 rec = make_int4(0, 0, 0, 0);
@@ -466,38 +519,29 @@ __noinline__ __device__ void phase_eps_round(const GraphDev &g, const WaveDev &w
                 rec = __ldg(&g.arcs[2 * a]);
                 if ((u32)rec.x == u_k) act = false;  // a positive self-loop never improves its state
             }
-            bool first = false, dec = false, ok = false, claimed = false;
-            int e = 0;
+            bool first = false, dec = false, ok = false;
             Slot want;
             want.key = EMPTY_KEY;
             if (act) {
                 ++neps;
                 want.key = cost_key(__dadd_rn(uc_k, __hiloint2double(rec.w, rec.z)));
                 want.arcp1 = (u32)a + 1u;
-                want.pay = ue_k | EPS_BIT;  // epsilon winner: payload = source entry
-                u32 h = hhash(ws, (u32)rec.x);
-                u32 old = atomicCAS(&hst[h], EMPTY_STATE, (u32)rec.x);
-                e = table_resolve(hst, mask, h, (u32)rec.x, old, &claimed);
-                if (e < 0) {
-                    L.status = WB_ERR_CAPACITY;
-                    claimed = false;
-                } else {
-                    Slot prev = cas_slot(&hslot[e], empty, want);
-                    ok = finish_relax(&hslot[e], want, prev, &first, &dec);
-                }
+                want.pay = u_k | EPS_BIT;  // epsilon winner: payload = source state
+                Slot prev = cas_slot(&slot[rec.x], empty, want);
+                ok = finish_relax(&slot[rec.x], want, prev, &first, &dec);
             }
             warp_minmax(cn, ok, want.key);
             int4 r1 = make_int4(0, 0, 0, 0);
             if (ok && dec) r1 = __ldg(&g.arcs[2 * a + 1]);
-            warp_append(claimed, (u32)e, r1, false, w, g, ws, L, par, fout, nullptr);
-            // entries that are new or got cheaper re-relax their epsilon arcs next round
+            warp_append(first, (u32)rec.x, r1, false, w, g, ws, L, par, fout, nullptr);
+            // states that are new or got cheaper re-relax their epsilon arcs next round
             bool push = ok && dec && r1.x < r1.y &&
-                        atomicExch(&ws.hqtag[lho(ws, w) + e], tag) != tag;
+                        atomicExch(&ws.qtag[lso(ws, w) + rec.x], tag) != tag;
             u32 mp;
             u32 fidx = warp_reserve((u32 *)&cn.nfront[rout], push, &mp);
             if (mp && l == __ffs(mp) - 1) atomicAdd(&ws.gctr[rout], (u32)__popc(mp));
             if (push) {
-                if ((int)fidx < ws.cap) fout[fidx] = (u32)e;
+                if ((int)fidx < ws.cap) fout[fidx] = (u32)rec.x;
                 else L.status = WB_ERR_CAPACITY;
             }
         }
@@ -507,11 +551,9 @@ __noinline__ __device__ void phase_eps_round(const GraphDev &g, const WaveDev &w
 }
 
 // ------------------------------------------------------------------ P3: gather + histogram
-constexpr int GC = 4;  // chunks per warp iteration in the per-candidate phases (loads in flight)
-
 template <int BLOCK>
-__noinline__ __device__ void phase_gather(const GraphDev &g, const WaveDev &ws, const CfgDev &cfg, int par,
-                             Smem<BLOCK> &sh) {
+__noinline__ __device__ void phase_gather(const GraphDev &g, const WaveDev &ws,
+                                          const CfgDev &cfg, int par, Smem<BLOCK> &sh) {
     constexpr int NW = BLOCK / 32;
     const int W = ws.W, l = threadIdx.x & 31;
     const int total = lane_chunks<BLOCK>(W, [&](int w) {
@@ -521,7 +563,7 @@ __noinline__ __device__ void phase_gather(const GraphDev &g, const WaveDev &ws, 
     const int gw = blockIdx.x * NW + (threadIdx.x >> 5), nwarps = gridDim.x * NW;
     for (int c0 = gw * GC; c0 < total; c0 += nwarps * GC) {
         int wq[GC], iq[GC];
-        u32 eq[GC], st[GC];
+        u32 st[GC];
         Slot v[GC];
 #pragma unroll
         for (int q = 0; q < GC; ++q) {
@@ -534,16 +576,13 @@ __noinline__ __device__ void phase_gather(const GraphDev &g, const WaveDev &ws, 
                 if (i < min(ws.lane[w].cnt[par].n_cand, ws.cap)) {
                     wq[q] = w;
                     iq[q] = i;
-                    eq[q] = ws.cand_ent[lco(ws, w) + i];
+                    st[q] = ws.cand_state[lco(ws, w) + i];
                 }
             }
         }
 #pragma unroll
         for (int q = 0; q < GC; ++q)
-            if (wq[q] >= 0) {
-                st[q] = __ldcg(&ws.hst[lho(ws, wq[q]) + eq[q]]);
-                v[q] = ld_slot(&ws.hslot[lho(ws, wq[q]) + eq[q]]);
-            }
+            if (wq[q] >= 0) v[q] = ld_slot(&ws.slot[lso(ws, wq[q]) + st[q]]);
 #pragma unroll
         for (int q = 0; q < GC; ++q) {
             const int ch = c0 + q;
@@ -554,7 +593,6 @@ __noinline__ __device__ void phase_gather(const GraphDev &g, const WaveDev &ws, 
             bool in = false;
             if (wq[q] >= 0) {
                 const size_t co = lco(ws, w) + iq[q];
-                ws.cand_state[co] = st[q];
                 ws.cand_key[co] = v[q].key;
                 ws.cand_arc[co] = v[q].arcp1;
                 ws.cand_pay[co] = v[q].pay;
@@ -716,8 +754,8 @@ __device__ __forceinline__ bool survives(u64 k, u32 st, const Beam &bm, const La
 // to its source candidate's record (written in P8); sources that are not survivors themselves
 // are claimed here (CAS on their record slot) so exactly one thread records each.
 template <int BLOCK>
-__noinline__ __device__ void phase_survive(const GraphDev &g, const WaveDev &ws, const CfgDev &cfg, int par,
-                              Smem<BLOCK> &sh) {
+__noinline__ __device__ void phase_survive(const GraphDev &g, const WaveDev &ws,
+                                           const CfgDev &cfg, int par, Smem<BLOCK> &sh) {
     constexpr int NW = BLOCK / 32;
     const int W = ws.W, l = threadIdx.x & 31;
     const int total = lane_chunks<BLOCK>(W, [&](int w) {
@@ -776,10 +814,10 @@ __noinline__ __device__ void phase_survive(const GraphDev &g, const WaveDev &ws,
                 continue;
             }
             // epsilon winner: claim the non-surviving candidates of its epsilon chain
-            u32 src = p & ~EPS_BIT;  // source table entry
+            u32 src = p & ~EPS_BIT;  // source state
             for (;;) {
-                const u32 uc = ws.hcand[lho(ws, w) + src];
-                if (survives(ws.cand_key[co + uc], ws.cand_state[co + uc], bm, L, need)) break;
+                const u32 uc = ws.cand_of[lso(ws, w) + src];
+                if (survives(ws.cand_key[co + uc], src, bm, L, need)) break;  // own thread records it
                 if (atomicCAS(&ws.ca_idx[co + uc], CA_NONE, CA_CLAIM) != CA_NONE) break;
                 const u64 ru = atomicAdd(ws.arena_ctr, 1ull);
                 atomicAdd(&cn.n_rec, 1ull);
@@ -798,14 +836,14 @@ __noinline__ __device__ void phase_survive(const GraphDev &g, const WaveDev &ws,
 
 // ------------------------------------------------------------------ P8: epsilon links + lanes
 template <int BLOCK>
-__noinline__ __device__ void phase_link(const GraphDev &g, const WaveDev &ws, const CfgDev &cfg, int k,
-                           Smem<BLOCK> &sh) {
+__noinline__ __device__ void phase_link(const GraphDev &g, const WaveDev &ws, const CfgDev &cfg,
+                                        int k, Smem<BLOCK> &sh) {
     constexpr int NW = BLOCK / 32;
     const int par = k & 1;
     const bool search_step = k > 0;
     const int W = ws.W, l = threadIdx.x & 31;
     {
-        // epsilon-winner records (their source's record index is final now) and the table
+        // epsilon-winner records (their source's record index is final now) and the slot
         // reset O(touched) for the next step
         const int total = lane_chunks<BLOCK>(W, [&](int w) {
             const LaneG &L = ws.lane[w];
@@ -813,7 +851,7 @@ __noinline__ __device__ void phase_link(const GraphDev &g, const WaveDev &ws, co
         }, sh);
         const int gw = blockIdx.x * NW + (threadIdx.x >> 5), nwarps = gridDim.x * NW;
         for (int c0 = gw * GC; c0 < total; c0 += nwarps * GC) {
-            u32 aq[GC], pq[GC], rq[GC], eq[GC];
+            u32 aq[GC], pq[GC], rq[GC], sq[GC];
             int wq[GC];
 #pragma unroll
             for (int q = 0; q < GC; ++q) {
@@ -825,7 +863,7 @@ __noinline__ __device__ void phase_link(const GraphDev &g, const WaveDev &ws, co
                     if (i < min(ws.lane[w].cnt[par].n_cand, ws.cap)) {
                         const size_t co = lco(ws, w) + i;
                         wq[q] = w;
-                        eq[q] = ws.cand_ent[co];
+                        sq[q] = ws.cand_state[co];
                         rq[q] = ws.ca_idx[co];
                         aq[q] = ws.cand_arc[co];
                         pq[q] = ws.cand_pay[co];
@@ -837,11 +875,10 @@ __noinline__ __device__ void phase_link(const GraphDev &g, const WaveDev &ws, co
                 if (wq[q] < 0) continue;
                 const int w = wq[q];
                 if (rq[q] < CA_CLAIM && aq[q] != 0u && (pq[q] & EPS_BIT)) {
-                    const u32 uc = ws.hcand[lho(ws, w) + (pq[q] & ~EPS_BIT)];
+                    const u32 uc = ws.cand_of[lso(ws, w) + (pq[q] & ~EPS_BIT)];
                     ws.arena[rq[q]] = (u64)aq[q] | ((u64)ws.ca_idx[lco(ws, w) + uc] << 32);
                 }
-                ws.hst[lho(ws, w) + eq[q]] = EMPTY_STATE;
-                st_slot_empty(&ws.hslot[lho(ws, w) + eq[q]]);
+                st_slot_empty(&ws.slot[lso(ws, w) + sq[q]]);
             }
         }
     }
@@ -854,13 +891,14 @@ __noinline__ __device__ void phase_link(const GraphDev &g, const WaveDev &ws, co
         nx.nfront[0] = nx.nfront[1] = nx.nfront[2] = 0;
         nx.n_surv = 0;
         nx.need = 0;
+        nx.n_log = 0;
         nx.kept = 0;
         nx.kmin = EMPTY_KEY;
         nx.khi = 0;
         nx.n_rec = 0;
         if (L.done) continue;
         const int n = min(cn.n_cand, ws.cap);
-        if (cn.n_cand > ws.cap) L.status = WB_ERR_CAPACITY;
+        if (cn.n_cand > ws.cap || cn.n_log > ws.logcap) L.status = WB_ERR_CAPACITY;
         L.n_cand_tot += n;
         L.n_rec_tot += cn.n_rec;
         if (!search_step) {  // initial tokens (decoder.py:236-249)
@@ -958,26 +996,25 @@ wave_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WaveDev 
                 cn.nfront[0] = cn.nfront[1] = cn.nfront[2] = 0;
                 cn.n_surv = 0;
                 cn.need = 0;
+                cn.n_log = 0;
                 cn.kept = 0;
                 cn.kmin = EMPTY_KEY;
                 cn.khi = 0;
                 cn.n_rec = 0;
             }
             if (real) {
-                // start entry (0.0, src -1, arc -1, ROOT) (decoder.py:241); tables are empty
-                const size_t ho = lho(ws, w), co = lco(ws, w);
-                const u32 e = hhash(ws, (u32)g.start);
+                // start entry (0.0, src -1, arc -1, ROOT) (decoder.py:241); slots are EMPTY
+                const size_t so = lso(ws, w), co = lco(ws, w);
                 const u64 k0 = cost_key(0.0);
-                ws.hst[ho + e] = (u32)g.start;
-                __stcg(reinterpret_cast<ulonglong2 *>(&ws.hslot[ho + e]),
+                __stcg(reinterpret_cast<ulonglong2 *>(&ws.slot[so + g.start]),
                        make_ulonglong2(k0, (u64)0u | ((u64)ROOT_PREV << 32)));
-                ws.hcand[ho + e] = 0u;
-                ws.cand_ent[co] = e;
+                ws.cand_state[co] = (u32)g.start;
                 L.cnt[0].n_cand = 1;
                 L.cnt[0].kmin = k0;
                 L.cnt[0].khi = k0;
                 if (g.has_eps && g.start_rng.x < g.start_rng.y) {
-                    ws.front[2 * co] = e;
+                    ws.cand_of[so + g.start] = 0u;
+                    ws.front[2 * co] = (u32)g.start;
                     L.cnt[0].nfront[0] = 1;
                     atomicAdd(&ws.gctr[0], 1u);
                 }
@@ -991,10 +1028,14 @@ wave_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WaveDev 
     u32 tag = ws.gctr[9];
     for (int k = 0;; ++k) {
         const int par = k & 1;
-        const bool search = k > 0;
-        if (search) {
+        if (k > 0) {
             if (ws.gctr[6 + (k % 3)] == 0) break;  // no active lane left
             phase_expand<BLOCK>(g, ws, b, cfg, par, sh);
+            grid.sync();
+            phase_tick(ws, sh, 0);
+            phase_emit_resolve<BLOCK>(g, ws, par, false, sh);
+            grid.sync();
+            phase_emit_resolve<BLOCK>(g, ws, par, true, sh);
             grid.sync();
             phase_tick(ws, sh, 1);
         }

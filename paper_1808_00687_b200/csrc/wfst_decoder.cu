@@ -36,7 +36,7 @@ static int set_err(int code, const std::string &msg) {
 
 struct wb_graph_s {
     int device = 0;
-    int S = 0, A = 0, start = 0, has_eps = 0, max_ilabel = 0;
+    int S = 0, A = 0, start = 0, has_eps = 0, max_ilabel = 0, max_emit_deg = 0;
     int4 start_rng{0, 0, 0, 0};
     int4 *arcs = nullptr;      // [2*A] 32-byte arc records
     double *final_w = nullptr;
@@ -47,11 +47,12 @@ struct wb_decoder_s {
     wb_graph_s *g = nullptr;
     int W = 0, cap = 0, T_cap = 0, block = 512, num_sms = 0, grid = 0;
     u64 arena_cap = 0;
-    int hlog2 = 0, dense = 0;
-    u32 *hst = nullptr, *hcand = nullptr, *hqtag = nullptr;
-    Slot *hslot = nullptr;
-    u32 *cand_ent = nullptr, *cand_state = nullptr, *cand_arc = nullptr, *cand_pay = nullptr,
-        *ca_idx = nullptr;
+    int logcap = 0;
+    Slot *slot = nullptr;
+    u32 *cand_of = nullptr, *qtag = nullptr;
+    u32 *log_dst = nullptr, *log_arc = nullptr, *log_pay = nullptr;
+    u64 *log_key = nullptr;
+    u32 *cand_state = nullptr, *cand_arc = nullptr, *cand_pay = nullptr, *ca_idx = nullptr;
     u64 *cand_key = nullptr;
     u32 *front = nullptr;
     int4 *tok_info = nullptr;
@@ -93,11 +94,12 @@ int wb_graph_create(const wb_graph_desc *d, int32_t device, wb_graph_t *out) {
         return set_err(WB_ERR_VALUE, "bad graph dimensions");
     const int S = d->num_states, A = d->num_arcs;
     if (d->row_ptr[0] != 0 || d->row_ptr[S] != A) return set_err(WB_ERR_VALUE, "row_ptr mismatch");
-    int has_eps = 0, max_il = 0;
+    int has_eps = 0, max_il = 0, max_deg = 0;
     for (int s = 0; s < S; ++s) {
         int lo = d->row_ptr[s], mid = d->eps_end[s], hi = d->row_ptr[s + 1];
         if (lo > mid || mid > hi) return set_err(WB_ERR_VALUE, "eps_end outside the state's arc range");
         if (mid > lo) has_eps = 1;
+        max_deg = std::max(max_deg, hi - mid);
     }
     // 32-byte arc records: {dst, ilabel, weight} + the destination's {eps_lo, emit_lo, emit_hi}
     // and the olabel, so relaxation and first touch need no per-state lookups.
@@ -123,6 +125,7 @@ int wb_graph_create(const wb_graph_desc *d, int32_t device, wb_graph_t *out) {
     g->start = d->start;
     g->has_eps = has_eps;
     g->max_ilabel = max_il;
+    g->max_emit_deg = max_deg;
     g->start_rng = make_int4(d->row_ptr[d->start], d->eps_end[d->start], d->row_ptr[d->start + 1], 0);
     cudaError_t e = cudaMalloc(&g->arcs, sizeof(int4) * arcs.size());
     if (e == cudaSuccess) e = cudaMalloc(&g->final_w, sizeof(double) * S);
@@ -159,7 +162,8 @@ int wb_graph_device_bytes(wb_graph_t g, int64_t *bytes) {
 }  // extern "C"
 
 static void free_decoder(wb_decoder_s *d) {
-    void *ptrs[] = {d->hst, d->hslot, d->hcand, d->hqtag, d->cand_ent, d->cand_state, d->cand_arc,
+    void *ptrs[] = {d->slot, d->cand_of, d->qtag, d->log_dst, d->log_arc, d->log_pay,
+                    d->log_key, d->cand_state, d->cand_arc,
                     d->cand_pay, d->ca_idx, d->cand_key, d->front, d->tok_info,
                     d->tok_cost, d->frames, d->hist, d->lane, d->gctr, d->phase, d->arena,
                     d->arena_ctr, d->h_costs, d->h_blank, d->h_off, d->h_T, d->h_res, d->h_lab};
@@ -229,29 +233,20 @@ int wb_decoder_create(wb_graph_t g, const wb_decoder_opts *o, wb_decoder_t *out)
         return set_err(WB_ERR_CUDA, "wave kernel occupancy query failed");
     }
     d->grid = d->num_sms * std::min(occ, 2);
-    // recombination table per lane: next power of two >= S (identity mapping, no probing)
-    // when that is at most hash_entries, else a hash table of hash_entries (load <= ~0.7)
-    const int64_t hmax = opts.hash_entries > 0 ? opts.hash_entries : 32768;
-    int hl = 0;
-    while ((1ll << hl) < (int64_t)g->S) ++hl;
-    if ((1ll << hl) <= hmax) {
-        d->dense = 1;
-    } else {
-        d->dense = 0;
-        hl = 0;
-        while ((1ll << hl) < hmax) ++hl;
-    }
-    d->hlog2 = std::max(hl, 1);
-    d->cap = std::min(d->cap, d->dense ? g->S : (int)((1ll << d->hlog2) * 7 / 8));
-    size_t H = (size_t)1 << d->hlog2, W = (size_t)d->W, cap = (size_t)d->cap;
+    // relaxation log per lane: every emitting arc of every candidate of one step
+    d->logcap = (int)std::min<int64_t>((int64_t)d->cap * std::max(g->max_emit_deg, 1) + 1024,
+                                       (int64_t)1 << 30);
+    size_t S = (size_t)g->S, W = (size_t)d->W, cap = (size_t)d->cap, lcap = (size_t)d->logcap;
     size_t acc = 0;
     e = cudaSuccess;
 #define DA(p, n) if (e == cudaSuccess) e = dalloc(&d->p, (n), acc)
-    DA(hst, W * H);
-    DA(hslot, W * H);
-    DA(hcand, W * H);
-    DA(hqtag, g->has_eps ? W * H : 1);
-    DA(cand_ent, W * cap);
+    DA(slot, W * S);
+    DA(cand_of, g->has_eps ? W * S : 1);
+    DA(qtag, g->has_eps ? W * S : 1);
+    DA(log_dst, W * lcap);
+    DA(log_arc, W * lcap);
+    DA(log_pay, W * lcap);
+    DA(log_key, W * lcap);
     DA(cand_state, W * cap);
     DA(cand_arc, W * cap);
     DA(cand_pay, W * cap);
@@ -266,9 +261,8 @@ int wb_decoder_create(wb_graph_t g, const wb_decoder_opts *o, wb_decoder_t *out)
     DA(phase, 8);
     DA(arena_ctr, 1);
 #undef DA
-    if (e == cudaSuccess) e = cudaMemset(d->hst, 0xFF, sizeof(u32) * W * H);
-    if (e == cudaSuccess) e = cudaMemset(d->hslot, 0xFF, sizeof(Slot) * W * H);
-    if (e == cudaSuccess && g->has_eps) e = cudaMemset(d->hqtag, 0, sizeof(u32) * W * H);
+    if (e == cudaSuccess) e = cudaMemset(d->slot, 0xFF, sizeof(Slot) * W * S);
+    if (e == cudaSuccess && g->has_eps) e = cudaMemset(d->qtag, 0, sizeof(u32) * W * S);
     if (e == cudaSuccess) e = cudaMemset(d->hist, 0, sizeof(u32) * W * wave::NB);
     if (e == cudaSuccess) e = cudaMemset(d->gctr, 0, sizeof(u32) * 16);
     if (e == cudaSuccess) e = cudaEventCreate(&d->ev0);
@@ -373,9 +367,10 @@ int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row
     wave::CfgDev cd{cfg->beam, cfg->blank_threshold, cfg->max_active, cfg->mode, cfg->lattice};
     wave::WaveDev wd;
     std::memset(&wd, 0, sizeof(wd));
-    wd.hst = d->hst; wd.hslot = d->hslot; wd.hcand = d->hcand; wd.hqtag = d->hqtag;
-    wd.hlog2 = d->hlog2; wd.dense = d->dense;
-    wd.cand_ent = d->cand_ent; wd.cand_state = d->cand_state; wd.cand_arc = d->cand_arc;
+    wd.slot = d->slot; wd.cand_of = d->cand_of; wd.qtag = d->qtag;
+    wd.log_dst = d->log_dst; wd.log_arc = d->log_arc; wd.log_pay = d->log_pay;
+    wd.log_key = d->log_key; wd.logcap = d->logcap;
+    wd.cand_state = d->cand_state; wd.cand_arc = d->cand_arc;
     wd.cand_pay = d->cand_pay; wd.ca_idx = d->ca_idx;
     wd.cand_key = d->cand_key; wd.front = d->front; wd.tok_info = d->tok_info;
     wd.tok_cost = d->tok_cost; wd.frames = d->frames; wd.hist = d->hist; wd.lane = d->lane;

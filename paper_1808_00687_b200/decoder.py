@@ -187,7 +187,6 @@ class BatchDecoder:
         self.opts["cand_capacity"] = min(S, cap * 2)
         arena = self.opts["arena_capacity"] or (1 << 24)
         self.opts["arena_capacity"] = min(2**31 - 2, max(arena * 2, arena_need or 0))
-        self.opts["hash_entries"] = 2 * (self.opts["hash_entries"] or 32768)
         self._create()
 
     def device_bytes(self) -> int:
