@@ -215,7 +215,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--utts", type=int, default=0, help="utterances per GPU (default: config)")
     ap.add_argument("--frames", type=int, default=0, help="frames per utterance (default: config)")
-    ap.add_argument("--block", type=int, default=0, help="threads per CTA (0 = auto)")
+    ap.add_argument("--block", type=int, default=0, help="threads per CTA (0 = library default)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu)")
@@ -255,8 +255,8 @@ def main():
     fill_inputs(cfg, rank, T, off, L1, costs_h.numpy(), blank_h.numpy())
     dcfg = DecodeConfig(beam=cfg["beam"], max_active=cfg["max_active"], mode=cfg["mode"])
 
-    block = args.block or 512
-    dec = BatchDecoder(g, local, max_utts_in_flight=min(utts, 148), block_threads=block)
+    block = args.block or 1024
+    dec = BatchDecoder(g, local, max_utts_in_flight=min(utts, 148), block_threads=args.block)
     dec.reserve(int(T.sum()) + utts, cfg["max_active"], int(T.max()))
     cap = frames + 64
 

@@ -68,6 +68,23 @@ __device__ __forceinline__ Slot cas_slot(Slot *p, const Slot &expect, const Slot
     return o;
 }
 
+// Fire-and-forget reductions (REDG): the issuing warp does not wait for the L2 round trip.
+__device__ __forceinline__ void red_min_u64(u64 *p, u64 v) {
+    asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(p), "l"(v));
+}
+__device__ __forceinline__ void red_max_u64(u64 *p, u64 v) {
+    asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(p), "l"(v));
+}
+__device__ __forceinline__ void red_min_u32(u32 *p, u32 v) {
+    asm volatile("red.relaxed.gpu.global.min.u32 [%0], %1;" ::"l"(p), "r"(v));
+}
+__device__ __forceinline__ void red_add_u32(u32 *p, u32 v) {
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v));
+}
+__device__ __forceinline__ void red_add_u64(u64 *p, u64 v) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v));
+}
+
 __device__ __forceinline__ bool slot_better(u64 key, u32 arcp1, const Slot &cur) {
     return key < cur.key || (key == cur.key && arcp1 < cur.arcp1);
 }

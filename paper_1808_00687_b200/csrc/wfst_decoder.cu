@@ -10,14 +10,9 @@
 #include <vector>
 
 #include "../../include/wfst_b200.h"
-#include "wave_kernel.cuh"
+#include "decode_kernel.cuh"
 
 using namespace wb;
-using wb::wave::LaneG;
-
-#ifndef WB_WAVE_MINB
-#define WB_WAVE_MINB 1  // CTAs per SM the wave kernel is register-budgeted for
-#endif
 
 static thread_local std::string g_err;
 
@@ -36,7 +31,7 @@ static int set_err(int code, const std::string &msg) {
 
 struct wb_graph_s {
     int device = 0;
-    int S = 0, A = 0, start = 0, has_eps = 0, max_ilabel = 0, max_emit_deg = 0;
+    int S = 0, A = 0, start = 0, has_eps = 0, max_ilabel = 0;
     int4 start_rng{0, 0, 0, 0};
     int4 *arcs = nullptr;      // [2*A] 32-byte arc records
     double *final_w = nullptr;
@@ -45,25 +40,19 @@ struct wb_graph_s {
 
 struct wb_decoder_s {
     wb_graph_s *g = nullptr;
-    int W = 0, cap = 0, T_cap = 0, block = 512, num_sms = 0, grid = 0;
+    int slots = 0, cap = 0, T_cap = 0, block = 0, num_sms = 0;
     u64 arena_cap = 0;
-    int logcap = 0;
     Slot *slot = nullptr;
-    u32 *cand_of = nullptr, *qtag = nullptr;
-    u32 *log_dst = nullptr, *log_arc = nullptr, *log_pay = nullptr;
-    u64 *log_key = nullptr;
-    u32 *cand_state = nullptr, *cand_arc = nullptr, *cand_pay = nullptr, *ca_idx = nullptr;
+    u32 *cand_of = nullptr, *qtag = nullptr, *tag_ctr = nullptr;
+    u32 *cand_state = nullptr, *cand_arc = nullptr, *cand_pay = nullptr, *cand_ca = nullptr;
+    int4 *cand_rng = nullptr;
     u64 *cand_key = nullptr;
     u32 *front = nullptr;
     int4 *tok_info = nullptr;
     double *tok_cost = nullptr;
     int *frames = nullptr;
-    u32 *hist = nullptr;
-    LaneG *lane = nullptr;
-    u32 *gctr = nullptr;
-    long long *phase = nullptr;
     u64 *arena = nullptr;
-    u64 *arena_ctr = nullptr;
+    u64 *counters = nullptr;  // [0] arena_ctr, [1] utt_ctr (u32 in the low half)
     // host-mode staging buffers (grown on demand)
     double *h_costs = nullptr, *h_blank = nullptr;
     size_t h_costs_n = 0, h_blank_n = 0;
@@ -94,12 +83,11 @@ int wb_graph_create(const wb_graph_desc *d, int32_t device, wb_graph_t *out) {
         return set_err(WB_ERR_VALUE, "bad graph dimensions");
     const int S = d->num_states, A = d->num_arcs;
     if (d->row_ptr[0] != 0 || d->row_ptr[S] != A) return set_err(WB_ERR_VALUE, "row_ptr mismatch");
-    int has_eps = 0, max_il = 0, max_deg = 0;
+    int has_eps = 0, max_il = 0;
     for (int s = 0; s < S; ++s) {
         int lo = d->row_ptr[s], mid = d->eps_end[s], hi = d->row_ptr[s + 1];
         if (lo > mid || mid > hi) return set_err(WB_ERR_VALUE, "eps_end outside the state's arc range");
         if (mid > lo) has_eps = 1;
-        max_deg = std::max(max_deg, hi - mid);
     }
     // 32-byte arc records: {dst, ilabel, weight} + the destination's {eps_lo, emit_lo, emit_hi}
     // and the olabel, so relaxation and first touch need no per-state lookups.
@@ -125,7 +113,6 @@ int wb_graph_create(const wb_graph_desc *d, int32_t device, wb_graph_t *out) {
     g->start = d->start;
     g->has_eps = has_eps;
     g->max_ilabel = max_il;
-    g->max_emit_deg = max_deg;
     g->start_rng = make_int4(d->row_ptr[d->start], d->eps_end[d->start], d->row_ptr[d->start + 1], 0);
     cudaError_t e = cudaMalloc(&g->arcs, sizeof(int4) * arcs.size());
     if (e == cudaSuccess) e = cudaMalloc(&g->final_w, sizeof(double) * S);
@@ -162,11 +149,10 @@ int wb_graph_device_bytes(wb_graph_t g, int64_t *bytes) {
 }  // extern "C"
 
 static void free_decoder(wb_decoder_s *d) {
-    void *ptrs[] = {d->slot, d->cand_of, d->qtag, d->log_dst, d->log_arc, d->log_pay,
-                    d->log_key, d->cand_state, d->cand_arc,
-                    d->cand_pay, d->ca_idx, d->cand_key, d->front, d->tok_info,
-                    d->tok_cost, d->frames, d->hist, d->lane, d->gctr, d->phase, d->arena,
-                    d->arena_ctr, d->h_costs, d->h_blank, d->h_off, d->h_T, d->h_res, d->h_lab};
+    void *ptrs[] = {d->slot, d->cand_of, d->qtag, d->tag_ctr, d->cand_state, d->cand_rng,
+                    d->cand_arc, d->cand_pay, d->cand_key, d->cand_ca, d->front, d->tok_info,
+                    d->tok_cost, d->frames, d->arena, d->counters, d->h_costs, d->h_blank,
+                    d->h_off, d->h_T, d->h_res, d->h_lab};
     for (void *p : ptrs) cudaFree(p);
     if (d->ev0) cudaEventDestroy(d->ev0);
     if (d->ev1) cudaEventDestroy(d->ev1);
@@ -182,7 +168,7 @@ static int alloc_frames(wb_decoder_s *d, int T_cap) {
     cudaFree(d->frames);
     d->frames = nullptr;
     d->T_cap = std::max(T_cap, 1);
-    CUDA_TRY(cudaMalloc(&d->frames, sizeof(int) * (size_t)d->W * d->T_cap));
+    CUDA_TRY(cudaMalloc(&d->frames, sizeof(int) * (size_t)d->slots * d->T_cap));
     return WB_OK;
 }
 
@@ -192,6 +178,34 @@ static int alloc_arena(wb_decoder_s *d, u64 cap) {
     d->arena_cap = std::min<u64>(std::max<u64>(cap, 1024), (u64)EPS_BIT - 1);
     CUDA_TRY(cudaMalloc(&d->arena, sizeof(u64) * d->arena_cap));
     return WB_OK;
+}
+
+template <int BLOCK>
+static cudaError_t launch_decode(int max_grid, int num_sms, int num_cols, cudaStream_t st,
+                                 const GraphDev &gd, WorkDev wd, const BatchDev &bd,
+                                 const CfgDev &cd, wb_utt_result *res) {
+    // One lane per SM: dynamic shared memory holds the cost row during expansion, then the
+    // step's candidate keys + flags (as many as fit; larger steps spill to global memory).
+    size_t avail = 0;
+    cudaError_t e = cudaOccupancyAvailableDynamicSMemPerBlock(&avail, decode_kernel<BLOCK>, 1, BLOCK);
+    if (e != cudaSuccess) return e;
+    const size_t hdr = smem_hdr<BLOCK>();
+    avail = avail > 1024 + hdr ? avail - 1024 - hdr : 0;
+    size_t row = num_cols <= ROW_SMEM_MAX ? sizeof(double) * (size_t)num_cols : 0;
+    if (row > avail) row = 0;  // the kernel reads the row from global memory instead
+    wd.smem_cands = (int)std::min<size_t>(avail / (sizeof(u64) + sizeof(u32)), (size_t)wd.cap);
+    wd.row_in_smem = row > 0;
+    size_t smem = hdr + std::max(row, (size_t)wd.smem_cands * (sizeof(u64) + sizeof(u32)));
+    smem = (smem + 15) & ~(size_t)15;
+    e = cudaFuncSetAttribute(decode_kernel<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    if (e != cudaSuccess) return e;
+    int occ = 1;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decode_kernel<BLOCK>, BLOCK, smem);
+    if (e != cudaSuccess) return e;
+    int grid = std::min(max_grid, num_sms * std::max(occ, 1));
+    decode_kernel<BLOCK><<<grid, BLOCK, smem, st>>>(gd, wd, bd, cd, res);
+    return cudaGetLastError();
 }
 
 template <class T>
@@ -216,55 +230,39 @@ int wb_decoder_create(wb_graph_t g, const wb_decoder_opts *o, wb_decoder_t *out)
     if (o) opts = *o;
     cudaDeviceProp prop;
     CUDA_TRY(cudaGetDeviceProperties(&prop, g->device));
-    if (opts.block_threads && opts.block_threads != 512)
-        return set_err(WB_ERR_VALUE, "block_threads must be 512 (or 0 = auto)");
+    if (opts.block_threads && opts.block_threads != 256 && opts.block_threads != 512 &&
+        opts.block_threads != 1024)
+        return set_err(WB_ERR_VALUE, "block_threads must be 256, 512 or 1024 (or 0 = auto)");
     wb_decoder_s *d = new wb_decoder_s();
     d->g = g;
     d->num_sms = prop.multiProcessorCount;
-    // utterance lanes per wave: every phase of a step is spread over all SMs
-    d->W = opts.max_utts_in_flight > 0 ? opts.max_utts_in_flight : 64;
-    d->W = std::min(d->W, wave::MAXW);
+    d->block = opts.block_threads;
+    // one persistent lane per SM (the kernel's shared-memory candidate store fills an SM)
+    d->slots = opts.max_utts_in_flight > 0 ? opts.max_utts_in_flight : d->num_sms;
     d->cap = opts.cand_capacity > 0 ? opts.cand_capacity : std::min(g->S, 1 << 18);
     d->cap = std::max(1, std::min(d->cap, g->S));
-    int occ = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave::wave_kernel<512, WB_WAVE_MINB>, 512, 0);
-    if (e != cudaSuccess || occ < 1) {
-        delete d;
-        return set_err(WB_ERR_CUDA, "wave kernel occupancy query failed");
-    }
-    d->grid = d->num_sms * std::min(occ, 2);
-    // relaxation log per lane: every emitting arc of every candidate of one step
-    d->logcap = (int)std::min<int64_t>((int64_t)d->cap * std::max(g->max_emit_deg, 1) + 1024,
-                                       (int64_t)1 << 30);
-    size_t S = (size_t)g->S, W = (size_t)d->W, cap = (size_t)d->cap, lcap = (size_t)d->logcap;
+    size_t S = (size_t)g->S, slots = (size_t)d->slots, cap = (size_t)d->cap;
     size_t acc = 0;
-    e = cudaSuccess;
+    cudaError_t e = cudaSuccess;
 #define DA(p, n) if (e == cudaSuccess) e = dalloc(&d->p, (n), acc)
-    DA(slot, W * S);
-    DA(cand_of, g->has_eps ? W * S : 1);
-    DA(qtag, g->has_eps ? W * S : 1);
-    DA(log_dst, W * lcap);
-    DA(log_arc, W * lcap);
-    DA(log_pay, W * lcap);
-    DA(log_key, W * lcap);
-    DA(cand_state, W * cap);
-    DA(cand_arc, W * cap);
-    DA(cand_pay, W * cap);
-    DA(ca_idx, W * cap);
-    DA(cand_key, W * cap);
-    DA(front, W * 2 * cap);
-    DA(tok_info, W * 2 * cap);
-    DA(tok_cost, W * 2 * cap);
-    DA(hist, W * wave::NB);
-    DA(lane, W);
-    DA(gctr, 16);
-    DA(phase, 8);
-    DA(arena_ctr, 1);
+    DA(slot, slots * S);
+    DA(cand_of, g->has_eps ? slots * S : 1);
+    DA(qtag, g->has_eps ? slots * S : 1);
+    DA(tag_ctr, slots);
+    DA(cand_state, slots * cap);
+    DA(cand_rng, slots * cap);
+    DA(cand_arc, slots * cap);
+    DA(cand_pay, slots * cap);
+    DA(cand_key, slots * cap);
+    DA(cand_ca, slots * cap);
+    DA(front, slots * 2 * cap);
+    DA(tok_info, slots * 2 * cap);
+    DA(tok_cost, slots * 2 * cap);
+    DA(counters, 4);
 #undef DA
-    if (e == cudaSuccess) e = cudaMemset(d->slot, 0xFF, sizeof(Slot) * W * S);
-    if (e == cudaSuccess && g->has_eps) e = cudaMemset(d->qtag, 0, sizeof(u32) * W * S);
-    if (e == cudaSuccess) e = cudaMemset(d->hist, 0, sizeof(u32) * W * wave::NB);
-    if (e == cudaSuccess) e = cudaMemset(d->gctr, 0, sizeof(u32) * 16);
+    if (e == cudaSuccess) e = cudaMemset(d->slot, 0xFF, sizeof(Slot) * slots * S);
+    if (e == cudaSuccess && g->has_eps) e = cudaMemset(d->qtag, 0, sizeof(u32) * slots * S);
+    if (e == cudaSuccess) e = cudaMemset(d->tag_ctr, 0, sizeof(u32) * slots);
     if (e == cudaSuccess) e = cudaEventCreate(&d->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&d->ev1);
     if (e != cudaSuccess) {
@@ -295,7 +293,7 @@ int wb_decoder_destroy(wb_decoder_t d) {
 }
 
 int wb_decoder_device_bytes(wb_decoder_t d, int64_t *bytes) {
-    *bytes = (int64_t)(d->bytes + sizeof(int) * (size_t)d->W * d->T_cap +
+    *bytes = (int64_t)(d->bytes + sizeof(int) * (size_t)d->slots * d->T_cap +
                        sizeof(u64) * d->arena_cap);
     return WB_OK;
 }
@@ -362,37 +360,35 @@ int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row
     }
     // device mode: frame counts stay on the device; an LSD utterance longer than the frame
     // list capacity reports WB_ERR_CAPACITY (callers size it with max_frames)
-    wave::GraphDev gd{g->S, g->A, g->start, g->has_eps, g->start_rng, g->arcs, g->final_w};
-    wave::BatchDev bd{dc, doff, dT, db, num_cols, n};
-    wave::CfgDev cd{cfg->beam, cfg->blank_threshold, cfg->max_active, cfg->mode, cfg->lattice};
-    wave::WaveDev wd;
+    CUDA_TRY(cudaMemsetAsync(d->counters, 0, sizeof(u64) * 4, st));
+    GraphDev gd{g->S, g->A, g->start, g->has_eps, g->start_rng, g->arcs, g->final_w};
+    WorkDev wd;
     std::memset(&wd, 0, sizeof(wd));
-    wd.slot = d->slot; wd.cand_of = d->cand_of; wd.qtag = d->qtag;
-    wd.log_dst = d->log_dst; wd.log_arc = d->log_arc; wd.log_pay = d->log_pay;
-    wd.log_key = d->log_key; wd.logcap = d->logcap;
-    wd.cand_state = d->cand_state; wd.cand_arc = d->cand_arc;
-    wd.cand_pay = d->cand_pay; wd.ca_idx = d->ca_idx;
-    wd.cand_key = d->cand_key; wd.front = d->front; wd.tok_info = d->tok_info;
-    wd.tok_cost = d->tok_cost; wd.frames = d->frames; wd.hist = d->hist; wd.lane = d->lane;
-    wd.gctr = d->gctr; wd.phase = d->phase; wd.arena = d->arena; wd.arena_cap = d->arena_cap;
-    wd.arena_ctr = d->arena_ctr; wd.S = g->S; wd.cap = d->cap; wd.T_cap = d->T_cap;
+    wd.slot = d->slot; wd.cand_of = d->cand_of; wd.qtag = d->qtag; wd.tag_ctr = d->tag_ctr;
+    wd.cand_state = d->cand_state; wd.cand_rng = d->cand_rng; wd.cand_arc = d->cand_arc;
+    wd.cand_pay = d->cand_pay; wd.cand_key = d->cand_key; wd.cand_ca = d->cand_ca;
+    wd.front = d->front; wd.tok_info = d->tok_info; wd.tok_cost = d->tok_cost;
+    wd.frames = d->frames;
+    wd.arena = d->arena; wd.arena_cap = d->arena_cap; wd.arena_ctr = d->counters;
+    wd.utt_ctr = reinterpret_cast<u32 *>(d->counters + 1);
+    wd.S = g->S; wd.cap = d->cap; wd.T_cap = d->T_cap;
+    BatchDev bd{dc, doff, dT, db, num_cols, n};
+    CfgDev cd{cfg->beam, cfg->blank_threshold, cfg->max_active, cfg->mode, cfg->lattice};
+    // 1024 threads per CTA, one persistent CTA (utterance lane) per SM
+    int block = d->block ? d->block : 1024;
+    int max_grid = std::min(n, d->slots);
     CUDA_TRY(cudaEventRecord(d->ev0, st));
-    for (int first = 0; first < n; first += d->W) {
-        // one wave: W utterances advance step by step on all SMs (cooperative launch)
-        wd.first_utt = first;
-        wd.W = std::min(d->W, n - first);
-        CUDA_TRY(cudaMemsetAsync(d->gctr, 0, sizeof(u32) * 9, st));
-        CUDA_TRY(cudaMemsetAsync(d->phase, 0, sizeof(long long) * 8, st));
-        CUDA_TRY(cudaMemsetAsync(d->arena_ctr, 0, sizeof(u64), st));
-        void *args[] = {(void *)&gd, (void *)&wd, (void *)&bd, (void *)&cd, (void *)&dres};
-        CUDA_TRY(cudaLaunchCooperativeKernel((void *)wave::wave_kernel<512, WB_WAVE_MINB>, d->grid, 512, args, 0, st));
-        // backtrace (decoder.py:276-291) of this wave before its arena is reused
-        wave::backtrace_kernel<<<(wd.W + 127) / 128, 128, 0, st>>>(d->arena, g->arcs, dres + first, wd.W,
-                                                             dol + (size_t)first * lcap,
-                                                             dil + (size_t)first * lcap, lcap);
-        CUDA_TRY(cudaGetLastError());
+    cudaError_t e;
+    switch (block) {
+        case 256: e = launch_decode<256>(max_grid, d->num_sms, num_cols, st, gd, wd, bd, cd, dres); break;
+        case 512: e = launch_decode<512>(max_grid, d->num_sms, num_cols, st, gd, wd, bd, cd, dres); break;
+        default: e = launch_decode<1024>(max_grid, d->num_sms, num_cols, st, gd, wd, bd, cd, dres); break;
     }
+    if (e != cudaSuccess)
+        return set_err(WB_ERR_CUDA, std::string("decode launch: ") + cudaGetErrorString(e));
     CUDA_TRY(cudaEventRecord(d->ev1, st));
+    backtrace_kernel<<<(n + 127) / 128, 128, 0, st>>>(gd, d->arena, dres, n, dol, dil, lcap);
+    CUDA_TRY(cudaGetLastError());
     if (host) {
         CUDA_TRY(cudaMemcpyAsync(results, dres, sizeof(wb_utt_result) * n, cudaMemcpyDeviceToHost, st));
         if (label_cap > 0) {
