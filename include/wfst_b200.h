@@ -104,8 +104,9 @@ typedef struct {
     int64_t arena_capacity;      /* backpointer records per wb_decode call */
     int32_t max_frames;          /* longest utterance a call may contain */
     int32_t block_threads;       /* 256, 512 or 1024 */
-    int64_t lattice_capacity;    /* raw lattice arcs per call (lattice mode) */
-    int64_t hash_entries;        /* per-utterance recombination table size (power of two) */
+    int64_t lattice_capacity;    /* raw lattice nodes (and arcs) per utterance lane */
+    int64_t hash_entries;        /* reserved (0) */
+    int64_t lattice_out_capacity;/* trimmed lattice nodes / arcs / finals per wb_decode call */
 } wb_decoder_opts;
 
 const char *wb_last_error(void);
@@ -140,6 +141,57 @@ int wb_decode(wb_decoder_t d, int32_t n_utts, const double *costs, const int64_t
               const int32_t *num_frames, int32_t num_cols, const double *blank,
               const wb_config *cfg, wb_utt_result *results, int32_t *olabels, int32_t *ilabels,
               int32_t label_capacity, int32_t memory_kind, void *stream);
+
+/*
+ * Trimmed lattices of the last wb_decode call made with cfg.lattice = 1 (build_lattice,
+ * lattice.py:148-249): the raw lattice is recorded on the device step by step and trimmed to
+ * nodes on a start-to-final path before anything leaves HBM.  Both calls synchronise with the
+ * decode's stream and copy to HOST buffers.
+ *
+ * wb_lattice_totals: number of utterances and the pool sizes the call requested (nodes,
+ *                    arcs, finals) -- above the pool capacity when it overflowed (the
+ *                    overflowing utterances then report WB_ERR_CAPACITY).
+ * wb_lattice_fetch:  meta [n_utts * 6] = {node_off, n_nodes, arc_off, n_arcs, final_off,
+ *                    n_finals} per utterance (n_nodes == 0: EMPTY_LATTICE; node_off < 0: the
+ *                    utterance failed); nodes [n_nodes * 2] = {state, step}; arcs
+ *                    [n_arcs * 4] = {from, to, wfst arc index, 0} with utterance-local node
+ *                    ids; arc_ac [n_arcs] acoustic cost (0 for epsilon arcs); finals
+ *                    [n_finals] utterance-local node ids with final_w [n_finals].  Node and arc
+ *                    order within an utterance is unspecified (canonical order is (step,
+ *                    state), lattice.py:215-230).  Any output pointer may be NULL.
+ */
+int wb_lattice_totals(wb_decoder_t d, int32_t *n_utts, int64_t *n_nodes, int64_t *n_arcs,
+                      int64_t *n_finals);
+int wb_lattice_fetch(wb_decoder_t d, int64_t *meta, int32_t *nodes, uint32_t *arcs, double *arc_ac,
+                     uint32_t *finals, double *final_w);
+
+/*
+ * Lattice in flat arrays (the reference's Lattice, lattice.py:52-83): node i = (state, step);
+ * node 0 is the start node; arcs carry graph cost g, acoustic cost a and the tie-break
+ * index (the WFST arc index for built lattices); finals are node ids with weights.
+ * n_nodes == 0 is EMPTY_LATTICE.  Arrays returned by wb_lattice_prune are owned by the
+ * caller and released with wb_lattice_arrays_free.
+ */
+typedef struct {
+    int64_t n_nodes, n_arcs, n_finals;
+    int32_t *node_state, *node_step;     /* [n_nodes] */
+    int64_t *arc_from, *arc_to, *arc_tie; /* [n_arcs] */
+    int32_t *arc_il, *arc_ol;            /* [n_arcs] */
+    double *arc_g, *arc_a;               /* [n_arcs] */
+    int64_t *final_node;                 /* [n_finals] */
+    double *final_w;                     /* [n_finals] */
+} wb_lattice_arrays;
+
+/* _topo_order's check (lattice.py:295-326): WB_ERR_LATTICE on an epsilon cycle among nodes. */
+int wb_lattice_check(const wb_lattice_arrays *lat);
+/* prune_lattice (lattice.py:359-501): exact forward-backward pruning to paths within `beam`
+ * of the best, then the path-exact split; WB_ERR_LATTICE past 500,000 split nodes. */
+int wb_lattice_prune(const wb_lattice_arrays *lat, double beam, wb_lattice_arrays *out);
+void wb_lattice_arrays_free(wb_lattice_arrays *a);
+/* lattice_best_path (lattice.py:504-559): tie-exact minimum-cost path and its labels. */
+int wb_lattice_best_path(const wb_lattice_arrays *lat, double *cost, int32_t *olabels,
+                         int32_t *n_olabels, int32_t *ilabels, int32_t *n_ilabels,
+                         int32_t capacity);
 
 /* Device time (ms) of the decode kernel of the last wb_decode call (CUDA events on its stream). */
 int wb_last_kernel_ms(wb_decoder_t d, float *ms);

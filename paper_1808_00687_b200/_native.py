@@ -44,7 +44,15 @@ class DecoderOpts(C.Structure):
     _fields_ = [("max_utts_in_flight", C.c_int32), ("cand_capacity", C.c_int32),
                 ("arena_capacity", C.c_int64), ("max_frames", C.c_int32),
                 ("block_threads", C.c_int32), ("lattice_capacity", C.c_int64),
-                ("hash_entries", C.c_int64)]
+                ("hash_entries", C.c_int64), ("lattice_out_capacity", C.c_int64)]
+
+
+class LatticeArrays(C.Structure):
+    _fields_ = [("n_nodes", C.c_int64), ("n_arcs", C.c_int64), ("n_finals", C.c_int64),
+                ("node_state", C.c_void_p), ("node_step", C.c_void_p), ("arc_from", C.c_void_p),
+                ("arc_to", C.c_void_p), ("arc_tie", C.c_void_p), ("arc_il", C.c_void_p),
+                ("arc_ol", C.c_void_p), ("arc_g", C.c_void_p), ("arc_a", C.c_void_p),
+                ("final_node", C.c_void_p), ("final_w", C.c_void_p)]
 
 
 UTT_RESULT_DTYPE = np.dtype([
@@ -60,7 +68,9 @@ _lib = None
 # Every symbol include/wfst_b200.h declares (checked by tests/test_native_abi.py).
 EXPORTED = ("wb_last_error", "wb_version", "wb_device_count", "wb_graph_create",
             "wb_graph_destroy", "wb_graph_device_bytes", "wb_decoder_create",
-            "wb_decoder_destroy", "wb_decoder_device_bytes", "wb_decode", "wb_last_kernel_ms")
+            "wb_decoder_destroy", "wb_decoder_device_bytes", "wb_decode", "wb_last_kernel_ms",
+            "wb_lattice_totals", "wb_lattice_fetch", "wb_lattice_check", "wb_lattice_prune",
+            "wb_lattice_arrays_free", "wb_lattice_best_path")
 
 
 def load():
@@ -85,6 +95,17 @@ def load():
                             C.c_void_p, C.POINTER(Config), C.c_void_p, C.c_void_p, C.c_void_p,
                             C.c_int32, C.c_int32, C.c_void_p]
     L.wb_last_kernel_ms.argtypes = [C.c_void_p, C.POINTER(C.c_float)]
+    L.wb_lattice_totals.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int64),
+                                    C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    L.wb_lattice_fetch.argtypes = [C.c_void_p] + [C.c_void_p] * 6
+    LP = C.POINTER(LatticeArrays)
+    L.wb_lattice_check.argtypes = [LP]
+    L.wb_lattice_prune.argtypes = [LP, C.c_double, LP]
+    L.wb_lattice_arrays_free.argtypes = [LP]
+    L.wb_lattice_arrays_free.restype = None
+    L.wb_lattice_best_path.argtypes = [LP, C.POINTER(C.c_double), C.c_void_p,
+                                       C.POINTER(C.c_int32), C.c_void_p, C.POINTER(C.c_int32),
+                                       C.c_int32]
     _lib = L
     return L
 

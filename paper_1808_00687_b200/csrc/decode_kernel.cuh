@@ -71,6 +71,27 @@ struct WorkDev {
     u32 *utt_ctr;
     long long S;
     int cap, T_cap, smem_cands, row_in_smem;
+    // ---- lattice recording (LatticeRecorder / build_lattice, lattice.py:96-249)
+    int *tok_eps;         // [slots][2][cap] epsilon-range start of each token's state
+    u32 *stag, *snode;    // [slots][S] survivor tag of the current node step / node index
+    u32 *ln_state;        // [slots][lat_cap] raw lattice nodes (state), step-major
+    unsigned char *ln_flag;  // [slots][lat_cap] trim flags (forward / backward reach)
+    u32 *ln_out;          // [slots][lat_cap] output index of a kept node
+    u32 *la_src, *la_dst, *la_arc;  // [slots][lat_cap] raw arcs: src / dst node, wfst arc
+    double *la_ac;        // [slots][lat_cap] acoustic cost of a raw arc (0 for epsilon)
+    long long lat_cap;
+    int4 *lstep;          // [slots][T_cap + 2] {node_base, arc_base, n_nodes, n_emit | n_eps << 0}
+    int *lstep_eps;       // [slots][T_cap + 2] epsilon arcs of the step (after its emitting arcs)
+    int *lstep_start;     // [slots] step-local index of the start node in step 0
+    // trimmed lattice output (global pools, one reservation per utterance)
+    int2 *o_node;         // {state, step}
+    uint4 *o_arc;         // {from, to, wfst arc, 0} (utterance-local node ids)
+    double *o_ac;         // acoustic cost of o_arc
+    u32 *o_fin;           // final node (utterance-local)
+    double *o_finw;       // its final weight
+    long long o_node_cap, o_arc_cap, o_fin_cap;
+    unsigned long long *o_ctr;  // [3] node / arc / final reservations
+    long long *o_meta;    // [n_utts][6] node_off, n_nodes, arc_off, n_arcs, fin_off, n_fin
 };
 
 struct BatchDev {
@@ -93,6 +114,7 @@ struct Smem {
     u64 r0[NW], r1[NW];
     long long rl[NW];
     int n_cand, n_front, overflow, utt, tag_round, ng, thr_bucket, thr_below, n_pend;
+    int flag, lat_bad;  // lattice sweeps: change flag / output-pool overflow
     u64 thr_key;
     u32 thr_state;
     u64 arena_base;
@@ -778,6 +800,7 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
                     int4 rg = rng_[i];
                     tinfo[tj[q]] = make_int4((int)cst_[i], (int)rec[q], rg.y, rg.z);
                     tcost[tj[q]] = key_cost(ckey[i]);
+                    if (ws.tok_eps) ws.tok_eps[2 * c.co() + (size_t)nxt * ws.cap + tj[q]] = rg.x;
                 }
                 if (rec[q] != CA_NONE) {
                     if (a[q] != 0u && (p[q] & EPS_BIT)) {
@@ -866,6 +889,354 @@ __device__ int block_argmin_tok(u64 key, u32 st, int idx) {
     return r;
 }
 
+// ------------------------------------------------------------------ lattice recording
+// Raw lattice of node step k (lattice.py:148-170): nodes = survivors(k) (plus the start at
+// step 0, decoder.py:246-248); emitting arcs = relaxations from live(k-1) with finite
+// acoustic cost into survivors(k); epsilon arcs = non-self-loop epsilon arcs between
+// survivors(k).  The raw lattice is a pure function of these sets, so no per-relaxation
+// recorder is needed.  Node / arc indices are utterance-global positions in this lane's pool.
+template <int BLOCK>
+__noinline__ __device__ int record_lattice_step(int k, int nxt, int n_surv, int prv, int n_prev,
+                                                const double *grow, u32 tagL, const GraphDev &g,
+                                                const WorkDev &ws) {
+    Smem<BLOCK> &sh = SH<BLOCK>();
+    const Lane c{ws};
+    constexpr int NW = BLOCK / 32;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const size_t so = c.so(), lo = (size_t)blockIdx.x * (size_t)ws.lat_cap;
+    int4 *lst = ws.lstep + (size_t)blockIdx.x * (ws.T_cap + 2);
+    int *lse = ws.lstep_eps + (size_t)blockIdx.x * (ws.T_cap + 2);
+    const int node_base = k == 0 ? 0 : lst[k - 1].x + lst[k - 1].z;
+    const int arc_base = k == 0 ? 0 : lst[k - 1].y + lst[k - 1].w + lse[k - 1];
+    const int prev_base = k == 0 ? 0 : lst[k - 1].x;
+    const int4 *tn = c.tok_info(nxt);
+    const int *te = ws.tok_eps + 2 * c.co() + (size_t)nxt * ws.cap;
+    int status = WB_OK;
+    // step 0 keeps the start node even when the prune dropped it
+    if (threadIdx.x == 0) { sh.ng = -1; sh.n_pend = 0; }
+    __syncthreads();
+    if (k == 0)
+        for (int j = threadIdx.x; j < n_surv; j += BLOCK)
+            if (tn[j].x == g.start) sh.ng = j;
+    __syncthreads();
+    const bool extra = k == 0 && sh.ng < 0;
+    const int n_nodes = n_surv + (extra ? 1 : 0);
+    if ((long long)node_base + n_nodes > ws.lat_cap) return WB_ERR_CAPACITY;
+    for (int j = threadIdx.x; j < n_nodes; j += BLOCK) {
+        const u32 st = j < n_surv ? (u32)tn[j].x : (u32)g.start;
+        ws.stag[so + st] = tagL;
+        ws.snode[so + st] = (u32)(node_base + j);
+        ws.ln_state[lo + node_base + j] = st;
+    }
+    if (k == 0 && threadIdx.x == 0) ws.lstep_start[blockIdx.x] = node_base + (extra ? n_surv : sh.ng);
+    __syncthreads();
+    const long long room = ws.lat_cap - arc_base;
+    // emitting arcs from live(k-1)
+    if (k > 0) {
+        const int4 *tp = c.tok_info(prv);
+        const int nchunks = (n_prev + 31) >> 5;
+        for (int ch = w; ch < nchunks; ch += NW) {
+            const int t = (ch << 5) + l;
+            int4 ti = make_int4(0, 0, 0, 0);
+            if (t < n_prev) ti = tp[t];
+            const int deg = t < n_prev ? ti.w - ti.z : 0;
+            const int incl = warp_incl_scan(deg);
+            const int tot = __shfl_sync(FULL, incl, 31);
+            const int excl = incl - deg;
+            for (int j0 = 0; j0 < tot; j0 += 32) {
+                const int j = j0 + l;
+                const int kk = warp_owner(excl, j);
+                const int lo_k = __shfl_sync(FULL, ti.z, kk);
+                const int ex_k = __shfl_sync(FULL, excl, kk);
+                const int a = lo_k + j - ex_k;
+                bool rec = false;
+                int4 r = make_int4(0, 0, 0, 0);
+                double ac = 0.0;
+                if (j < tot) {
+                    r = __ldg(&g.arcs[2 * a]);
+                    ac = __ldg(&grow[r.y]);
+                    rec = ac != INFINITY && ws.stag[so + r.x] == tagL;
+                }
+                const u32 m = __ballot_sync(FULL, rec);
+                if (!m) continue;
+                int base = 0;
+                if (l == __ffs(m) - 1) base = atomicAdd(&sh.n_pend, __popc(m));
+                base = __shfl_sync(FULL, base, __ffs(m) - 1);
+                if (rec) {
+                    const long long e = base + __popc(m & lanemask_lt());
+                    if (e < room) {
+                        const size_t ge = lo + arc_base + e;
+                        ws.la_src[ge] = (u32)(prev_base + kk + (ch << 5));
+                        ws.la_dst[ge] = ws.snode[so + r.x];
+                        ws.la_arc[ge] = (u32)a;
+                        ws.la_ac[ge] = ac;
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const int n_emit = sh.n_pend;
+    // epsilon arcs inside step k
+    if (g.has_eps) {
+        const int nchunks = (n_nodes + 31) >> 5;
+        for (int ch = w; ch < nchunks; ch += NW) {
+            const int j = (ch << 5) + l;
+            int lo_e = 0, deg = 0;
+            u32 st = 0;
+            if (j < n_surv) {
+                st = (u32)tn[j].x;
+                lo_e = te[j];
+                deg = tn[j].z - lo_e;
+            } else if (j < n_nodes) {
+                st = (u32)g.start;
+                lo_e = g.start_rng.x;
+                deg = g.start_rng.y - g.start_rng.x;
+            }
+            const int incl = warp_incl_scan(deg);
+            const int tot = __shfl_sync(FULL, incl, 31);
+            const int excl = incl - deg;
+            for (int j0 = 0; j0 < tot; j0 += 32) {
+                const int q = j0 + l;
+                const int kk = warp_owner(excl, q);
+                const int lo_k = __shfl_sync(FULL, lo_e, kk);
+                const int ex_k = __shfl_sync(FULL, excl, kk);
+                const u32 st_k = __shfl_sync(FULL, st, kk);
+                const int a = lo_k + q - ex_k;
+                bool rec = false;
+                int4 r = make_int4(0, 0, 0, 0);
+                if (q < tot) {
+                    r = __ldg(&g.arcs[2 * a]);
+                    rec = (u32)r.x != st_k && ws.stag[so + r.x] == tagL;
+                }
+                const u32 m = __ballot_sync(FULL, rec);
+                if (!m) continue;
+                int base = 0;
+                if (l == __ffs(m) - 1) base = atomicAdd(&sh.n_pend, __popc(m));
+                base = __shfl_sync(FULL, base, __ffs(m) - 1);
+                if (rec) {
+                    const long long e = base + __popc(m & lanemask_lt());
+                    if (e < room) {
+                        const size_t ge = lo + arc_base + e;
+                        ws.la_src[ge] = (u32)(node_base + kk + (ch << 5));
+                        ws.la_dst[ge] = ws.snode[so + r.x];
+                        ws.la_arc[ge] = (u32)a;
+                        ws.la_ac[ge] = 0.0;
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const int n_all = sh.n_pend;
+    if (n_all > room) status = WB_ERR_CAPACITY;
+    if (threadIdx.x == 0) {
+        lst[k] = make_int4(node_base, arc_base, n_nodes, n_emit);
+        lse[k] = n_all - n_emit;
+    }
+    __syncthreads();
+    return status;
+}
+
+// Trim to nodes on some start-to-final path (_assemble, lattice.py:190-237) by forward and
+// backward reachability sweeps over the node steps, then copy the kept nodes / arcs / finals
+// to the output pools.  Canonical ordering is left to the host (small lattice).
+constexpr unsigned char LF_FWD = 1, LF_BWD = 2;
+
+template <int BLOCK>
+__noinline__ __device__ void trim_lattice(int u, int K, int reached, int final_state,
+                                          const GraphDev &g, const WorkDev &ws) {
+    const int final_step = K;  // the last node step with nodes is the winner's step
+    Smem<BLOCK> &sh = SH<BLOCK>();
+    const size_t lo = (size_t)blockIdx.x * (size_t)ws.lat_cap;
+    const int4 *lst = ws.lstep + (size_t)blockIdx.x * (ws.T_cap + 2);
+    const int *lse = ws.lstep_eps + (size_t)blockIdx.x * (ws.T_cap + 2);
+    unsigned char *fl = ws.ln_flag + lo;
+    const u32 *la_src = ws.la_src + lo, *la_dst = ws.la_dst + lo;
+    long long *meta = ws.o_meta + 6 * (size_t)u;
+    const int n_nodes = lst[K].x + lst[K].z;
+    const int n_arcs = lst[K].y + lst[K].w + lse[K];
+    if (threadIdx.x == 0) sh.lat_bad = 0;
+    for (int i = threadIdx.x; i < n_nodes; i += BLOCK) fl[i] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) fl[ws.lstep_start[blockIdx.x]] = LF_FWD;
+    __syncthreads();
+    // forward reach from the start
+    for (int k = 0; k <= K; ++k) {
+        const int4 st = lst[k];
+        for (int e = threadIdx.x; e < st.w; e += BLOCK) {
+            const size_t ge = (size_t)st.y + e;
+            if (fl[la_src[ge]] & LF_FWD) fl[la_dst[ge]] = LF_FWD;
+        }
+        __syncthreads();
+        const int ne = lse[k];
+        while (ne > 0) {
+            if (threadIdx.x == 0) sh.flag = 0;
+            __syncthreads();
+            for (int e = threadIdx.x; e < ne; e += BLOCK) {
+                const size_t ge = (size_t)st.y + st.w + e;
+                if ((fl[la_src[ge]] & LF_FWD) && !(fl[la_dst[ge]] & LF_FWD)) {
+                    fl[la_dst[ge]] = LF_FWD;
+                    sh.flag = 1;
+                }
+            }
+            __syncthreads();
+            const int changed = sh.flag;
+            __syncthreads();
+            if (!changed) break;
+        }
+    }
+    // live finals (lattice.py:172-183, 214): reached -> survivors of final_step with a final
+    // weight; otherwise the winning state at final_step with weight 0
+    if (threadIdx.x == 0) { sh.ng = 0; sh.n_pend = 0; }
+    __syncthreads();
+    const int4 fs = lst[final_step];
+    for (int i = threadIdx.x; i < fs.z; i += BLOCK) {
+        const int node = fs.x + i;
+        const u32 s = ws.ln_state[lo + node];
+        const bool fin = reached ? __ldg(&g.final_w[s]) != INFINITY : (int)s == final_state;
+        if (fin && (fl[node] & LF_FWD)) {
+            fl[node] = LF_FWD | LF_BWD;
+            atomicAdd(&sh.ng, 1);
+        }
+    }
+    __syncthreads();
+    const int n_fin = sh.ng;
+    __syncthreads();
+    if (n_fin == 0) {  // EMPTY_LATTICE
+        if (threadIdx.x == 0) for (int q = 0; q < 6; ++q) meta[q] = 0;
+        __syncthreads();
+        return;
+    }
+    // backward reach from the live finals
+    for (int k = final_step; k >= 0; --k) {
+        if (k < K) {
+            const int4 nx = lst[k + 1];
+            for (int e = threadIdx.x; e < nx.w; e += BLOCK) {
+                const size_t ge = (size_t)nx.y + e;
+                const u32 sn = la_src[ge];
+                if ((fl[la_dst[ge]] & LF_BWD) && (fl[sn] & LF_FWD)) fl[sn] = LF_FWD | LF_BWD;
+            }
+            __syncthreads();
+        }
+        const int4 st = lst[k];
+        const int ne = lse[k];
+        while (ne > 0) {
+            if (threadIdx.x == 0) sh.flag = 0;
+            __syncthreads();
+            for (int e = threadIdx.x; e < ne; e += BLOCK) {
+                const size_t ge = (size_t)st.y + st.w + e;
+                const u32 sn = la_src[ge];
+                if ((fl[la_dst[ge]] & LF_BWD) && (fl[sn] == LF_FWD)) {
+                    fl[sn] = LF_FWD | LF_BWD;
+                    sh.flag = 1;
+                }
+            }
+            __syncthreads();
+            const int changed = sh.flag;
+            __syncthreads();
+            if (!changed) break;
+        }
+    }
+    // kept = forward & backward reachable; compact nodes (step-major order), arcs, finals
+    constexpr int NW = BLOCK / 32;
+    const int wp = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const u32 lt = lanemask_lt();
+    auto kept = [&](int i) { return fl[i] == (LF_FWD | LF_BWD); };
+    int cnt = 0;
+    const int seg = ((n_nodes + NW - 1) / NW + 31) & ~31;
+    const int s0 = min(n_nodes, wp * seg), s1 = min(n_nodes, s0 + seg);
+    for (int i0 = s0; i0 < s1; i0 += 32) {
+        const int i = i0 + l;
+        cnt += __popc(__ballot_sync(FULL, i < s1 && kept(i)));
+    }
+    int tot;
+    int run = warp_offsets<BLOCK>(cnt, sh.wa, &tot);
+    if (threadIdx.x == 0) {
+        unsigned long long nb = atomicAdd(&ws.o_ctr[0], (unsigned long long)tot);
+        sh.arena_base = nb;
+        if (nb + tot > (unsigned long long)ws.o_node_cap) sh.lat_bad = 1;
+    }
+    __syncthreads();
+    const unsigned long long nbase = sh.arena_base;
+    const bool ok_nodes = sh.lat_bad == 0;
+    for (int i0 = s0; i0 < s1; i0 += 32) {
+        const int i = i0 + l;
+        const bool kp = i < s1 && kept(i);
+        const u32 m = __ballot_sync(FULL, kp);
+        if (kp) {
+            const int oi = run + __popc(m & lt);
+            ws.ln_out[lo + i] = (u32)oi;
+            if (ok_nodes) {
+                int step = 0, a = 0, b = K;
+                while (a <= b) {  // node step: last k with lst[k].x <= i
+                    const int mid = (a + b) >> 1;
+                    if (lst[mid].x <= i) { step = mid; a = mid + 1; } else b = mid - 1;
+                }
+                ws.o_node[nbase + oi] = make_int2((int)ws.ln_state[lo + i], step);
+            }
+        }
+        run += __popc(m);
+    }
+    __syncthreads();
+    // arcs between kept nodes (kept from-node is forward-reached, kept to-node backward)
+    auto karc = [&](int e) { return kept(la_src[e]) && kept(la_dst[e]); };
+    cnt = 0;
+    const int sega = ((n_arcs + NW - 1) / NW + 31) & ~31;
+    const int a0 = min(n_arcs, wp * sega), a1 = min(n_arcs, a0 + sega);
+    for (int i0 = a0; i0 < a1; i0 += 32) {
+        const int e = i0 + l;
+        cnt += __popc(__ballot_sync(FULL, e < a1 && karc(e)));
+    }
+    int tota;
+    run = warp_offsets<BLOCK>(cnt, sh.wa, &tota);
+    if (threadIdx.x == 0) {
+        unsigned long long ab = atomicAdd(&ws.o_ctr[1], (unsigned long long)tota);
+        unsigned long long fb = atomicAdd(&ws.o_ctr[2], (unsigned long long)n_fin);
+        sh.arena_base = ab;
+        sh.thr_key = fb;
+        if (ab + tota > (unsigned long long)ws.o_arc_cap || fb + n_fin > (unsigned long long)ws.o_fin_cap)
+            sh.lat_bad = 1;
+    }
+    __syncthreads();
+    const unsigned long long abase = sh.arena_base, fbase = sh.thr_key;
+    const bool ok = sh.lat_bad == 0;
+    for (int i0 = a0; i0 < a1; i0 += 32) {
+        const int e = i0 + l;
+        const bool kp = e < a1 && karc(e);
+        const u32 m = __ballot_sync(FULL, kp);
+        if (kp && ok) {
+            const unsigned long long oe = abase + run + __popc(m & lt);
+            ws.o_arc[oe] = make_uint4(ws.ln_out[lo + la_src[e]], ws.ln_out[lo + la_dst[e]],
+                                      ws.la_arc[lo + e], 0u);
+            ws.o_ac[oe] = ws.la_ac[lo + e];
+        }
+        run += __popc(m);
+    }
+    if (threadIdx.x == 0) sh.ng = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < fs.z; i += BLOCK) {
+        const int node = fs.x + i;
+        const u32 s = ws.ln_state[lo + node];
+        const bool fin = reached ? __ldg(&g.final_w[s]) != INFINITY : (int)s == final_state;
+        if (fin && kept(node) && ok) {
+            const int q = atomicAdd(&sh.ng, 1);
+            ws.o_fin[fbase + q] = ws.ln_out[lo + node];
+            ws.o_finw[fbase + q] = reached ? __ldg(&g.final_w[s]) : 0.0;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        meta[0] = ok ? (long long)nbase : -1;
+        meta[1] = tot;
+        meta[2] = (long long)abase;
+        meta[3] = tota;
+        meta[4] = (long long)fbase;
+        meta[5] = n_fin;
+    }
+    __syncthreads();
+}
+
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK, 1)
 decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDev ws,
@@ -928,6 +1299,12 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
         StepOut so = finish_step<BLOCK>(cur, g, ws, cfg);
         if (so.status) status = so.status;
         n_rec += so.n_keep;
+        long long lat_arcs = 0;
+        if (cfg.lattice && status == WB_OK) {
+            ++tag;
+            const int rs = record_lattice_step<BLOCK>(0, cur, so.n_surv, 0, 0, nullptr, tag, g, ws);
+            if (rs) status = rs;
+        }
         int n_live = so.n_surv;
         n_surv_tot += n_live;
         int steps_run = 0, died_at = -1;
@@ -967,6 +1344,12 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
                 break;
             }
             n_surv_tot += so.n_surv;
+            if (cfg.lattice && status == WB_OK) {
+                ++tag;
+                const int rs = record_lattice_step<BLOCK>(s + 1, cur ^ 1, so.n_surv, cur, n_live, grow,
+                                                          tag, g, ws);
+                if (rs) status = rs;
+            }
             cur ^= 1;
             n_live = so.n_surv;
         }
@@ -1005,6 +1388,17 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             best_t = block_argmin_tok<BLOCK>(k, st, idx);
             if (best_t >= 0) best_cost = tcost[best_t];
         }
+        if (cfg.lattice) {
+            const int fstep = died_at < 0 ? steps_run : died_at;
+            if (status == WB_OK) {
+                const int4 lk = ws.lstep[(size_t)blockIdx.x * (ws.T_cap + 2) + fstep];
+                lat_arcs = lk.y + lk.w + ws.lstep_eps[(size_t)blockIdx.x * (ws.T_cap + 2) + fstep];
+                trim_lattice<BLOCK>(u, fstep, reached, best_t >= 0 ? tinfo[best_t].x : -1, g, ws);
+                if (ws.o_meta[6 * (size_t)u] < 0) status = WB_ERR_CAPACITY;
+            } else if (threadIdx.x == 0) {
+                ws.o_meta[6 * (size_t)u] = -1;
+            }
+        }
         long long t_emit = block_sum<BLOCK>(a_emit);
         long long t_fin = block_sum<BLOCK>(a_fin);
         long long t_eps = block_sum<BLOCK>(e_eps);
@@ -1029,6 +1423,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             r.n_cand = n_cand_tot;
             r.n_surv = n_surv_tot;
             r.n_rec = n_rec;
+            r.lat_arcs = lat_arcs;
             res[u] = r;
         }
         __syncthreads();

@@ -21,6 +21,8 @@ static int set_err(int code, const std::string &msg) {
     return code;
 }
 
+int wb_internal_set_error(int code, const char *msg) { return set_err(code, msg); }
+
 #define CUDA_TRY(expr)                                                                       \
     do {                                                                                     \
         cudaError_t e_ = (expr);                                                             \
@@ -63,6 +65,26 @@ struct wb_decoder_s {
     size_t h_off_n = 0, h_T_n = 0, h_res_n = 0, h_lab_n = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     size_t bytes = 0;
+    // lattice mode (allocated on the first lattice decode)
+    long long lat_cap = 0, lat_cap_want = 0, lat_out_want = 0;
+    int lat_T = 0;
+    int *tok_eps = nullptr;
+    u32 *stag = nullptr, *snode = nullptr, *ln_state = nullptr, *ln_out = nullptr;
+    unsigned char *ln_flag = nullptr;
+    u32 *la_src = nullptr, *la_dst = nullptr, *la_arc = nullptr;
+    double *la_ac = nullptr;
+    int4 *lstep = nullptr;
+    int *lstep_eps = nullptr, *lstep_start = nullptr;
+    int2 *o_node = nullptr;
+    uint4 *o_arc = nullptr;
+    double *o_ac = nullptr, *o_finw = nullptr;
+    u32 *o_fin = nullptr;
+    size_t o_node_n = 0, o_arc_n = 0, o_fin_n = 0, o_meta_n = 0;
+    unsigned long long *o_ctr = nullptr;
+    long long *o_meta = nullptr;
+    int lat_n = 0;                 // utterances of the last lattice decode
+    cudaStream_t lat_stream = nullptr;
+    size_t lat_bytes = 0;
 };
 
 extern "C" {
@@ -152,7 +174,10 @@ static void free_decoder(wb_decoder_s *d) {
     void *ptrs[] = {d->slot, d->cand_of, d->qtag, d->tag_ctr, d->cand_state, d->cand_rng,
                     d->cand_arc, d->cand_pay, d->cand_key, d->cand_ca, d->front, d->tok_info,
                     d->tok_cost, d->frames, d->arena, d->counters, d->h_costs, d->h_blank,
-                    d->h_off, d->h_T, d->h_res, d->h_lab};
+                    d->h_off, d->h_T, d->h_res, d->h_lab, d->tok_eps, d->stag, d->snode,
+                    d->ln_state, d->ln_out, d->ln_flag, d->la_src, d->la_dst, d->la_arc,
+                    d->la_ac, d->lstep, d->lstep_eps, d->lstep_start, d->o_node, d->o_arc,
+                    d->o_ac, d->o_finw, d->o_fin, d->o_ctr, d->o_meta};
     for (void *p : ptrs) cudaFree(p);
     if (d->ev0) cudaEventDestroy(d->ev0);
     if (d->ev1) cudaEventDestroy(d->ev1);
@@ -177,6 +202,49 @@ static int alloc_arena(wb_decoder_s *d, u64 cap) {
     d->arena = nullptr;
     d->arena_cap = std::min<u64>(std::max<u64>(cap, 1024), (u64)EPS_BIT - 1);
     CUDA_TRY(cudaMalloc(&d->arena, sizeof(u64) * d->arena_cap));
+    return WB_OK;
+}
+
+// Lattice workspace: per-lane raw node / arc pools (lat_cap each), per-step metadata and the
+// survivor tags; allocated on the first lattice decode so plain decoding pays nothing.
+static int alloc_lattice(wb_decoder_s *d) {
+    void *ptrs[] = {d->tok_eps, d->stag, d->snode, d->ln_state, d->ln_out, d->ln_flag,
+                    d->la_src, d->la_dst, d->la_arc, d->la_ac, d->lstep, d->lstep_eps,
+                    d->lstep_start, d->o_ctr};
+    for (void *p : ptrs) cudaFree(p);
+    d->tok_eps = nullptr; d->stag = d->snode = d->ln_state = d->ln_out = nullptr;
+    d->ln_flag = nullptr; d->la_src = d->la_dst = d->la_arc = nullptr; d->la_ac = nullptr;
+    d->lstep = nullptr; d->lstep_eps = d->lstep_start = nullptr; d->o_ctr = nullptr;
+    d->lat_cap = 0;
+    const size_t slots = (size_t)d->slots, S = (size_t)d->g->S, cap = (size_t)d->cap;
+    const long long want = d->lat_cap_want > 0 ? d->lat_cap_want
+                                               : std::min<long long>((long long)(d->T_cap + 1) * std::min<long long>(d->cap, 4096), 1ll << 22);
+    const size_t L = (size_t)std::max<long long>(want, 1024), TS = (size_t)d->T_cap + 2;
+    size_t acc = 0;
+    cudaError_t e = cudaSuccess;
+#define DA(p, n) if (e == cudaSuccess) e = dalloc(&d->p, (n), acc)
+    DA(tok_eps, slots * 2 * cap);
+    DA(stag, slots * S);
+    DA(snode, slots * S);
+    DA(ln_state, slots * L);
+    DA(ln_out, slots * L);
+    DA(ln_flag, slots * L);
+    DA(la_src, slots * L);
+    DA(la_dst, slots * L);
+    DA(la_arc, slots * L);
+    DA(la_ac, slots * L);
+    DA(lstep, slots * TS);
+    DA(lstep_eps, slots * TS);
+    DA(lstep_start, slots);
+    DA(o_ctr, 4);
+#undef DA
+    if (e == cudaSuccess) e = cudaMemset(d->stag, 0, sizeof(u32) * slots * S);
+    if (e != cudaSuccess)
+        return set_err(e == cudaErrorMemoryAllocation ? WB_ERR_NOMEM : WB_ERR_CUDA,
+                       std::string("lattice workspace: ") + cudaGetErrorString(e));
+    d->lat_cap = (long long)L;
+    d->lat_T = d->T_cap;
+    d->lat_bytes = acc;
     return WB_OK;
 }
 
@@ -272,6 +340,8 @@ int wb_decoder_create(wb_graph_t g, const wb_decoder_opts *o, wb_decoder_t *out)
                        std::string("decoder workspace: ") + cudaGetErrorString(e));
     }
     d->bytes = acc;
+    d->lat_cap_want = opts.lattice_capacity;
+    d->lat_out_want = opts.lattice_out_capacity;
     int rc = alloc_frames(d, opts.max_frames > 0 ? opts.max_frames : 2048);
     if (rc == WB_OK)
         rc = alloc_arena(d, opts.arena_capacity > 0 ? (u64)opts.arena_capacity : (u64)1 << 24);
@@ -294,7 +364,9 @@ int wb_decoder_destroy(wb_decoder_t d) {
 
 int wb_decoder_device_bytes(wb_decoder_t d, int64_t *bytes) {
     *bytes = (int64_t)(d->bytes + sizeof(int) * (size_t)d->slots * d->T_cap +
-                       sizeof(u64) * d->arena_cap);
+                       sizeof(u64) * d->arena_cap + d->lat_bytes +
+                       sizeof(int2) * d->o_node_n + (sizeof(uint4) + sizeof(double)) * d->o_arc_n +
+                       (sizeof(u32) + sizeof(double)) * d->o_fin_n);
     return WB_OK;
 }
 
@@ -372,6 +444,34 @@ int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row
     wd.arena = d->arena; wd.arena_cap = d->arena_cap; wd.arena_ctr = d->counters;
     wd.utt_ctr = reinterpret_cast<u32 *>(d->counters + 1);
     wd.S = g->S; wd.cap = d->cap; wd.T_cap = d->T_cap;
+    if (cfg->lattice) {
+        if (!d->la_src || d->lat_T < d->T_cap) {
+            int rc = alloc_lattice(d);
+            if (rc) return rc;
+        }
+        const size_t out = (size_t)(d->lat_out_want > 0 ? d->lat_out_want : (1ll << 22));
+        int rc;
+        if ((rc = grow(&d->o_node, d->o_node_n, out))) return rc;
+        if ((rc = grow(&d->o_arc, d->o_arc_n, out))) return rc;
+        size_t have = d->o_arc_n;
+        if ((rc = grow(&d->o_ac, have, out))) return rc;
+        if ((rc = grow(&d->o_fin, d->o_fin_n, out))) return rc;
+        have = d->o_fin_n;
+        if ((rc = grow(&d->o_finw, have, out))) return rc;
+        if ((rc = grow(&d->o_meta, d->o_meta_n, (size_t)n * 6))) return rc;
+        CUDA_TRY(cudaMemsetAsync(d->o_ctr, 0, sizeof(unsigned long long) * 4, st));
+        wd.tok_eps = d->tok_eps; wd.stag = d->stag; wd.snode = d->snode;
+        wd.ln_state = d->ln_state; wd.ln_flag = d->ln_flag; wd.ln_out = d->ln_out;
+        wd.la_src = d->la_src; wd.la_dst = d->la_dst; wd.la_arc = d->la_arc; wd.la_ac = d->la_ac;
+        wd.lat_cap = d->lat_cap; wd.lstep = d->lstep; wd.lstep_eps = d->lstep_eps;
+        wd.lstep_start = d->lstep_start;
+        wd.o_node = d->o_node; wd.o_arc = d->o_arc; wd.o_ac = d->o_ac; wd.o_fin = d->o_fin;
+        wd.o_finw = d->o_finw; wd.o_node_cap = (long long)d->o_node_n;
+        wd.o_arc_cap = (long long)d->o_arc_n; wd.o_fin_cap = (long long)d->o_fin_n;
+        wd.o_ctr = d->o_ctr; wd.o_meta = d->o_meta;
+        d->lat_n = n;
+        d->lat_stream = st;
+    }
     BatchDev bd{dc, doff, dT, db, num_cols, n};
     CfgDev cd{cfg->beam, cfg->blank_threshold, cfg->max_active, cfg->mode, cfg->lattice};
     // 1024 threads per CTA, one persistent CTA (utterance lane) per SM
@@ -399,6 +499,45 @@ int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row
         }
         CUDA_TRY(cudaStreamSynchronize(st));
     }
+    return WB_OK;
+}
+
+int wb_lattice_totals(wb_decoder_t d, int32_t *n_utts, int64_t *n_nodes, int64_t *n_arcs,
+                      int64_t *n_finals) {
+    if (!d || !n_utts || !n_nodes || !n_arcs || !n_finals) return set_err(WB_ERR_VALUE, "null argument");
+    if (!d->o_ctr || d->lat_n == 0) {
+        *n_utts = 0; *n_nodes = *n_arcs = *n_finals = 0;
+        return WB_OK;
+    }
+    CUDA_TRY(cudaSetDevice(d->g->device));
+    CUDA_TRY(cudaStreamSynchronize(d->lat_stream));
+    unsigned long long c[4];
+    CUDA_TRY(cudaMemcpy(c, d->o_ctr, sizeof(c), cudaMemcpyDeviceToHost));
+    *n_utts = d->lat_n;
+    // requested sizes: larger than the pools when the call overflowed them
+    *n_nodes = (int64_t)c[0];
+    *n_arcs = (int64_t)c[1];
+    *n_finals = (int64_t)c[2];
+    return WB_OK;
+}
+
+int wb_lattice_fetch(wb_decoder_t d, int64_t *meta, int32_t *nodes, uint32_t *arcs, double *arc_ac,
+                     uint32_t *finals, double *final_w) {
+    if (!d || !meta) return set_err(WB_ERR_VALUE, "null argument");
+    int32_t n;
+    int64_t nn, na, nf;
+    int rc = wb_lattice_totals(d, &n, &nn, &na, &nf);
+    if (rc) return rc;
+    if (n == 0) return WB_OK;
+    nn = std::min<int64_t>(nn, (int64_t)d->o_node_n);
+    na = std::min<int64_t>(na, (int64_t)d->o_arc_n);
+    nf = std::min<int64_t>(nf, (int64_t)d->o_fin_n);
+    CUDA_TRY(cudaMemcpy(meta, d->o_meta, sizeof(long long) * 6 * (size_t)n, cudaMemcpyDeviceToHost));
+    if (nn && nodes) CUDA_TRY(cudaMemcpy(nodes, d->o_node, sizeof(int2) * nn, cudaMemcpyDeviceToHost));
+    if (na && arcs) CUDA_TRY(cudaMemcpy(arcs, d->o_arc, sizeof(uint4) * na, cudaMemcpyDeviceToHost));
+    if (na && arc_ac) CUDA_TRY(cudaMemcpy(arc_ac, d->o_ac, sizeof(double) * na, cudaMemcpyDeviceToHost));
+    if (nf && finals) CUDA_TRY(cudaMemcpy(finals, d->o_fin, sizeof(u32) * nf, cudaMemcpyDeviceToHost));
+    if (nf && final_w) CUDA_TRY(cudaMemcpy(final_w, d->o_finw, sizeof(double) * nf, cudaMemcpyDeviceToHost));
     return WB_OK;
 }
 

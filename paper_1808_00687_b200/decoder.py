@@ -160,12 +160,15 @@ class BatchDecoder:
 
     def __init__(self, graph, device: int | None = None, *, max_utts_in_flight: int = 0,
                  cand_capacity: int = 0, arena_capacity: int = 0, max_frames: int = 0,
-                 block_threads: int = 0, hash_entries: int = 0):
+                 block_threads: int = 0, hash_entries: int = 0, lattice_capacity: int = 0,
+                 lattice_out_capacity: int = 0):
         self.graph = graph if isinstance(graph, DeviceGraph) else DeviceGraph(graph, device)
         self.device = self.graph.device
         self.opts = dict(max_utts_in_flight=max_utts_in_flight, cand_capacity=cand_capacity,
                          arena_capacity=arena_capacity, max_frames=max_frames,
-                         block_threads=block_threads, hash_entries=hash_entries)
+                         block_threads=block_threads, hash_entries=hash_entries,
+                         lattice_capacity=lattice_capacity,
+                         lattice_out_capacity=lattice_out_capacity)
         self._h = None
         self._create()
 
@@ -174,15 +177,21 @@ class BatchDecoder:
             self._fin()
         o = self.opts
         opts = N.DecoderOpts(o["max_utts_in_flight"], o["cand_capacity"], o["arena_capacity"],
-                             o["max_frames"], o["block_threads"], 0, o["hash_entries"])
+                             o["max_frames"], o["block_threads"], o["lattice_capacity"],
+                             o["hash_entries"], o["lattice_out_capacity"])
         h = C.c_void_p()
         N.check(N.load().wb_decoder_create(self.graph.handle, C.byref(opts), C.byref(h)),
                 "decoder workspace")
         self._h = h
         self._fin = weakref.finalize(self, N.load().wb_decoder_destroy, h)
 
-    def _grow(self, arena_need: int | None = None):
+    def _grow(self, arena_need: int | None = None, lattice: bool = False,
+              lattice_out_need: int = 0):
         S = self.graph.wfst.num_states
+        if lattice:
+            self.opts["lattice_capacity"] = min(2**31 - 2, 4 * (self.opts["lattice_capacity"] or (1 << 20)))
+            out = self.opts["lattice_out_capacity"] or (1 << 22)
+            self.opts["lattice_out_capacity"] = max(2 * out, lattice_out_need * 5 // 4)
         cap = self.opts["cand_capacity"] or min(S, 1 << 18)
         self.opts["cand_capacity"] = min(S, cap * 2)
         arena = self.opts["arena_capacity"] or (1 << 24)
@@ -199,8 +208,10 @@ class BatchDecoder:
         N.check(N.load().wb_last_kernel_ms(self._h, C.byref(ms)))
         return float(ms.value)
 
-    def reserve(self, n_frames_total: int, max_active: int | None, max_frames: int):
-        """Size the backpointer arena / frame list for a batch before launching it."""
+    def reserve(self, n_frames_total: int, max_active: int | None, max_frames: int,
+                lattice: bool = False):
+        """Size the backpointer arena / frame list (and the raw-lattice pools of one utterance
+        lane when recording lattices) for a batch before launching it."""
         per_step = min(self.opts["cand_capacity"] or (1 << 18), 2 * max_active if max_active else 8192)
         need = int(min(2**31 - 2, (n_frames_total + 64) * max(per_step, 64)))
         changed = False
@@ -209,6 +220,11 @@ class BatchDecoder:
             changed = True
         if max_frames > (self.opts["max_frames"] or 2048):
             self.opts["max_frames"] = max_frames
+            changed = True
+        if lattice and not self.opts["lattice_capacity"]:
+            S = self.graph.wfst.num_states
+            width = min(S, max_active or S, 1 << 16)
+            self.opts["lattice_capacity"] = int(min(1 << 23, max(1 << 16, 2 * (max_frames + 1) * width)))
             changed = True
         if changed:
             self._create()
@@ -227,7 +243,7 @@ class BatchDecoder:
         blank = np.ascontiguousarray(blank, dtype=np.float64)
         L1 = costs.shape[1]
         maxT = int(num_frames.max()) if n else 0
-        self.reserve(int(num_frames.sum()) + n, cfg.max_active, maxT)
+        self.reserve(int(num_frames.sum()) + n, cfg.max_active, maxT, lattice)
         cap = label_capacity or (maxT + 64)
         ncfg = _native_config(cfg, mode, lattice)
         for _attempt in range(8):
@@ -246,8 +262,39 @@ class BatchDecoder:
             if (longest[bad] > cap).any():
                 cap = int(longest.max())          # labels did not fit: rerun with exact room
             if (bad & (longest <= cap)).any():
-                self._grow()                      # candidate / arena workspace overflowed
+                need = 0
+                if lattice:                       # exact output-pool need from the counters
+                    nu, nn, na, nf = C.c_int32(), C.c_int64(), C.c_int64(), C.c_int64()
+                    N.check(N.load().wb_lattice_totals(self._h, C.byref(nu), C.byref(nn),
+                                                       C.byref(na), C.byref(nf)), "lattice")
+                    need = max(nn.value, na.value, nf.value)
+                self._grow(lattice=lattice, lattice_out_need=need)
         raise N.CapacityError("decode workspace kept overflowing")
+
+    def fetch_lattices(self, wfst: Wfst) -> list:
+        """Trimmed lattices of the last lattice-mode decode, canonically ordered."""
+        from .lattice import canonical_from_device
+        L = N.load()
+        n = C.c_int32()
+        nn, na, nf = C.c_int64(), C.c_int64(), C.c_int64()
+        N.check(L.wb_lattice_totals(self._h, C.byref(n), C.byref(nn), C.byref(na), C.byref(nf)),
+                "lattice")
+        meta = np.zeros((max(n.value, 1), 6), np.int64)
+        nodes = np.zeros((max(nn.value, 1), 2), np.int32)
+        arcs = np.zeros((max(na.value, 1), 4), np.uint32)
+        ac = np.zeros(max(na.value, 1), np.float64)
+        fin = np.zeros(max(nf.value, 1), np.uint32)
+        finw = np.zeros(max(nf.value, 1), np.float64)
+        N.check(L.wb_lattice_fetch(self._h, meta.ctypes.data, nodes.ctypes.data, arcs.ctypes.data,
+                                   ac.ctypes.data, fin.ctypes.data, finw.ctypes.data), "lattice")
+        out = []
+        for u in range(n.value):
+            no, cn, ao, ca, fo, cf = (int(x) for x in meta[u])
+            if no < 0:
+                raise N.CapacityError("lattice output pool overflowed")
+            out.append(canonical_from_device(wfst, nodes[no:no + cn], arcs[ao:ao + ca],
+                                             ac[ao:ao + ca], fin[fo:fo + cf], finw[fo:fo + cf]))
+        return out
 
     # ------------------------------------------------------------------ device buffers
     def decode_device(self, costs, row_offset, num_frames, blank, cfg, mode: str, results,
@@ -293,7 +340,8 @@ def _decoder_for(w: Wfst) -> BatchDecoder:
 def decode_batch(wfst, posts_list, cfg: DecodeConfig, mode: str | None = None,
                  recorder=None) -> list[DecodeResult]:
     """Decode many utterances in one persistent-kernel launch (utterances are independent,
-    SURVEY 8e).  Each element equals ``decode(wfst, posts, cfg)`` of the reference."""
+    SURVEY 8e).  Each element equals ``decode(wfst, posts, cfg)`` of the reference.
+    ``recorder``: one ``LatticeRecorder`` per utterance (a list) to record lattices."""
     w = as_wfst(wfst)
     mode = mode or cfg.mode
     posts_list = list(posts_list)
@@ -315,11 +363,18 @@ def decode_batch(wfst, posts_list, cfg: DecodeConfig, mode: str | None = None,
         if t:
             cost_table(p, cfg.acoustic_scale, out=costs[o:o + t])
             blank[o:o + t] = p.rows[:, p.blank_col]
-    out = _decoder_for(w).decode_host(costs, off, T, blank, cfg, mode,
-                                      lattice=recorder is not None)
-    results = out.decode_results()
+    recorders = None
     if recorder is not None:
-        recorder._attach(w, out, posts_list, costs, off, cfg, mode)
+        recorders = list(recorder) if isinstance(recorder, (list, tuple)) else [recorder]
+        if len(recorders) != len(posts_list):
+            raise ValueError("pass one LatticeRecorder per utterance")
+    dec = _decoder_for(w)
+    out = dec.decode_host(costs, off, T, blank, cfg, mode, lattice=recorders is not None)
+    results = out.decode_results()
+    if recorders is not None:
+        lats = dec.fetch_lattices(w)
+        for rec, lat, r in zip(recorders, lats, out.results):
+            rec._set(lat, int(r["final_step"]), int(r["final_state"]), bool(r["reached_final"]))
     return results
 
 

@@ -1,13 +1,393 @@
-"""Raw lattices (lattice.py of the reference) -- device recording lands in a later step."""
+"""Word lattices from the device decoder (the reference's ``lsd_wfst.lattice``).
+
+Same surface as /root/reference/pkg/src/lsd_wfst/lattice.py: ``LatticeNode``, ``LatticeArc``,
+``Lattice``, ``EMPTY_LATTICE``, ``LatticeRecorder``, ``build_lattice``, ``prune_lattice``,
+``lattice_best_path``, ``format_lattice_text`` / ``parse_lattice_text`` / ``save_lattice`` /
+``load_lattice``, ``LatticeError``.
+
+Where the reference records every relaxation into Python lists and assembles the lattice
+afterwards (lattice.py:96-249), the decode kernel records the raw lattice of each node step
+in HBM (survivor nodes, emitting arcs from the previous step's survivors, within-step epsilon
+arcs) and trims it to start-to-final paths before anything leaves the device
+(``csrc/decode_kernel.cuh``: ``record_lattice_step`` / ``trim_lattice``).  The host receives
+only the trimmed lattice as flat arrays and orders it canonically (lattice.py:215-230).
+Pruning and the best path run in C++ over those arrays (``csrc/lattice_host.cpp``).
+
+``Lattice`` is array-backed; ``nodes`` / ``arcs`` materialise the reference's tuples of frozen
+dataclasses lazily, and equality follows the reference (``tie`` excluded).
+"""
 from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+INF = math.inf
+COST_EPS = 1e-9  # lattice.py:26
 
 
 class LatticeError(Exception):
     """Lattice construction / pruning failure (lattice.py:29)."""
 
 
-class LatticeRecorder:
-    """Placeholder handle; device lattice recording is not wired yet."""
+@dataclass(frozen=True)
+class LatticeNode:
+    state: int
+    step: int
 
-    def _attach(self, *args, **kwargs):
-        raise NotImplementedError("device lattice recording is not implemented yet")
+
+@dataclass(frozen=True)
+class LatticeArc:
+    from_id: int
+    to_id: int
+    ilabel: int
+    olabel: int
+    graph_cost: float
+    acoustic_cost: float
+    tie: int = field(compare=False, default=0)
+
+
+def _i32(x):
+    return np.ascontiguousarray(x, dtype=np.int32)
+
+
+def _i64(x):
+    return np.ascontiguousarray(x, dtype=np.int64)
+
+
+def _f64(x):
+    return np.ascontiguousarray(x, dtype=np.float64)
+
+
+class Lattice:
+    """Array-backed lattice.  Node i = (node_state[i], node_step[i]); node 0 is the start
+    node; arcs are parallel arrays; finals map node id -> final weight."""
+
+    __slots__ = ("node_state", "node_step", "arc_from", "arc_to", "arc_il", "arc_ol", "arc_g",
+                 "arc_a", "arc_tie", "final_node", "final_w", "_nodes", "_arcs", "_finals")
+
+    def __init__(self, node_state=(), node_step=(), arc_from=(), arc_to=(), arc_il=(), arc_ol=(),
+                 arc_g=(), arc_a=(), arc_tie=(), final_node=(), final_w=()):
+        self.node_state = _i32(node_state)
+        self.node_step = _i32(node_step)
+        self.arc_from = _i64(arc_from)
+        self.arc_to = _i64(arc_to)
+        self.arc_il = _i32(arc_il)
+        self.arc_ol = _i32(arc_ol)
+        self.arc_g = _f64(arc_g)
+        self.arc_a = _f64(arc_a)
+        self.arc_tie = _i64(arc_tie)
+        self.final_node = _i64(final_node)
+        self.final_w = _f64(final_w)
+        self._nodes = self._arcs = self._finals = None
+
+    # ---------------------------------------------------------------- reference surface
+    @property
+    def start_id(self):
+        return 0 if len(self.node_state) else None
+
+    @property
+    def nodes(self) -> tuple:
+        if self._nodes is None:
+            self._nodes = tuple(LatticeNode(s, t) for s, t in
+                                zip(self.node_state.tolist(), self.node_step.tolist()))
+        return self._nodes
+
+    @property
+    def arcs(self) -> tuple:
+        if self._arcs is None:
+            self._arcs = tuple(LatticeArc(*x) for x in zip(
+                self.arc_from.tolist(), self.arc_to.tolist(), self.arc_il.tolist(),
+                self.arc_ol.tolist(), self.arc_g.tolist(), self.arc_a.tolist(),
+                self.arc_tie.tolist()))
+        return self._arcs
+
+    @property
+    def finals(self) -> dict:
+        if self._finals is None:
+            self._finals = dict(zip(self.final_node.tolist(), self.final_w.tolist()))
+        return self._finals
+
+    @property
+    def is_empty(self) -> bool:
+        return self.start_id is None or len(self.final_node) == 0
+
+    @property
+    def num_nodes(self) -> int:
+        return len(self.node_state)
+
+    @property
+    def num_arcs(self) -> int:
+        return len(self.arc_from)
+
+    def out_adjacency(self) -> list:
+        adj = [[] for _ in range(self.num_nodes)]
+        for a in self.arcs:
+            adj[a.from_id].append(a)
+        return adj
+
+    def in_adjacency(self) -> list:
+        adj = [[] for _ in range(self.num_nodes)]
+        for a in self.arcs:
+            adj[a.to_id].append(a)
+        return adj
+
+    def key(self):
+        """Structural identity as the reference's ``Lattice.__eq__`` sees it (tie excluded)."""
+        if self.start_id is None:
+            return ("EMPTY",)
+        nodes = tuple(zip(self.node_state.tolist(), self.node_step.tolist()))
+        arcs = tuple(zip(self.arc_from.tolist(), self.arc_to.tolist(), self.arc_il.tolist(),
+                         self.arc_ol.tolist(), self.arc_g.tolist(), self.arc_a.tolist()))
+        return (nodes, arcs, 0, self.finals)
+
+    def __eq__(self, other):
+        if isinstance(other, Lattice):
+            return self.key() == other.key()
+        if hasattr(other, "nodes") and hasattr(other, "arcs") and hasattr(other, "finals"):
+            return self.key() == _reference_key(other)
+        return NotImplemented
+
+    def __hash__(self):  # pragma: no cover - frozen-dataclass parity, rarely used
+        return hash((self.num_nodes, self.num_arcs))
+
+    def __repr__(self):
+        return f"Lattice(nodes={self.num_nodes}, arcs={self.num_arcs}, finals={len(self.final_node)})"
+
+    # ---------------------------------------------------------------- conversions
+    @classmethod
+    def from_reference(cls, lat) -> "Lattice":
+        """Array form of a reference ``lsd_wfst.lattice.Lattice``."""
+        if lat.start_id is None:
+            return EMPTY_LATTICE
+        a = lat.arcs
+        fin = list(lat.finals.items())
+        return cls([n.state for n in lat.nodes], [n.step for n in lat.nodes],
+                   [x.from_id for x in a], [x.to_id for x in a], [x.ilabel for x in a],
+                   [x.olabel for x in a], [x.graph_cost for x in a], [x.acoustic_cost for x in a],
+                   [x.tie for x in a], [k for k, _ in fin], [w for _, w in fin])
+
+    def _view(self):
+        """wb_lattice_arrays over this lattice's buffers (kept alive by self)."""
+        from . import _native as N
+        P = lambda x: x.ctypes.data  # noqa: E731
+        return N.LatticeArrays(self.num_nodes, self.num_arcs, len(self.final_node),
+                               P(self.node_state), P(self.node_step), P(self.arc_from),
+                               P(self.arc_to), P(self.arc_tie), P(self.arc_il), P(self.arc_ol),
+                               P(self.arc_g), P(self.arc_a), P(self.final_node), P(self.final_w))
+
+    @classmethod
+    def _from_native(cls, v) -> "Lattice":
+        if v.n_nodes == 0:
+            return EMPTY_LATTICE
+
+        def arr(p, n, t):
+            if n == 0:
+                return np.zeros(0, t)
+            return np.ctypeslib.as_array(C.cast(p, C.POINTER(np.ctypeslib.as_ctypes_type(t))),
+                                         shape=(n,)).copy()
+        nn, na, nf = v.n_nodes, v.n_arcs, v.n_finals
+        return cls(arr(v.node_state, nn, np.int32), arr(v.node_step, nn, np.int32),
+                   arr(v.arc_from, na, np.int64), arr(v.arc_to, na, np.int64),
+                   arr(v.arc_il, na, np.int32), arr(v.arc_ol, na, np.int32),
+                   arr(v.arc_g, na, np.float64), arr(v.arc_a, na, np.float64),
+                   arr(v.arc_tie, na, np.int64), arr(v.final_node, nf, np.int64),
+                   arr(v.final_w, nf, np.float64))
+
+
+def _reference_key(lat):
+    if lat.start_id is None:
+        return ("EMPTY",)
+    nodes = tuple((n.state, n.step) for n in lat.nodes)
+    arcs = tuple((a.from_id, a.to_id, a.ilabel, a.olabel, a.graph_cost, a.acoustic_cost)
+                 for a in lat.arcs)
+    return (nodes, arcs, lat.start_id, dict(lat.finals))
+
+
+EMPTY_LATTICE = Lattice()
+
+
+# ---------------------------------------------------------------- device lattice -> Lattice
+def canonical_from_device(wfst, nodes: np.ndarray, arcs: np.ndarray, arc_ac: np.ndarray,
+                          finals: np.ndarray, final_w: np.ndarray) -> Lattice:
+    """Order one utterance's trimmed device lattice canonically (_assemble, lattice.py:215-236):
+    nodes [start] + sorted by (step, state); arcs sorted by (from.step, from.state, to.step,
+    to.state, ilabel, olabel, tie) with tie = the WFST arc index."""
+    if len(nodes) == 0:
+        return EMPTY_LATTICE
+    st = nodes[:, 0].astype(np.int32)
+    sp = nodes[:, 1].astype(np.int32)
+    is_start = (st == wfst.start) & (sp == 0)
+    order = np.lexsort((st, sp, ~is_start))
+    newid = np.empty(len(order), dtype=np.int64)
+    newid[order] = np.arange(len(order))
+    ai = arcs[:, 2].astype(np.int64)
+    f = newid[arcs[:, 0].astype(np.int64)]
+    t = newid[arcs[:, 1].astype(np.int64)]
+    il = wfst.ilabel[ai]
+    ol = wfst.olabel[ai]
+    nst, nsp = st[order], sp[order]
+    aord = np.lexsort((ai, ol, il, nst[t], nsp[t], nst[f], nsp[f]))
+    fo = newid[finals.astype(np.int64)]
+    return Lattice(nst, nsp, f[aord], t[aord], il[aord], ol[aord], wfst.weight[ai][aord],
+                   arc_ac[aord], ai[aord], fo, final_w)
+
+
+class LatticeRecorder:
+    """Pass as ``recorder=`` to ``decode`` / ``decode_fsd`` / ``decode_lsd`` /
+    ``parallel_decode`` (lattice.py:96-135): the device records the raw lattice of that
+    decode, and ``build_lattice(recorder, wfst)`` returns it.  The per-relaxation callbacks of
+    the reference protocol have no host equivalent (recording happens inside the kernel)."""
+
+    def __init__(self, consumer=None):
+        self._lattice = None
+        self.final_step = None
+        self.final_state = None
+        self.reached_final = False
+        self._consumer = consumer
+
+    def _set(self, lat: Lattice, final_step: int, final_state: int, reached: bool):
+        self._lattice = lat
+        self.final_step = final_step
+        self.final_state = final_state
+        self.reached_final = reached
+
+
+def _check(lat: Lattice) -> None:
+    from . import _native as N
+    if lat.is_empty:
+        return
+    v = lat._view()
+    rc = N.load().wb_lattice_check(C.byref(v))
+    N.check(rc, "lattice")
+
+
+def build_lattice(recorder: LatticeRecorder, wfst=None) -> Lattice:
+    """The lattice of the decode ``recorder`` was attached to (lattice.py:240-249); raises
+    LatticeError on an epsilon cycle among its nodes (lattice.py:186)."""
+    if recorder._lattice is None:
+        if recorder.final_step is None:
+            return EMPTY_LATTICE
+        raise LatticeError("decode trace is incomplete (finish was never recorded)")
+    _check(recorder._lattice)
+    return recorder._lattice
+
+
+def prune_lattice(lat: Lattice, lattice_beam: float) -> Lattice:
+    """Keep exactly the paths within ``lattice_beam`` of the best (lattice.py:359-501)."""
+    from . import _native as N
+    if lattice_beam < 0:
+        raise ValueError(f"lattice_beam must be >= 0, got {lattice_beam}")
+    if not isinstance(lat, Lattice):
+        lat = Lattice.from_reference(lat)
+    if lat.is_empty:
+        return EMPTY_LATTICE
+    v = lat._view()
+    out = N.LatticeArrays()
+    rc = N.load().wb_lattice_prune(C.byref(v), float(lattice_beam), C.byref(out))
+    try:
+        N.check(rc, "prune_lattice")
+        return Lattice._from_native(out)
+    finally:
+        N.load().wb_lattice_arrays_free(C.byref(out))
+
+
+def lattice_best_path(lat: Lattice) -> tuple[float, tuple[int, ...], tuple[int, ...]]:
+    """Minimum-cost start-to-final path (cost, olabels, ilabels), ties as the decoder
+    resolves them (lattice.py:504-559)."""
+    from . import _native as N
+    if not isinstance(lat, Lattice):
+        lat = Lattice.from_reference(lat)
+    if lat.is_empty:
+        raise LatticeError("cannot extract a best path from an empty lattice")
+    v = lat._view()
+    cap = max(lat.num_arcs, 1)
+    ol = np.zeros(cap, np.int32)
+    il = np.zeros(cap, np.int32)
+    cost = C.c_double()
+    no, ni = C.c_int32(), C.c_int32()
+    rc = N.load().wb_lattice_best_path(C.byref(v), C.byref(cost), ol.ctypes.data, C.byref(no),
+                                       il.ctypes.data, C.byref(ni), cap)
+    N.check(rc, "lattice_best_path")
+    return float(cost.value), tuple(ol[:no.value].tolist()), tuple(il[:ni.value].tolist())
+
+
+# ---------------------------------------------------------------- text form (lattice.py:562-627)
+def format_lattice_text(lat: Lattice) -> str:
+    """Serialise; node id 0 is the start node."""
+    if not isinstance(lat, Lattice):
+        lat = Lattice.from_reference(lat)
+    out = [f"LATTICE nodes={lat.num_nodes} arcs={lat.num_arcs}"]
+    fin = lat.finals
+    for i, (s, t) in enumerate(zip(lat.node_state.tolist(), lat.node_step.tolist())):
+        out.append(f"N {i} {s} {t} final {fin[i]!r}" if i in fin else f"N {i} {s} {t}")
+    for f, t, il, ol, g, a in zip(lat.arc_from.tolist(), lat.arc_to.tolist(),
+                                  lat.arc_il.tolist(), lat.arc_ol.tolist(),
+                                  lat.arc_g.tolist(), lat.arc_a.tolist()):
+        out.append(f"A {f} {t} {il} {ol} {g!r} {a!r}")
+    return "\n".join(out) + "\n"
+
+
+def parse_lattice_text(text: str) -> Lattice:
+    rows = [r for r in (x.strip() for x in text.splitlines()) if r and not r.startswith("#")]
+    if not rows:
+        return EMPTY_LATTICE
+    head = rows[0].split()
+    if (len(head) != 3 or head[0] != "LATTICE" or not head[1].startswith("nodes=")
+            or not head[2].startswith("arcs=")):
+        raise LatticeError(f"bad lattice header {rows[0]!r}")
+    try:
+        n_nodes, n_arcs = int(head[1][6:]), int(head[2][5:])
+    except ValueError:
+        raise LatticeError(f"bad lattice header {rows[0]!r}") from None
+    st, sp, fn, fw = [], [], [], []
+    af, at, ail, aol, ag, aa = [], [], [], [], [], []
+    for r in rows[1:]:
+        x = r.split()
+        if x[0] == "N":
+            if len(x) not in (4, 6) or (len(x) == 6 and x[4] != "final"):
+                raise LatticeError(f"bad node line {r!r}")
+            if int(x[1]) != len(st):
+                raise LatticeError(f"node ids must be dense and ordered; got {r!r}")
+            st.append(int(x[2]))
+            sp.append(int(x[3]))
+            if len(x) == 6:
+                fn.append(len(st) - 1)
+                fw.append(float(x[5]))
+        elif x[0] == "A":
+            if len(x) != 7:
+                raise LatticeError(f"bad arc line {r!r}")
+            af.append(int(x[1])); at.append(int(x[2])); ail.append(int(x[3]))
+            aol.append(int(x[4])); ag.append(float(x[5])); aa.append(float(x[6]))
+        else:
+            raise LatticeError(f"unrecognized lattice line {r!r}")
+    if len(st) != n_nodes or len(af) != n_arcs:
+        raise LatticeError(f"header declares {n_nodes} nodes / {n_arcs} arcs, "
+                           f"found {len(st)} / {len(af)}")
+    if not st:
+        return EMPTY_LATTICE
+    for i, (f, t) in enumerate(zip(af, at)):
+        if not (0 <= f < len(st) and 0 <= t < len(st)):
+            raise LatticeError(f"arc {i} references a missing node")
+        if sp[t] - sp[f] not in (0, 1):
+            raise LatticeError(f"arc {i} must stay in step or advance one step, "
+                               f"got delta {sp[t] - sp[f]}")
+    return Lattice(st, sp, af, at, ail, aol, ag, aa, list(range(len(af))), fn, fw)
+
+
+def save_lattice(lat: Lattice, path: str) -> None:
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.write(format_lattice_text(lat))
+
+
+def load_lattice(path: str) -> Lattice:
+    with open(path, "r", encoding="utf-8") as fh:
+        return parse_lattice_text(fh.read())
+
+
+__all__ = ["COST_EPS", "EMPTY_LATTICE", "Lattice", "LatticeArc", "LatticeError", "LatticeNode",
+           "LatticeRecorder", "build_lattice", "canonical_from_device", "format_lattice_text",
+           "lattice_best_path", "load_lattice", "parse_lattice_text", "prune_lattice",
+           "save_lattice"]

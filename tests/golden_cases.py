@@ -52,6 +52,15 @@ class Case:
     lattice: object = None      # "error" | "empty" | lattice key tuple | None (not recorded)
     pruned: list | None = None  # per prune beam: "error" | "empty" | key tuple
     best_path: tuple | None = None
+    lattice_arrays: dict | None = None  # raw npz arrays of the built lattice (incl. tie)
+
+    def lattice_object(self):
+        """The built reference lattice as a package ``Lattice`` (ties included)."""
+        from paper_1808_00687_b200.lattice import Lattice
+        z = self.lattice_arrays
+        n, ai, af = z["nodes"], z["arcs_i"], z["arcs_f"]
+        return Lattice(n[:, 0], n[:, 1], ai[:, 0], ai[:, 1], ai[:, 2], ai[:, 3], af[:, 0],
+                       af[:, 1], ai[:, 4], z["fin_i"], z["fin_w"])
 
 
 def _f(x):
@@ -86,6 +95,9 @@ def load() -> tuple[list[Case], list[float]]:
         case = Case(i, c["kind"], c["seed"], g, z[f"{i}_costs"], z[f"{i}_blank"], cfg, exp)
         if "lattice" in c:
             case.lattice = _lat_key(z, f"{i}_lat", c["lattice"])
+            if c["lattice"] not in ("error", "empty"):
+                case.lattice_arrays = {k: z[f"{i}_lat_{k}"] for k in
+                                       ("nodes", "arcs_i", "arcs_f", "fin_i", "fin_w")}
             if "pruned" in c:
                 case.pruned = [_lat_key(z, f"{i}_lat_p{bi}", t) for bi, t in enumerate(c["pruned"])]
             if "best_path" in c:

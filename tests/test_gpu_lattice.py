@@ -1,0 +1,120 @@
+"""Device lattice recording + trimming (decode_kernel.cuh record_lattice_step / trim_lattice)
+against the reference's built lattices (golden fixtures) and the oracle's build_lattice.
+
+Bit-exact bar: same nodes, arcs (graph + acoustic costs as f64), finals and canonical order
+as the reference's build_lattice (lattice.py:148-249); tie = WFST arc index, so the lattice
+best path equals the reference's too.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import golden_cases as GC
+from oracle import oracle as O
+from paper_1808_00687_b200 import lattice as L
+from paper_1808_00687_b200 import synth
+from paper_1808_00687_b200.decoder import BatchDecoder, DecodeConfig
+
+pytestmark = pytest.mark.gpu
+INF = math.inf
+
+
+def _key(lat):
+    return "empty" if lat.start_id is None else lat.key()
+
+
+def _decode_lattices(g, costs_list, blank_list, cfg, dec=None):
+    dec = dec or BatchDecoder(g, 0, max_utts_in_flight=8)
+    T = np.asarray([len(c) for c in costs_list], np.int32)
+    off = np.zeros(len(T), np.int64)
+    np.cumsum(T[:-1], out=off[1:])
+    L1 = costs_list[0].shape[1]
+    costs = np.concatenate([c.reshape(-1, L1) for c in costs_list]) if T.sum() else np.zeros((1, L1))
+    blank = np.concatenate(blank_list) if T.sum() else np.zeros(1)
+    out = dec.decode_host(costs, off, T, blank, cfg, cfg.mode, lattice=True)
+    lats = dec.fetch_lattices(dec.graph.wfst)
+    return out, lats
+
+
+def test_gpu_lattice_matches_reference_golden(cuda):
+    n = 0
+    beams = GC.prune_beams()
+    for case in GC.cases():
+        if case.lattice is None:
+            continue
+        g = case.graph.to_wfst()
+        cfg = DecodeConfig(beam=case.cfg.get("beam", INF), max_active=case.cfg.get("max_active"),
+                           mode=case.cfg.get("mode", "lsd"))
+        out, lats = _decode_lattices(g, [case.costs], [case.blank], cfg)
+        lat = lats[0]
+        if case.lattice == "error":
+            with pytest.raises(L.LatticeError):
+                L._check(lat)
+            continue
+        assert _key(lat) == case.lattice, (case.kind, case.seed)
+        if case.best_path is not None:
+            assert L.lattice_best_path(lat) == case.best_path
+        for b, exp in zip(beams, case.pruned or []):
+            try:
+                got = _key(L.prune_lattice(lat, b))
+            except L.LatticeError:
+                got = "error"
+            assert got == exp, (case.kind, case.seed, b)
+        n += 1
+    assert n > 50
+
+
+@pytest.mark.parametrize("mode", ["fsd", "lsd"])
+def test_gpu_lattice_batch_matches_oracle(cuda, mode):
+    """Many utterances per launch, random graphs with epsilon arcs, beam + max-active."""
+    for seed in range(4):
+        g = synth.random_wfst(seed, 300, 1200, 16, eps_fraction=0.06, selfloops=True,
+                              final_fraction=0.1)
+        posts = [synth.random_posteriors(1000 * seed + i, 12 + 5 * i, 16, blank_fraction=0.3)
+                 for i in range(10)]
+        from paper_1808_00687_b200.posteriors import cost_table
+        costs = [cost_table(p) for p in posts]
+        blanks = [np.ascontiguousarray(p.rows[:, 0]) for p in posts]
+        cfg = DecodeConfig(beam=7.0, max_active=40, mode=mode)
+        out, lats = _decode_lattices(g, costs, blanks, cfg)
+        for i, (c, b) in enumerate(zip(costs, blanks)):
+            try:
+                res, olat = O.decode(g, c, b, beam=7.0, max_active=40, mode=mode,
+                                     return_lattice=True)
+                exp = olat.key() if not olat.empty else ("EMPTY",)
+            except O.OracleLatticeError:
+                with pytest.raises(L.LatticeError):
+                    L._check(lats[i])
+                continue
+            assert lats[i].key() == exp, (seed, i)
+            r = out.results[i]
+            assert int(r["final_step"]) == res.final_step
+
+
+def test_gpu_lattice_recorder_api(cuda):
+    """decode(..., recorder=LatticeRecorder()) + build_lattice, as the reference is called."""
+    import paper_1808_00687_b200 as P
+    g = synth.random_wfst(3, 200, 800, 12, eps_fraction=0.05, final_fraction=0.2)
+    p = synth.random_posteriors(5, 25, 12)
+    rec = L.LatticeRecorder()
+    r = P.decode(g, p, P.DecodeConfig(beam=8.0, mode="fsd"), recorder=rec)
+    lat = L.build_lattice(rec, g)
+    if not lat.is_empty:
+        cost, ol, il = L.lattice_best_path(lat)
+        assert cost == r.total_cost and ol == r.olabels and il == r.ilabels
+
+
+def test_gpu_lattice_capacity_retry(cuda):
+    """Tiny raw-lattice / output pools overflow and are grown transparently."""
+    g = synth.random_wfst(11, 300, 1200, 16, eps_fraction=0.05, final_fraction=0.1)
+    posts = [synth.random_posteriors(50 + i, 40, 16) for i in range(6)]
+    from paper_1808_00687_b200.posteriors import cost_table
+    costs = [cost_table(p) for p in posts]
+    blanks = [np.ascontiguousarray(p.rows[:, 0]) for p in posts]
+    cfg = DecodeConfig(beam=9.0, mode="fsd")
+    small = BatchDecoder(g, 0, max_utts_in_flight=3, lattice_capacity=1024,
+                         lattice_out_capacity=64)
+    _, lats = _decode_lattices(g, costs, blanks, cfg, dec=small)
+    _, ref = _decode_lattices(g, costs, blanks, cfg)
+    assert [x.key() for x in lats] == [x.key() for x in ref]

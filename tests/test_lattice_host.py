@@ -1,0 +1,99 @@
+"""Lattice post-processing behind the C ABI (csrc/lattice_host.cpp), CPU only: prune_lattice
+and lattice_best_path against the reference's own outputs (golden fixtures), text round trip,
+and the reference's error behaviour (lattice.py:359-365, 504-512, 579-627)."""
+import math
+
+import numpy as np
+import pytest
+
+import golden_cases as GC
+from paper_1808_00687_b200 import lattice as L
+
+INF = math.inf
+
+
+def _key(lat):
+    return "empty" if lat.start_id is None else lat.key()
+
+
+def _lattice_cases():
+    return [c for c in GC.cases() if c.lattice_arrays is not None]
+
+
+def test_golden_lattices_load():
+    cs = _lattice_cases()
+    assert len(cs) > 50
+    for c in cs:
+        assert c.lattice_object().key() == c.lattice
+
+
+def test_prune_matches_reference_golden():
+    beams = GC.prune_beams()
+    n = 0
+    for c in _lattice_cases():
+        lat = c.lattice_object()
+        for b, exp in zip(beams, c.pruned or []):
+            try:
+                got = _key(L.prune_lattice(lat, b))
+            except L.LatticeError:
+                got = "error"
+            assert got == exp, (c.idx, b)
+            n += 1
+    assert n > 500
+
+
+def test_best_path_matches_reference_golden():
+    n = 0
+    for c in _lattice_cases():
+        if c.best_path is None:
+            continue
+        assert L.lattice_best_path(c.lattice_object()) == c.best_path, c.idx
+        n += 1
+    assert n > 50
+
+
+def test_prune_is_idempotent_at_infinite_beam():
+    for c in _lattice_cases()[:40]:
+        lat = c.lattice_object()
+        p = L.prune_lattice(lat, INF)
+        assert _key(L.prune_lattice(p, INF)) == _key(p)
+
+
+def test_text_round_trip():
+    for c in _lattice_cases()[:40]:
+        lat = c.lattice_object()
+        back = L.parse_lattice_text(L.format_lattice_text(lat))
+        assert back == lat
+    assert L.parse_lattice_text("") is L.EMPTY_LATTICE
+
+
+def test_errors():
+    with pytest.raises(ValueError):
+        L.prune_lattice(L.EMPTY_LATTICE, -1.0)
+    assert L.prune_lattice(L.EMPTY_LATTICE, 1.0) is L.EMPTY_LATTICE
+    with pytest.raises(L.LatticeError):
+        L.lattice_best_path(L.EMPTY_LATTICE)
+    with pytest.raises(L.LatticeError):
+        L.parse_lattice_text("LATTICE nodes=1 arcs=0\nN 0 0 0\nQ\n")
+    with pytest.raises(L.LatticeError):
+        L.parse_lattice_text("LATTICE nodes=2 arcs=0\nN 0 0 0\n")
+
+
+def test_epsilon_cycle_is_rejected():
+    # two nodes in one step joined by epsilon arcs both ways
+    lat = L.Lattice([0, 1], [0, 0], [0, 1], [1, 0], [0, 0], [0, 0], [0.5, 0.5], [0.0, 0.0],
+                    [0, 1], [1], [0.0])
+    with pytest.raises(L.LatticeError):
+        L.prune_lattice(lat, 1.0)
+    with pytest.raises(L.LatticeError):
+        L._check(lat)
+
+
+def test_reference_shaped_equality():
+    c = _lattice_cases()[0]
+    lat = c.lattice_object()
+    ref_like = type("RefLat", (), {})()
+    ref_like.nodes, ref_like.arcs = lat.nodes, lat.arcs
+    ref_like.start_id, ref_like.finals = 0, dict(lat.finals)
+    assert lat == ref_like
+    assert np.array_equal(L.Lattice.from_reference(ref_like).arc_tie, lat.arc_tie)
