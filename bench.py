@@ -52,6 +52,11 @@ CONFIGS = {
                     "1000 frames, beam 13, max-active 7000, FSD", states=30_000, arcs=90_000,
                labels=3000, utts=64, frames=1000, beam=13.0, max_active=7000, mode="fsd",
                blank_fraction=0.0, eps=0.015, selfloops=False, final_fraction=0.01),
+    "3": dict(name="config3: config-2 graph with exact lattice generation + lattice-beam 8 "
+                   "pruning, 256 utt x 1000 frames, beam 13, max-active 7000, FSD",
+              states=1_000_000, arcs=3_000_000, labels=3000, utts=256, frames=1000, beam=13.0,
+              max_active=7000, mode="fsd", blank_fraction=0.0, eps=0.015, selfloops=False,
+              final_fraction=0.01, lattice_beam=8.0),
     "4": dict(name="config4: CTC LSD, 5k-label synthetic TLG-like graph (self-loops), 256 utt x "
                    "1500 frames, 80% blank frames, blank-skip threshold 0.98, beam 13, "
                    "max-active 7000", states=100_000, arcs=300_000, labels=5000, utts=256,
@@ -169,8 +174,23 @@ def cpu_sample(g, cfg, L1, n_threads: int, frames: int):
         blanks.append(np.ascontiguousarray(rows[:, 0]))
     og = O.OracleGraph(g)
     t0 = time.perf_counter()
-    res = O.decode_batch(og, costs, blanks, beam=cfg["beam"], max_active=cfg["max_active"],
-                         mode=cfg["mode"], n_threads=n_threads)
+    if cfg.get("lattice_beam") is None:
+        res = O.decode_batch(og, costs, blanks, beam=cfg["beam"], max_active=cfg["max_active"],
+                             mode=cfg["mode"], n_threads=n_threads)
+    else:   # decode + build_lattice + prune_lattice per utterance, one utterance per thread
+        from concurrent.futures import ThreadPoolExecutor
+
+        def one(i):
+            r, lat = O.decode(og, costs[i], blanks[i], beam=cfg["beam"],
+                              max_active=cfg["max_active"], mode=cfg["mode"],
+                              return_lattice=True)
+            try:
+                O.prune_lattice(lat, cfg["lattice_beam"])
+            except O.OracleLatticeError:
+                pass
+            return r
+        with ThreadPoolExecutor(n_threads) as ex:
+            res = list(ex.map(one, range(n)))
     wall = time.perf_counter() - t0
     return wall, n * frames, res
 
@@ -257,7 +277,8 @@ def main():
 
     block = args.block or 1024
     dec = BatchDecoder(g, local, max_utts_in_flight=min(utts, 148), block_threads=args.block)
-    dec.reserve(int(T.sum()) + utts, cfg["max_active"], int(T.max()))
+    lat_on = cfg.get("lattice_beam") is not None
+    dec.reserve(int(T.sum()) + utts, cfg["max_active"], int(T.max()), lattice=lat_on)
     cap = frames + 64
 
     dev = torch.device(f"cuda:{local}")
@@ -272,7 +293,8 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def step():
-        dec.decode_device(costs_d, off_d, T_d, blank_d, dcfg, cfg["mode"], res_d, ol_d, il_d, cap)
+        dec.decode_device(costs_d, off_d, T_d, blank_d, dcfg, cfg["mode"], res_d, ol_d, il_d, cap,
+                          lattice=lat_on)
 
     for _ in range(max(args.warmup, 0)):
         step()
@@ -318,16 +340,38 @@ def main():
 
     # ---------------- e2e through the C ABI with host buffers
     e2e = None
+    lat_stats = None
     if not (args.no_e2e or args.profile):
+        from paper_1808_00687_b200.lattice import LatticeError, prune_lattice
         costs_np, blank_np = costs_h.numpy(), blank_h.numpy()
-        dec.decode_host(costs_np, off, T, blank_np, dcfg, cfg["mode"], cap)  # warm
+
+        def e2e_step():
+            o = dec.decode_host(costs_np, off, T, blank_np, dcfg, cfg["mode"], cap,
+                                lattice=lat_on)
+            st = None
+            if lat_on:   # reference path: decode + build_lattice + prune_lattice(lb)
+                lats = dec.fetch_lattices(dec.graph.wfst)
+                st = {"lattices": len(lats), "nodes": 0, "arcs": 0, "pruned_nodes": 0,
+                      "pruned_arcs": 0, "prune_errors": 0}
+                for lat in lats:
+                    st["nodes"] += lat.num_nodes
+                    st["arcs"] += lat.num_arcs
+                    try:
+                        p = prune_lattice(lat, cfg["lattice_beam"])
+                        st["pruned_nodes"] += p.num_nodes
+                        st["pruned_arcs"] += p.num_arcs
+                    except LatticeError:
+                        st["prune_errors"] += 1
+            return o, st
+
+        e2e_step()  # warm
         e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                 for _ in range(args.steps)]
         barrier()
         for k in range(args.steps):
             flush.zero_()
             e_ev[k][0].record()
-            out = dec.decode_host(costs_np, off, T, blank_np, dcfg, cfg["mode"], cap)
+            out, lat_stats = e2e_step()
             e_ev[k][1].record()
             torch.cuda.synchronize()
         barrier()
@@ -338,6 +382,8 @@ def main():
             e_ms = float(t.item())
         h2d = costs_np.nbytes + blank_np.nbytes + off.nbytes + T.nbytes
         d2h = out.results.nbytes + out.olabels.nbytes + out.ilabels.nbytes
+        if lat_stats:   # trimmed lattice pools: node 8 B, arc 16 + 8 B, meta 48 B / utt
+            d2h += 8 * lat_stats["nodes"] + 24 * lat_stats["arcs"] + 48 * utts
         e2e = {"value": frames_step * world * args.steps / (e_ms / 1e3), "unit": "frames/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": e_ms / args.steps}
@@ -380,6 +426,7 @@ def main():
                          "kernel": "decode_kernel", "kernel_ms": avg_kernel_ms,
                          "algorithmic_bytes": nbytes, "peak_source": peak_src},
             "cpu_baseline": cpu,
+            "lattice": lat_stats,
             "e2e": e2e,
             "clocks": clocks,
             "gpu_launches": 2 * args.steps,

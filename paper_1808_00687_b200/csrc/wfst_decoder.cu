@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -254,10 +255,23 @@ static cudaError_t launch_decode(int max_grid, int num_sms, int num_cols, cudaSt
                                  const CfgDev &cd, wb_utt_result *res) {
     // One lane per SM: dynamic shared memory holds the cost row during expansion, then the
     // step's candidate keys + flags (as many as fit; larger steps spill to global memory).
+    // lift the 48 KB default first: the occupancy query honours the current attribute
+    int dev = 0, optin = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(decode_kernel<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    if (e != cudaSuccess) return e;
     size_t avail = 0;
-    cudaError_t e = cudaOccupancyAvailableDynamicSMemPerBlock(&avail, decode_kernel<BLOCK>, 1, BLOCK);
+    e = cudaOccupancyAvailableDynamicSMemPerBlock(&avail, decode_kernel<BLOCK>, 1, BLOCK);
     if (e != cudaSuccess) return e;
     const size_t hdr = smem_hdr<BLOCK>();
+    // Cap the carve-out at 100 KB: the rest of the SM's 256 KB stays L1 for the graph's arc
+    // records and the call stack.  Measured (config 2): 48-160 KB all ~207 ms, the full 227 KB
+    // 331 ms (L1 shrinks to 28 KB and stack reloads miss).  WB_SMEM_KB overrides (tuning).
+    size_t cap = 100 * 1024;
+    if (const char *cap_kb = std::getenv("WB_SMEM_KB")) cap = (size_t)std::atoi(cap_kb) * 1024;
+    if (cap > 0 && cap < avail) avail = cap;
     avail = avail > 1024 + hdr ? avail - 1024 - hdr : 0;
     size_t row = num_cols <= ROW_SMEM_MAX ? sizeof(double) * (size_t)num_cols : 0;
     if (row > avail) row = 0;  // the kernel reads the row from global memory instead

@@ -298,11 +298,12 @@ class BatchDecoder:
 
     # ------------------------------------------------------------------ device buffers
     def decode_device(self, costs, row_offset, num_frames, blank, cfg, mode: str, results,
-                      olabels, ilabels, label_capacity: int, stream=None):
+                      olabels, ilabels, label_capacity: int, stream=None, lattice: bool = False):
         """Enqueue a decode on device-resident torch tensors (no host sync besides the
-        frame-count read); ``results`` is a uint8 CUDA tensor of n * itemsize bytes."""
+        frame-count read); ``results`` is a uint8 CUDA tensor of n * itemsize bytes.  With
+        ``lattice`` the trimmed lattices stay on the device until ``fetch_lattices``."""
         n = int(num_frames.numel())
-        ncfg = _native_config(cfg, mode)
+        ncfg = _native_config(cfg, mode, lattice)
         if stream is None:
             import torch
             stream = torch.cuda.current_stream(self.device).cuda_stream
