@@ -134,8 +134,9 @@ int wb_decoder_device_bytes(wb_decoder_t d, int64_t *bytes);
  *
  * memory_kind WB_MEM_DEVICE: pointers are device pointers, work is enqueued on `stream`
  * (a cudaStream_t, may be NULL) and the call returns without synchronising.
- * memory_kind WB_MEM_HOST: pointers are host pointers (pinned for full copy bandwidth); the
- * call copies inputs in, decodes, copies results out and synchronises.
+ * memory_kind WB_MEM_HOST: pointers are host pointers; the call copies inputs in (a
+ * page-locked cost table is instead read zero-copy by the kernel, see wb_last_transfer),
+ * decodes, copies results out and synchronises.
  */
 int wb_decode(wb_decoder_t d, int32_t n_utts, const double *costs, const int64_t *row_offset,
               const int32_t *num_frames, int32_t num_cols, const double *blank,
@@ -192,6 +193,11 @@ void wb_lattice_arrays_free(wb_lattice_arrays *a);
 int wb_lattice_best_path(const wb_lattice_arrays *lat, double *cost, int32_t *olabels,
                          int32_t *n_olabels, int32_t *ilabels, int32_t *n_ilabels,
                          int32_t capacity);
+
+/* Host->device bytes of the last WB_MEM_HOST wb_decode call and whether its cost table was
+ * read zero-copy (page-locked host memory, one staged row per search step: the transfer
+ * overlaps the search and LSD reads only the non-blank rows).  Pageable tables are copied. */
+int wb_last_transfer(wb_decoder_t d, int64_t *h2d_bytes, int32_t *zero_copy);
 
 /* Device time (ms) of the decode kernel of the last wb_decode call (CUDA events on its stream). */
 int wb_last_kernel_ms(wb_decoder_t d, float *ms);

@@ -70,7 +70,7 @@ EXPORTED = ("wb_last_error", "wb_version", "wb_device_count", "wb_graph_create",
             "wb_graph_destroy", "wb_graph_device_bytes", "wb_decoder_create",
             "wb_decoder_destroy", "wb_decoder_device_bytes", "wb_decode", "wb_last_kernel_ms",
             "wb_lattice_totals", "wb_lattice_fetch", "wb_lattice_check", "wb_lattice_prune",
-            "wb_lattice_arrays_free", "wb_lattice_best_path")
+            "wb_lattice_arrays_free", "wb_lattice_best_path", "wb_last_transfer")
 
 
 def load():
@@ -95,6 +95,7 @@ def load():
                             C.c_void_p, C.POINTER(Config), C.c_void_p, C.c_void_p, C.c_void_p,
                             C.c_int32, C.c_int32, C.c_void_p]
     L.wb_last_kernel_ms.argtypes = [C.c_void_p, C.POINTER(C.c_float)]
+    L.wb_last_transfer.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
     L.wb_lattice_totals.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int64),
                                     C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     L.wb_lattice_fetch.argtypes = [C.c_void_p] + [C.c_void_p] * 6

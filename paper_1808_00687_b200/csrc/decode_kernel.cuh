@@ -39,9 +39,15 @@ constexpr u32 F_SURV = 1u, F_MARK = 2u, CA_NONE = 0xFFFFFFFFu;
 constexpr int MAX_EPS_ROUNDS = 1 << 20;
 // relaxations in flight per lane (expand) / gathers per thread (prune): halved for 1024-thread
 // CTAs, whose register budget is 64 per thread
+#ifndef WB_UNROLL_1024
+#define WB_UNROLL_1024 1
+#endif
+#ifndef WB_GATHER_1024
+#define WB_GATHER_1024 2
+#endif
 template <int BLOCK> struct Tune {
-    static constexpr int UNROLL = BLOCK >= 1024 ? 2 : 4;
-    static constexpr int GATHER = 4;
+    static constexpr int UNROLL = BLOCK >= 1024 ? WB_UNROLL_1024 : 4;
+    static constexpr int GATHER = BLOCK >= 1024 ? WB_GATHER_1024 : 4;
 };
 
 struct GraphDev {
@@ -897,8 +903,8 @@ __device__ int block_argmin_tok(u64 key, u32 st, int idx) {
 // recorder is needed.  Node / arc indices are utterance-global positions in this lane's pool.
 template <int BLOCK>
 __noinline__ __device__ int record_lattice_step(int k, int nxt, int n_surv, int prv, int n_prev,
-                                                const double *grow, u32 tagL, const GraphDev &g,
-                                                const WorkDev &ws) {
+                                                const double *grow, int L1, u32 tagL,
+                                                const GraphDev &g, const WorkDev &ws) {
     Smem<BLOCK> &sh = SH<BLOCK>();
     const Lane c{ws};
     constexpr int NW = BLOCK / 32;
@@ -929,6 +935,13 @@ __noinline__ __device__ int record_lattice_step(int k, int nxt, int n_surv, int 
         ws.ln_state[lo + node_base + j] = st;
     }
     if (k == 0 && threadIdx.x == 0) ws.lstep_start[blockIdx.x] = node_base + (extra ? n_surv : sh.ng);
+    // the step's cost row again in shared memory (the prune reused that space)
+    const double *row = grow;
+    if (k > 0 && ws.row_in_smem) {
+        double *srow = s_row<BLOCK>();
+        for (int q = threadIdx.x; q < L1; q += BLOCK) srow[q] = __ldg(&grow[q]);
+        row = srow;
+    }
     __syncthreads();
     const long long room = ws.lat_cap - arc_base;
     // emitting arcs from live(k-1)
@@ -954,7 +967,7 @@ __noinline__ __device__ int record_lattice_step(int k, int nxt, int n_surv, int 
                 double ac = 0.0;
                 if (j < tot) {
                     r = __ldg(&g.arcs[2 * a]);
-                    ac = __ldg(&grow[r.y]);
+                    ac = row[r.y];
                     rec = ac != INFINITY && ws.stag[so + r.x] == tagL;
                 }
                 const u32 m = __ballot_sync(FULL, rec);
@@ -1302,7 +1315,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
         long long lat_arcs = 0;
         if (cfg.lattice && status == WB_OK) {
             ++tag;
-            const int rs = record_lattice_step<BLOCK>(0, cur, so.n_surv, 0, 0, nullptr, tag, g, ws);
+            const int rs = record_lattice_step<BLOCK>(0, cur, so.n_surv, 0, 0, nullptr, 0, tag, g, ws);
             if (rs) status = rs;
         }
         int n_live = so.n_surv;
@@ -1347,7 +1360,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             if (cfg.lattice && status == WB_OK) {
                 ++tag;
                 const int rs = record_lattice_step<BLOCK>(s + 1, cur ^ 1, so.n_surv, cur, n_live, grow,
-                                                          tag, g, ws);
+                                                          b.L1, tag, g, ws);
                 if (rs) status = rs;
             }
             cur ^= 1;

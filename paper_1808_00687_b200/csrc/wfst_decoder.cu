@@ -66,6 +66,8 @@ struct wb_decoder_s {
     size_t h_off_n = 0, h_T_n = 0, h_res_n = 0, h_lab_n = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     size_t bytes = 0;
+    long long last_h2d = 0;   // bytes moved host -> device by the last WB_MEM_HOST call
+    int last_zero_copy = 0;
     // lattice mode (allocated on the first lattice decode)
     long long lat_cap = 0, lat_cap_want = 0, lat_out_want = 0;
     int lat_T = 0;
@@ -252,7 +254,7 @@ static int alloc_lattice(wb_decoder_s *d) {
 template <int BLOCK>
 static cudaError_t launch_decode(int max_grid, int num_sms, int num_cols, cudaStream_t st,
                                  const GraphDev &gd, WorkDev wd, const BatchDev &bd,
-                                 const CfgDev &cd, wb_utt_result *res) {
+                                 const CfgDev &cd, wb_utt_result *res, bool zero_copy) {
     // One lane per SM: dynamic shared memory holds the cost row during expansion, then the
     // step's candidate keys + flags (as many as fit; larger steps spill to global memory).
     // lift the 48 KB default first: the occupancy query honours the current attribute
@@ -275,6 +277,7 @@ static cudaError_t launch_decode(int max_grid, int num_sms, int num_cols, cudaSt
     avail = avail > 1024 + hdr ? avail - 1024 - hdr : 0;
     size_t row = num_cols <= ROW_SMEM_MAX ? sizeof(double) * (size_t)num_cols : 0;
     if (row > avail) row = 0;  // the kernel reads the row from global memory instead
+    if (zero_copy && row == 0) return cudaErrorNotSupported;  // host rows must be staged
     wd.smem_cands = (int)std::min<size_t>(avail / (sizeof(u64) + sizeof(u32)), (size_t)wd.cap);
     wd.row_in_smem = row > 0;
     size_t smem = hdr + std::max(row, (size_t)wd.smem_cands * (sizeof(u64) + sizeof(u32)));
@@ -408,6 +411,8 @@ int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row
     cudaStream_t st = (cudaStream_t)stream;
     if (n == 0) return WB_OK;
     const bool host = memory_kind == WB_MEM_HOST;
+    bool zc = false;
+    const double *zc_ptr = nullptr;
     const double *dc = costs, *db = blank;
     const long long *doff = (const long long *)row_offset;
     const int *dT = num_frames;
@@ -435,13 +440,28 @@ int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row
         if ((rc = grow(&d->h_T, d->h_T_n, nn))) return rc;
         if ((rc = grow(&d->h_res, d->h_res_n, nn))) return rc;
         if ((rc = grow(&d->h_lab, d->h_lab_n, nn * lcap * 2))) return rc;
-        if (ncost)
+        // Zero-copy: a page-locked cost table is read by the kernel straight from host memory,
+        // one staged row per search step, so the transfer overlaps the search and LSD reads
+        // only non-blank rows.  Pageable tables (or rows too wide to stage) are copied first.
+        zc = false;
+        const char *zc_env = std::getenv("WB_ZERO_COPY");
+        if (ncost && !(zc_env && zc_env[0] == '0')) {
+            cudaPointerAttributes pa;
+            if (cudaPointerGetAttributes(&pa, costs) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+                pa.devicePointer)
+                zc = true, zc_ptr = (const double *)pa.devicePointer;
+            else
+                cudaGetLastError();
+        }
+        if (ncost && !zc)
             CUDA_TRY(cudaMemcpyAsync(d->h_costs, costs, sizeof(double) * ncost, cudaMemcpyHostToDevice, st));
+        d->last_h2d = (long long)(sizeof(double) * (zc ? 0 : ncost) + sizeof(double) * rows +
+                                  (sizeof(long long) + sizeof(int)) * nn);
         if (rows)
             CUDA_TRY(cudaMemcpyAsync(d->h_blank, blank, sizeof(double) * rows, cudaMemcpyHostToDevice, st));
         CUDA_TRY(cudaMemcpyAsync(d->h_off, row_offset, sizeof(long long) * n, cudaMemcpyHostToDevice, st));
         CUDA_TRY(cudaMemcpyAsync(d->h_T, num_frames, sizeof(int) * n, cudaMemcpyHostToDevice, st));
-        dc = d->h_costs; db = d->h_blank; doff = d->h_off; dT = d->h_T; dres = d->h_res;
+        dc = zc ? zc_ptr : d->h_costs; db = d->h_blank; doff = d->h_off; dT = d->h_T; dres = d->h_res;
         dol = d->h_lab; dil = d->h_lab + nn * lcap;
     }
     // device mode: frame counts stay on the device; an LSD utterance longer than the frame
@@ -493,11 +513,25 @@ int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row
     int max_grid = std::min(n, d->slots);
     CUDA_TRY(cudaEventRecord(d->ev0, st));
     cudaError_t e;
-    switch (block) {
-        case 256: e = launch_decode<256>(max_grid, d->num_sms, num_cols, st, gd, wd, bd, cd, dres); break;
-        case 512: e = launch_decode<512>(max_grid, d->num_sms, num_cols, st, gd, wd, bd, cd, dres); break;
-        default: e = launch_decode<1024>(max_grid, d->num_sms, num_cols, st, gd, wd, bd, cd, dres); break;
+    auto launch = [&]() {
+        switch (block) {
+            case 256: return launch_decode<256>(max_grid, d->num_sms, num_cols, st, gd, wd, bd, cd, dres, zc);
+            case 512: return launch_decode<512>(max_grid, d->num_sms, num_cols, st, gd, wd, bd, cd, dres, zc);
+            default: return launch_decode<1024>(max_grid, d->num_sms, num_cols, st, gd, wd, bd, cd, dres, zc);
+        }
+    };
+    e = launch();
+    if (e == cudaErrorNotSupported && zc) {  // rows too wide to stage: copy the table instead
+        zc = false;
+        long long rows = 0;
+        for (int i = 0; i < n; ++i) rows = std::max<long long>(rows, row_offset[i] + num_frames[i]);
+        const size_t ncost = (size_t)rows * num_cols;
+        CUDA_TRY(cudaMemcpyAsync(d->h_costs, costs, sizeof(double) * ncost, cudaMemcpyHostToDevice, st));
+        d->last_h2d += (long long)(sizeof(double) * ncost);
+        bd.costs = d->h_costs;
+        e = launch();
     }
+    d->last_zero_copy = zc ? 1 : 0;
     if (e != cudaSuccess)
         return set_err(WB_ERR_CUDA, std::string("decode launch: ") + cudaGetErrorString(e));
     CUDA_TRY(cudaEventRecord(d->ev1, st));
@@ -512,7 +546,19 @@ int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row
                                      cudaMemcpyDeviceToHost, st));
         }
         CUDA_TRY(cudaStreamSynchronize(st));
+        if (zc) {  // rows the kernel staged from host memory: one per search step (+ lattice)
+            long long steps = 0;
+            for (int i = 0; i < n; ++i) steps += results[i].search_steps;
+            d->last_h2d += steps * (long long)num_cols * (long long)sizeof(double) * (cfg->lattice ? 2 : 1);
+        }
     }
+    return WB_OK;
+}
+
+int wb_last_transfer(wb_decoder_t d, int64_t *h2d_bytes, int32_t *zero_copy) {
+    if (!d || !h2d_bytes || !zero_copy) return set_err(WB_ERR_VALUE, "null argument");
+    *h2d_bytes = d->last_h2d;
+    *zero_copy = d->last_zero_copy;
     return WB_OK;
 }
 

@@ -203,6 +203,12 @@ class BatchDecoder:
         N.check(N.load().wb_decoder_device_bytes(self._h, C.byref(b)))
         return int(b.value)
 
+    def last_transfer(self) -> tuple[int, bool]:
+        """(host->device bytes, zero-copy?) of the last host-buffer decode."""
+        b, z = C.c_int64(), C.c_int32()
+        N.check(N.load().wb_last_transfer(self._h, C.byref(b), C.byref(z)))
+        return int(b.value), bool(z.value)
+
     def last_kernel_ms(self) -> float:
         ms = C.c_float()
         N.check(N.load().wb_last_kernel_ms(self._h, C.byref(ms)))
