@@ -57,6 +57,12 @@ CONFIGS = {
               states=1_000_000, arcs=3_000_000, labels=3000, utts=256, frames=1000, beam=13.0,
               max_active=7000, mode="fsd", blank_fraction=0.0, eps=0.015, selfloops=False,
               final_fraction=0.01, lattice_beam=8.0),
+    "5": dict(name="config5: large synthetic graph 7M states/20M arcs/512 pdfs, 4096 utt x 1000 "
+                   "frames in total sharded by utterance over the GPUs (strong scaling), beam 13, "
+                   "max-active 7000, FSD; 64 distinct posterior streams tiled",
+              states=7_000_000, arcs=20_000_000, labels=512, utts=4096, frames=1000, beam=13.0,
+              max_active=7000, mode="fsd", blank_fraction=0.0, eps=0.015, selfloops=False,
+              final_fraction=0.01, strong=True, distinct=64),
     "4": dict(name="config4: CTC LSD, 5k-label synthetic TLG-like graph (self-loops), 256 utt x "
                    "1500 frames, 80% blank frames, blank-skip threshold 0.98, beam 13, "
                    "max-active 7000", states=100_000, arcs=300_000, labels=5000, utts=256,
@@ -149,15 +155,27 @@ def make_workload(cfg: dict, rank: int, utts: int, frames: int):
     return g, L1, T, off, R
 
 
-def fill_inputs(cfg, rank, T, off, L1, costs_out, blank_out):
+def fill_inputs(cfg, rank, T, off, L1, costs_out, blank_out, ids=None):
+    """Cost table rows of each utterance (numpy -log, exactly frame_costs); ``ids`` are the
+    global utterance ids (strong scaling), ``cfg['distinct']`` tiles that many streams."""
     from paper_1808_00687_b200 import synth
     from paper_1808_00687_b200.posteriors import PosteriorMatrix, cost_table
+    distinct = cfg.get("distinct")
+    made = {}
     for i, (o, t) in enumerate(zip(off, T)):
-        rows = synth.random_posterior_rows(1000 * rank + i + 1, int(t), cfg["labels"],
+        uid = int(ids[i]) if ids is not None else 1000 * rank + i
+        seed = (uid % distinct if distinct else uid) + 1
+        if seed in made:
+            src = made[seed]
+            costs_out[o:o + t] = costs_out[src:src + t]
+            blank_out[o:o + t] = blank_out[src:src + t]
+            continue
+        rows = synth.random_posterior_rows(seed, int(t), cfg["labels"],
                                            blank_fraction=cfg["blank_fraction"])
         p = PosteriorMatrix(rows, 0, validate=False)
         cost_table(p, 1.0, out=costs_out[o:o + t])
         blank_out[o:o + t] = rows[:, 0]
+        made[seed] = o
 
 
 def cpu_sample(g, cfg, L1, n_threads: int, frames: int):
@@ -268,11 +286,16 @@ def main():
 
     utts = args.utts or cfg["utts"]
     frames = args.frames or cfg["frames"]
+    ids = None
+    if cfg.get("strong"):   # a fixed total of utterances, sharded by utterance over the ranks
+        from paper_1808_00687_b200.shard import shard_utterances
+        ids = shard_utterances([frames] * utts, world)[rank]
+        utts = len(ids)
     g, L1, T, off, R = make_workload(cfg, rank, utts, frames)
     # pinned host inputs (the e2e path copies from these every step)
     costs_h = torch.empty((R, L1), dtype=torch.float64, pin_memory=True)
     blank_h = torch.empty(R, dtype=torch.float64, pin_memory=True)
-    fill_inputs(cfg, rank, T, off, L1, costs_h.numpy(), blank_h.numpy())
+    fill_inputs(cfg, rank, T, off, L1, costs_h.numpy(), blank_h.numpy(), ids)
     dcfg = DecodeConfig(beam=cfg["beam"], max_active=cfg["max_active"], mode=cfg["mode"])
 
     block = args.block or 1024
@@ -335,6 +358,12 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     frames_step = int(T.sum())
+    # frames of all ranks per step (shards may differ by one utterance under strong scaling)
+    frames_all = frames_step * world
+    if dist is not None:
+        t = torch.tensor([frames_step], dtype=torch.int64, device=dev)
+        dist.all_reduce(t)
+        frames_all = int(t.item())
     res = np.frombuffer(res_d.cpu().numpy().tobytes(), dtype=N.UTT_RESULT_DTYPE)
     relax = int(res["a_fin"].sum() + res["e_eps"].sum())
     nbytes = algorithmic_bytes(res)
@@ -346,7 +375,7 @@ def main():
     e2e = None
     lat_stats = None
     if not (args.no_e2e or args.profile):
-        from paper_1808_00687_b200.lattice import LatticeError, prune_lattice
+        from paper_1808_00687_b200.lattice import LatticeError, prune_lattices
         costs_np, blank_np = costs_h.numpy(), blank_h.numpy()
 
         def e2e_step():
@@ -357,15 +386,14 @@ def main():
                 lats = dec.fetch_lattices(dec.graph.wfst)
                 st = {"lattices": len(lats), "nodes": 0, "arcs": 0, "pruned_nodes": 0,
                       "pruned_arcs": 0, "prune_errors": 0}
-                for lat in lats:
+                for lat, p in zip(lats, prune_lattices(lats, cfg["lattice_beam"])):
                     st["nodes"] += lat.num_nodes
                     st["arcs"] += lat.num_arcs
-                    try:
-                        p = prune_lattice(lat, cfg["lattice_beam"])
+                    if isinstance(p, LatticeError):
+                        st["prune_errors"] += 1
+                    else:
                         st["pruned_nodes"] += p.num_nodes
                         st["pruned_arcs"] += p.num_arcs
-                    except LatticeError:
-                        st["prune_errors"] += 1
             return o, st
 
         e2e_step()  # warm
@@ -388,7 +416,7 @@ def main():
         d2h = out.results.nbytes + out.olabels.nbytes + out.ilabels.nbytes
         if lat_stats:   # trimmed lattice pools: node 8 B, arc 16 + 8 B, meta 48 B / utt
             d2h += 8 * lat_stats["nodes"] + 24 * lat_stats["arcs"] + 48 * utts
-        e2e = {"value": frames_step * world * args.steps / (e_ms / 1e3), "unit": "frames/s",
+        e2e = {"value": frames_all * args.steps / (e_ms / 1e3), "unit": "frames/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": e_ms / args.steps,
                "input_path": ("pinned host cost table read zero-copy by the kernel (one staged "
@@ -405,7 +433,7 @@ def main():
                          f"thread) of the same workload, oracle/ C port of decoder.py"}
 
     if rank == 0:
-        value = frames_step * world * args.steps / (total_ms / 1e3)
+        value = frames_all * args.steps / (total_ms / 1e3)
         traffic = None
         tfile = os.path.join(ROOT, "profiles", "decode_traffic.json")
         if os.path.exists(tfile):
@@ -417,7 +445,8 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if cfg.get("strong") else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded random graph + posteriors, reference fixture semantics)",
             "config": {"workload": cfg["name"], "utts_per_gpu": utts, "frames_per_utt": frames,
                        "graph": {"states": g.num_states, "arcs": g.num_arcs,
@@ -436,7 +465,7 @@ def main():
             "lattice": lat_stats,
             "e2e": e2e,
             "clocks": clocks,
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": args.steps,  # one persistent decode kernel per step (backtrace in-kernel)
             "counters_per_step": {k: int(res[k].sum()) for k in
                                   ("n_tok", "a_emit", "a_fin", "e_eps", "n_cand", "n_surv", "n_rec")},
             "phase_share": dict(zip(["stage_row", "expand", "eps_closure", "gather", "select",

@@ -80,7 +80,7 @@ typedef struct {
     int32_t n_olabels;
     int32_t n_ilabels;
     int32_t status;          /* WB_OK or WB_ERR_CAPACITY */
-    int64_t best_trace;      /* backpointer-arena index of the winning token */
+    int64_t best_trace;      /* lane-arena index of the winning token's record */
     /* counters for the roofline: summed over the utterance's steps */
     int64_t n_tok;           /* live tokens expanded */
     int64_t a_emit;          /* emitting arcs scanned */
@@ -101,7 +101,7 @@ typedef struct {
 typedef struct {
     int32_t max_utts_in_flight;  /* concurrent utterances = persistent CTAs */
     int32_t cand_capacity;       /* per-step candidate capacity per utterance */
-    int64_t arena_capacity;      /* backpointer records per wb_decode call */
+    int64_t arena_capacity;      /* backpointer records per utterance lane (reused per utterance) */
     int32_t max_frames;          /* longest utterance a call may contain */
     int32_t block_threads;       /* 256, 512 or 1024 */
     int64_t lattice_capacity;    /* raw lattice nodes (and arcs) per utterance lane */

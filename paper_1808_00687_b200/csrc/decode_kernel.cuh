@@ -71,9 +71,9 @@ struct WorkDev {
     int4 *tok_info;       // [slots][2][cap] {state, trace, emit_lo, emit_hi}
     double *tok_cost;     // [slots][2][cap]
     int *frames;          // [slots][T_cap]
-    u64 *arena;           // [arena_cap] backpointer records (arcp1 | prev << 32)
+    u64 *arena;           // [slots][arena_cap] backpointer records (arcp1 | prev << 32), reused
+                          // per utterance (the lane backtraces before taking the next one)
     u64 arena_cap;
-    u64 *arena_ctr;
     u32 *utt_ctr;
     long long S;
     int cap, T_cap, smem_cands, row_in_smem;
@@ -106,6 +106,8 @@ struct BatchDev {
     const int *T;
     const double *blank;
     int L1, n;
+    int *olab, *ilab;  // [n][lab_cap] best-path labels
+    int lab_cap;
 };
 
 struct CfgDev {
@@ -124,6 +126,7 @@ struct Smem {
     u64 thr_key;
     u32 thr_state;
     u64 arena_base;
+    u64 arena_used;    // records of the lane's current utterance
     long long pc[8];   // phase cycle counters (thread 0)
     long long t_mark;  // last phase boundary (thread 0)
     union {
@@ -250,6 +253,7 @@ struct Lane {
         return ws.tok_cost + 2 * co() + (size_t)k * ws.cap;
     }
     __device__ __forceinline__ int *frames() const { return ws.frames + (size_t)blockIdx.x * ws.T_cap; }
+    __device__ __forceinline__ u64 *arena() const { return ws.arena + (size_t)blockIdx.x * ws.arena_cap; }
 };
 
 
@@ -369,7 +373,7 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
                 act[u] = j < total;
                 int arc = lo_k + j - ex_k;
                 want[u].arcp1 = (u32)arc + 1u;
-                if (act[u]) rec[u] = __ldg(&g.arcs[2 * arc]);
+                if (act[u]) rec[u] = ld_arc(&g.arcs[2 * arc]);
                 want[u].key = __double_as_longlong(cst);  // carry the token cost
             }
 #pragma unroll
@@ -469,7 +473,7 @@ __noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev 
                 int a = lo_k + j - ex_k;
                 int4 rec = make_int4(0, 0, 0, 0);
                 if (act) {
-                    rec = __ldg(&g.arcs[2 * a]);
+                    rec = ld_arc(&g.arcs[2 * a]);
                     if ((u32)rec.x == u_k) act = false;  // a positive self-loop never improves its state
                 }
                 bool first = false, dec = false;
@@ -746,9 +750,10 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
         if (l == 31) {
             sh.wa[NW] = ia;
             sh.wb[NW] = ib;
-            u64 base = atomicAdd(ws.arena_ctr, (u64)ia);
+            u64 base = sh.arena_used;
             if (base + (u64)ia > ws.arena_cap || base + (u64)ia >= (u64)EPS_BIT) sh.overflow = 2;
             sh.arena_base = base;
+            sh.arena_used = base + (u64)ia;
             sh.n_pend = 0;
         }
     }
@@ -814,7 +819,7 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
                         pend[qq] = (u32)i;  // epsilon winner: needs its source's record index
                     } else {
                         u32 prev = a[q] == 0u ? ROOT_PREV : p[q];
-                        ws.arena[rec[q]] = (u64)a[q] | ((u64)prev << 32);
+                        c.arena()[rec[q]] = (u64)a[q] | ((u64)prev << 32);
                     }
                 }
             }
@@ -825,7 +830,7 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
     for (int q = threadIdx.x; q < n_pend; q += BLOCK) {
         int i = (int)pend[q];
         u32 a = c.cand_arc()[i], p = c.cand_pay()[i];
-        ws.arena[vca[i]] = (u64)a | ((u64)vca[p & ~EPS_BIT] << 32);
+        c.arena()[vca[i]] = (u64)a | ((u64)vca[p & ~EPS_BIT] << 32);
     }
     __syncthreads();
     tick<BLOCK>(6);
@@ -1250,6 +1255,30 @@ __noinline__ __device__ void trim_lattice(int u, int K, int reached, int final_s
     __syncthreads();
 }
 
+// Backtrace (decoder.py:276-291): the lane's thread 0 walks its arena from the winner before
+// the lane takes its next utterance; labels are written back to front so they land in path
+// order without a second walk.
+__device__ __noinline__ void backtrace(const GraphDev &g, const u64 *arena, long long best,
+                                       int *ob, int *ib, int cap, int *n_o, int *n_i) {
+    int po = cap, pi = cap, no = 0, ni = 0;
+    u32 idx = best < 0 ? ROOT_PREV : (u32)best;
+    while (idx != ROOT_PREV) {
+        const u64 rec = __ldcg(&arena[idx]);
+        const u32 a1 = (u32)rec;
+        idx = (u32)(rec >> 32);
+        if (a1 == 0u) continue;
+        const int a = (int)a1 - 1;
+        const int il = __ldg(&g.arcs[2 * a].y);
+        const int ol = __ldg(&g.arcs[2 * a + 1].w);
+        if (ol != 0) { ++no; if (po > 0) ob[--po] = ol; }
+        if (il != 0) { ++ni; if (pi > 0) ib[--pi] = il; }
+    }
+    if (no <= cap) for (int i = 0; i < no; ++i) ob[i] = ob[po + i];
+    if (ni <= cap) for (int i = 0; i < ni; ++i) ib[i] = ib[pi + i];
+    *n_o = no;
+    *n_i = ni;
+}
+
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK, 1)
 decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDev ws,
@@ -1268,7 +1297,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
         const int u = sh.utt;
         if (u >= b.n) break;
         if (threadIdx.x < 8) sh.pc[threadIdx.x] = 0;
-        if (threadIdx.x == 0) sh.t_mark = clock64();
+        if (threadIdx.x == 0) { sh.t_mark = clock64(); sh.arena_used = 0; }
         const int T = b.T[u];
         const long long row0 = b.row_off[u];
         int status = WB_OK;
@@ -1427,8 +1456,12 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             r.died_at_step = died_at;
             r.final_state = best_t >= 0 ? tinfo[best_t].x : -1;
             r.final_step = died_at < 0 ? steps_run : died_at;
-            r.status = status;
             r.best_trace = best_t >= 0 ? (long long)(u32)tinfo[best_t].y : -1;
+            backtrace(g, c.arena(), r.best_trace, b.olab + (size_t)u * b.lab_cap,
+                      b.ilab + (size_t)u * b.lab_cap, b.lab_cap, &r.n_olabels, &r.n_ilabels);
+            if ((r.n_olabels > b.lab_cap || r.n_ilabels > b.lab_cap) && status == WB_OK)
+                status = WB_ERR_CAPACITY;
+            r.status = status;
             r.n_tok = n_tok;
             r.a_emit = t_emit;
             r.a_fin = t_fin;
@@ -1442,34 +1475,6 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
         __syncthreads();
     }
     if (threadIdx.x == 0) ws.tag_ctr[slot_id] = tag;
-}
-
-// Backtrace (decoder.py:276-291): one thread per utterance walks the arena from the winner;
-// labels are written back-to-front so they land in path order without a second walk.
-__global__ void backtrace_kernel(GraphDev g, const u64 *arena, wb_utt_result *res, int n,
-                                 int *olab, int *ilab, int cap) {
-    int u = blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= n) return;
-    wb_utt_result r = res[u];
-    int *ob = olab + (size_t)u * cap, *ib = ilab + (size_t)u * cap;
-    int po = cap, pi = cap, no = 0, ni = 0;
-    u32 idx = r.best_trace < 0 ? ROOT_PREV : (u32)r.best_trace;
-    while (idx != ROOT_PREV) {
-        u64 rec = arena[idx];
-        u32 a1 = (u32)rec;
-        idx = (u32)(rec >> 32);
-        if (a1 == 0u) continue;
-        int a = (int)a1 - 1;
-        int il = __ldg(&g.arcs[2 * a].y);
-        int ol = __ldg(&g.arcs[2 * a + 1].w);
-        if (ol != 0) { ++no; if (po > 0) ob[--po] = ol; }
-        if (il != 0) { ++ni; if (pi > 0) ib[--pi] = il; }
-    }
-    if (no <= cap) for (int i = 0; i < no; ++i) ob[i] = ob[po + i];
-    if (ni <= cap) for (int i = 0; i < ni; ++i) ib[i] = ib[pi + i];
-    res[u].n_olabels = no;
-    res[u].n_ilabels = ni;
-    if ((no > cap || ni > cap) && r.status == WB_OK) res[u].status = WB_ERR_CAPACITY;
 }
 
 }  // namespace wb

@@ -112,6 +112,22 @@ __device__ __forceinline__ bool relax_slot(Slot *p, u64 key, u32 arcp1, u32 pay,
     return false;
 }
 
+// Arc-record load.  With WB_ARC_EVICT_FIRST the line is marked evict-first in L2 (a random
+// graph's arc records have little reuse; the step's candidate data should keep the L2).
+__device__ __forceinline__ int4 ld_arc(const int4 *p) {
+#ifdef WB_ARC_EVICT_FIRST
+    int4 r;
+    u64 pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("ld.global.nc.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p), "l"(pol));
+    return r;
+#else
+    return __ldg(p);
+#endif
+}
+
 __device__ __forceinline__ u32 lanemask_lt() {
     u32 m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

@@ -203,8 +203,8 @@ static int alloc_frames(wb_decoder_s *d, int T_cap) {
 static int alloc_arena(wb_decoder_s *d, u64 cap) {
     cudaFree(d->arena);
     d->arena = nullptr;
-    d->arena_cap = std::min<u64>(std::max<u64>(cap, 1024), (u64)EPS_BIT - 1);
-    CUDA_TRY(cudaMalloc(&d->arena, sizeof(u64) * d->arena_cap));
+    d->arena_cap = std::min<u64>(std::max<u64>(cap, 1024), (u64)EPS_BIT - 1);  // per lane
+    CUDA_TRY(cudaMalloc(&d->arena, sizeof(u64) * d->arena_cap * (size_t)d->slots));
     return WB_OK;
 }
 
@@ -361,7 +361,7 @@ int wb_decoder_create(wb_graph_t g, const wb_decoder_opts *o, wb_decoder_t *out)
     d->lat_out_want = opts.lattice_out_capacity;
     int rc = alloc_frames(d, opts.max_frames > 0 ? opts.max_frames : 2048);
     if (rc == WB_OK)
-        rc = alloc_arena(d, opts.arena_capacity > 0 ? (u64)opts.arena_capacity : (u64)1 << 24);
+        rc = alloc_arena(d, opts.arena_capacity > 0 ? (u64)opts.arena_capacity : (u64)1 << 22);
     if (rc != WB_OK) {
         free_decoder(d);
         delete d;
@@ -381,7 +381,7 @@ int wb_decoder_destroy(wb_decoder_t d) {
 
 int wb_decoder_device_bytes(wb_decoder_t d, int64_t *bytes) {
     *bytes = (int64_t)(d->bytes + sizeof(int) * (size_t)d->slots * d->T_cap +
-                       sizeof(u64) * d->arena_cap + d->lat_bytes +
+                       sizeof(u64) * d->arena_cap * (size_t)d->slots + d->lat_bytes +
                        sizeof(int2) * d->o_node_n + (sizeof(uint4) + sizeof(double)) * d->o_arc_n +
                        (sizeof(u32) + sizeof(double)) * d->o_fin_n);
     return WB_OK;
@@ -475,7 +475,7 @@ int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row
     wd.cand_pay = d->cand_pay; wd.cand_key = d->cand_key; wd.cand_ca = d->cand_ca;
     wd.front = d->front; wd.tok_info = d->tok_info; wd.tok_cost = d->tok_cost;
     wd.frames = d->frames;
-    wd.arena = d->arena; wd.arena_cap = d->arena_cap; wd.arena_ctr = d->counters;
+    wd.arena = d->arena; wd.arena_cap = d->arena_cap;
     wd.utt_ctr = reinterpret_cast<u32 *>(d->counters + 1);
     wd.S = g->S; wd.cap = d->cap; wd.T_cap = d->T_cap;
     if (cfg->lattice) {
@@ -506,7 +506,7 @@ int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row
         d->lat_n = n;
         d->lat_stream = st;
     }
-    BatchDev bd{dc, doff, dT, db, num_cols, n};
+    BatchDev bd{dc, doff, dT, db, num_cols, n, dol, dil, lcap};
     CfgDev cd{cfg->beam, cfg->blank_threshold, cfg->max_active, cfg->mode, cfg->lattice};
     // 1024 threads per CTA, one persistent CTA (utterance lane) per SM
     int block = d->block ? d->block : 1024;
@@ -535,8 +535,6 @@ int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row
     if (e != cudaSuccess)
         return set_err(WB_ERR_CUDA, std::string("decode launch: ") + cudaGetErrorString(e));
     CUDA_TRY(cudaEventRecord(d->ev1, st));
-    backtrace_kernel<<<(n + 127) / 128, 128, 0, st>>>(gd, d->arena, dres, n, dol, dil, lcap);
-    CUDA_TRY(cudaGetLastError());
     if (host) {
         CUDA_TRY(cudaMemcpyAsync(results, dres, sizeof(wb_utt_result) * n, cudaMemcpyDeviceToHost, st));
         if (label_cap > 0) {

@@ -194,7 +194,7 @@ class BatchDecoder:
             self.opts["lattice_out_capacity"] = max(2 * out, lattice_out_need * 5 // 4)
         cap = self.opts["cand_capacity"] or min(S, 1 << 18)
         self.opts["cand_capacity"] = min(S, cap * 2)
-        arena = self.opts["arena_capacity"] or (1 << 24)
+        arena = self.opts["arena_capacity"] or (1 << 22)
         self.opts["arena_capacity"] = min(2**31 - 2, max(arena * 2, arena_need or 0))
         self._create()
 
@@ -218,10 +218,13 @@ class BatchDecoder:
                 lattice: bool = False):
         """Size the backpointer arena / frame list (and the raw-lattice pools of one utterance
         lane when recording lattices) for a batch before launching it."""
-        per_step = min(self.opts["cand_capacity"] or (1 << 18), 2 * max_active if max_active else 8192)
-        need = int(min(2**31 - 2, (n_frames_total + 64) * max(per_step, 64)))
+        # the arena is per utterance lane and reused per utterance: one utterance's records
+        S = self.graph.wfst.num_states
+        per_step = min(self.opts["cand_capacity"] or (1 << 18), S,
+                       2 * max_active if max_active else 8192)
+        need = int(min(2**31 - 2, (max_frames + 2) * max(per_step, 64)))
         changed = False
-        if need > (self.opts["arena_capacity"] or (1 << 24)):
+        if need > (self.opts["arena_capacity"] or (1 << 22)):
             self.opts["arena_capacity"] = need
             changed = True
         if max_frames > (self.opts["max_frames"] or 2048):

@@ -294,6 +294,25 @@ def prune_lattice(lat: Lattice, lattice_beam: float) -> Lattice:
         N.load().wb_lattice_arrays_free(C.byref(out))
 
 
+def prune_lattices(lats, lattice_beam: float, max_workers: int | None = None) -> list:
+    """``prune_lattice`` over many lattices on host threads (the C++ pass runs without the
+    GIL).  A lattice whose split exceeds the cap yields its ``LatticeError`` in its slot."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one(lat):
+        try:
+            return prune_lattice(lat, lattice_beam)
+        except LatticeError as exc:
+            return exc
+    lats = list(lats)
+    workers = max_workers or min(len(lats), len(os.sched_getaffinity(0))) or 1
+    if workers <= 1:
+        return [one(x) for x in lats]
+    with ThreadPoolExecutor(workers) as ex:
+        return list(ex.map(one, lats))
+
+
 def lattice_best_path(lat: Lattice) -> tuple[float, tuple[int, ...], tuple[int, ...]]:
     """Minimum-cost start-to-final path (cost, olabels, ilabels), ties as the decoder
     resolves them (lattice.py:504-559)."""
@@ -389,5 +408,5 @@ def load_lattice(path: str) -> Lattice:
 
 __all__ = ["COST_EPS", "EMPTY_LATTICE", "Lattice", "LatticeArc", "LatticeError", "LatticeNode",
            "LatticeRecorder", "build_lattice", "canonical_from_device", "format_lattice_text",
-           "lattice_best_path", "load_lattice", "parse_lattice_text", "prune_lattice",
+           "lattice_best_path", "load_lattice", "parse_lattice_text", "prune_lattice", "prune_lattices",
            "save_lattice"]

@@ -97,3 +97,17 @@ def test_reference_shaped_equality():
     ref_like.start_id, ref_like.finals = 0, dict(lat.finals)
     assert lat == ref_like
     assert np.array_equal(L.Lattice.from_reference(ref_like).arc_tie, lat.arc_tie)
+
+
+def test_prune_lattices_threaded_matches_serial():
+    beams = GC.prune_beams()
+    lats = [c.lattice_object() for c in _lattice_cases()[:60]]
+    for b in beams[:3]:
+        par = L.prune_lattices(lats, b, max_workers=4)
+        for lat, p in zip(lats, par):
+            try:
+                want = _key(L.prune_lattice(lat, b))
+            except L.LatticeError:
+                want = "error"
+            got = "error" if isinstance(p, L.LatticeError) else _key(p)
+            assert got == want
