@@ -254,11 +254,15 @@ def main():
     ap.add_argument("--utts", type=int, default=0, help="utterances per GPU (default: config)")
     ap.add_argument("--frames", type=int, default=0, help="frames per utterance (default: config)")
     ap.add_argument("--block", type=int, default=0, help="threads per CTA (0 = library default)")
+    ap.add_argument("--max-active", type=int, default=0, help="override the config's max-active (tuning)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu)")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.max_active:
+        cfg["max_active"] = args.max_active
+        cfg["name"] += f" [max-active overridden to {args.max_active}]"
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -79,7 +79,11 @@ struct WorkDev {
     int cap, T_cap, smem_cands, row_in_smem;
     // ---- lattice recording (LatticeRecorder / build_lattice, lattice.py:96-249)
     int *tok_eps;         // [slots][2][cap] epsilon-range start of each token's state
-    u32 *stag, *snode;    // [slots][S] survivor tag of the current node step / node index
+    u32 *sbits;           // [slots][ceil(S/32)] survivor bitmap of the current node step (L2-resident)
+    u32 *snode;           // [slots][S] node index of a survivor state
+    int4 *rlog;           // [slots][rlog_cap] this step's finite emitting relaxations
+                          // {token, arc, dst, ilabel} (logged by expand, filtered by record)
+    long long rlog_cap;
     u32 *ln_state;        // [slots][lat_cap] raw lattice nodes (state), step-major
     unsigned char *ln_flag;  // [slots][lat_cap] trim flags (forward / backward reach)
     u32 *ln_out;          // [slots][lat_cap] output index of a kept node
@@ -123,6 +127,7 @@ struct Smem {
     long long rl[NW];
     int n_cand, n_front, overflow, utt, tag_round, ng, thr_bucket, thr_below, n_pend;
     int flag, lat_bad;  // lattice sweeps: change flag / output-pool overflow
+    int n_log;          // relaxations logged this step (lattice mode)
     u64 thr_key;
     u32 thr_state;
     u64 arena_base;
@@ -362,10 +367,12 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
             int4 rec[U];
             Slot want[U];
             bool act[U];
+            int tk[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 int j = j0 + u * 32 + l;
                 int k = warp_owner(excl, j);
+                tk[u] = (ch << 5) + k;
                 int lo_k = __shfl_sync(FULL, ti.z, k);
                 int ex_k = __shfl_sync(FULL, excl, k);
                 double cst = __shfl_sync(FULL, tc, k);
@@ -387,6 +394,20 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
                 double wgt = __hiloint2double(rec[u].w, rec[u].z);
                 double cst = __longlong_as_double((long long)want[u].key);
                 want[u].key = cost_key(__dadd_rn(__dadd_rn(cst, wgt), ac));
+            }
+            if (ws.rlog) {  // lattice mode: log the finite relaxations for record_lattice_step
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const u32 m = __ballot_sync(FULL, act[u]);
+                    if (!m) continue;
+                    int base = 0;
+                    if (l == __ffs(m) - 1) base = atomicAdd(&SH<BLOCK>().n_log, __popc(m));
+                    base = __shfl_sync(FULL, base, __ffs(m) - 1);
+                    const long long e = base + __popc(m & lanemask_lt());
+                    if (act[u] && e < ws.rlog_cap)
+                        ws.rlog[(size_t)blockIdx.x * ws.rlog_cap + e] =
+                            make_int4(tk[u], (int)want[u].arcp1 - 1, rec[u].x, rec[u].y);
+                }
             }
             Slot prev[U];
 #pragma unroll
@@ -901,6 +922,10 @@ __device__ int block_argmin_tok(u64 key, u32 st, int idx) {
 }
 
 // ------------------------------------------------------------------ lattice recording
+__device__ __forceinline__ bool surv_bit(const u32 *bits, u32 s) {
+    return (__ldcg(&bits[s >> 5]) >> (s & 31)) & 1u;  // L2-coherent: set by this step's atomics
+}
+
 // Raw lattice of node step k (lattice.py:148-170): nodes = survivors(k) (plus the start at
 // step 0, decoder.py:246-248); emitting arcs = relaxations from live(k-1) with finite
 // acoustic cost into survivors(k); epsilon arcs = non-self-loop epsilon arcs between
@@ -915,6 +940,7 @@ __noinline__ __device__ int record_lattice_step(int k, int nxt, int n_surv, int 
     constexpr int NW = BLOCK / 32;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     const size_t so = c.so(), lo = (size_t)blockIdx.x * (size_t)ws.lat_cap;
+    const size_t bo = (size_t)blockIdx.x * (size_t)((ws.S + 31) >> 5);
     int4 *lst = ws.lstep + (size_t)blockIdx.x * (ws.T_cap + 2);
     int *lse = ws.lstep_eps + (size_t)blockIdx.x * (ws.T_cap + 2);
     const int node_base = k == 0 ? 0 : lst[k - 1].x + lst[k - 1].z;
@@ -935,7 +961,7 @@ __noinline__ __device__ int record_lattice_step(int k, int nxt, int n_surv, int 
     if ((long long)node_base + n_nodes > ws.lat_cap) return WB_ERR_CAPACITY;
     for (int j = threadIdx.x; j < n_nodes; j += BLOCK) {
         const u32 st = j < n_surv ? (u32)tn[j].x : (u32)g.start;
-        ws.stag[so + st] = tagL;
+        atomicOr(&ws.sbits[bo + (st >> 5)], 1u << (st & 31));
         ws.snode[so + st] = (u32)(node_base + j);
         ws.ln_state[lo + node_base + j] = st;
     }
@@ -949,45 +975,43 @@ __noinline__ __device__ int record_lattice_step(int k, int nxt, int n_surv, int 
     }
     __syncthreads();
     const long long room = ws.lat_cap - arc_base;
-    // emitting arcs from live(k-1)
+    // emitting arcs from live(k-1): the finite relaxations expand logged, into survivors
     if (k > 0) {
-        const int4 *tp = c.tok_info(prv);
-        const int nchunks = (n_prev + 31) >> 5;
-        for (int ch = w; ch < nchunks; ch += NW) {
-            const int t = (ch << 5) + l;
-            int4 ti = make_int4(0, 0, 0, 0);
-            if (t < n_prev) ti = tp[t];
-            const int deg = t < n_prev ? ti.w - ti.z : 0;
-            const int incl = warp_incl_scan(deg);
-            const int tot = __shfl_sync(FULL, incl, 31);
-            const int excl = incl - deg;
-            for (int j0 = 0; j0 < tot; j0 += 32) {
-                const int j = j0 + l;
-                const int kk = warp_owner(excl, j);
-                const int lo_k = __shfl_sync(FULL, ti.z, kk);
-                const int ex_k = __shfl_sync(FULL, excl, kk);
-                const int a = lo_k + j - ex_k;
-                bool rec = false;
-                int4 r = make_int4(0, 0, 0, 0);
-                double ac = 0.0;
-                if (j < tot) {
-                    r = __ldg(&g.arcs[2 * a]);
-                    ac = row[r.y];
-                    rec = ac != INFINITY && ws.stag[so + r.x] == tagL;
-                }
-                const u32 m = __ballot_sync(FULL, rec);
+        const int n_log = sh.n_log;
+        if ((long long)n_log > ws.rlog_cap) status = WB_ERR_CAPACITY;
+        const int4 *lg = ws.rlog + (size_t)blockIdx.x * ws.rlog_cap;
+        const int nl = (int)min((long long)n_log, ws.rlog_cap);
+        constexpr int G = 4;  // log entries per thread with their loads in flight
+        for (int i0 = 0; i0 < nl; i0 += BLOCK * G) {
+            int4 r[G];
+            bool rec[G];
+            u32 dn[G];
+#pragma unroll
+            for (int q = 0; q < G; ++q) {
+                const int i = i0 + q * BLOCK + (int)threadIdx.x;
+                r[q] = i < nl ? lg[i] : make_int4(0, 0, -1, 0);
+            }
+#pragma unroll
+            for (int q = 0; q < G; ++q)
+                rec[q] = r[q].z >= 0 && surv_bit(ws.sbits + bo, (u32)r[q].z);
+#pragma unroll
+            for (int q = 0; q < G; ++q)
+                dn[q] = rec[q] ? __ldcg(&ws.snode[so + r[q].z]) : 0u;
+#pragma unroll
+            for (int q = 0; q < G; ++q) {
+                const u32 m = __ballot_sync(FULL, rec[q]);
                 if (!m) continue;
                 int base = 0;
                 if (l == __ffs(m) - 1) base = atomicAdd(&sh.n_pend, __popc(m));
                 base = __shfl_sync(FULL, base, __ffs(m) - 1);
-                if (rec) {
+                if (rec[q]) {
                     const long long e = base + __popc(m & lanemask_lt());
                     if (e < room) {
                         const size_t ge = lo + arc_base + e;
-                        ws.la_src[ge] = (u32)(prev_base + kk + (ch << 5));
-                        ws.la_dst[ge] = ws.snode[so + r.x];
-                        ws.la_arc[ge] = (u32)a;
-                        ws.la_ac[ge] = ac;
+                        ws.la_src[ge] = (u32)(prev_base + r[q].x);
+                        ws.la_dst[ge] = dn[q];
+                        ws.la_arc[ge] = (u32)r[q].y;
+                        ws.la_ac[ge] = row[r[q].w];
                     }
                 }
             }
@@ -1025,7 +1049,7 @@ __noinline__ __device__ int record_lattice_step(int k, int nxt, int n_surv, int 
                 int4 r = make_int4(0, 0, 0, 0);
                 if (q < tot) {
                     r = __ldg(&g.arcs[2 * a]);
-                    rec = (u32)r.x != st_k && ws.stag[so + r.x] == tagL;
+                    rec = (u32)r.x != st_k && surv_bit(ws.sbits + bo, (u32)r.x);
                 }
                 const u32 m = __ballot_sync(FULL, rec);
                 if (!m) continue;
@@ -1037,7 +1061,7 @@ __noinline__ __device__ int record_lattice_step(int k, int nxt, int n_surv, int 
                     if (e < room) {
                         const size_t ge = lo + arc_base + e;
                         ws.la_src[ge] = (u32)(node_base + kk + (ch << 5));
-                        ws.la_dst[ge] = ws.snode[so + r.x];
+                        ws.la_dst[ge] = __ldcg(&ws.snode[so + r.x]);
                         ws.la_arc[ge] = (u32)a;
                         ws.la_ac[ge] = 0.0;
                     }
@@ -1048,6 +1072,8 @@ __noinline__ __device__ int record_lattice_step(int k, int nxt, int n_surv, int 
     __syncthreads();
     const int n_all = sh.n_pend;
     if (n_all > room) status = WB_ERR_CAPACITY;
+    for (int j = threadIdx.x; j < n_nodes; j += BLOCK)  // every set bit is one of these nodes
+        ws.sbits[bo + (ws.ln_state[lo + node_base + j] >> 5)] = 0u;
     if (threadIdx.x == 0) {
         lst[k] = make_int4(node_base, arc_base, n_nodes, n_emit);
         lse[k] = n_all - n_emit;
@@ -1359,7 +1385,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
                 for (int q = threadIdx.x; q < b.L1; q += BLOCK) srow[q] = __ldg(&grow[q]);
                 row = srow;
             }
-            if (threadIdx.x == 0) { sh.n_cand = 0; sh.n_front = 0; sh.overflow = 0; }
+            if (threadIdx.x == 0) { sh.n_cand = 0; sh.n_front = 0; sh.overflow = 0; sh.n_log = 0; }
             __syncthreads();
             tick<BLOCK>(0);
             expanded += n_live;

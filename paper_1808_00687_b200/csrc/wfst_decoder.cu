@@ -72,10 +72,12 @@ struct wb_decoder_s {
     long long lat_cap = 0, lat_cap_want = 0, lat_out_want = 0;
     int lat_T = 0;
     int *tok_eps = nullptr;
-    u32 *stag = nullptr, *snode = nullptr, *ln_state = nullptr, *ln_out = nullptr;
+    u32 *sbits = nullptr, *snode = nullptr, *ln_state = nullptr, *ln_out = nullptr;
     unsigned char *ln_flag = nullptr;
     u32 *la_src = nullptr, *la_dst = nullptr, *la_arc = nullptr;
     double *la_ac = nullptr;
+    int4 *rlog = nullptr;
+    long long rlog_cap = 0;
     int4 *lstep = nullptr;
     int *lstep_eps = nullptr, *lstep_start = nullptr;
     int2 *o_node = nullptr;
@@ -177,10 +179,10 @@ static void free_decoder(wb_decoder_s *d) {
     void *ptrs[] = {d->slot, d->cand_of, d->qtag, d->tag_ctr, d->cand_state, d->cand_rng,
                     d->cand_arc, d->cand_pay, d->cand_key, d->cand_ca, d->front, d->tok_info,
                     d->tok_cost, d->frames, d->arena, d->counters, d->h_costs, d->h_blank,
-                    d->h_off, d->h_T, d->h_res, d->h_lab, d->tok_eps, d->stag, d->snode,
+                    d->h_off, d->h_T, d->h_res, d->h_lab, d->tok_eps, d->sbits, d->snode,
                     d->ln_state, d->ln_out, d->ln_flag, d->la_src, d->la_dst, d->la_arc,
                     d->la_ac, d->lstep, d->lstep_eps, d->lstep_start, d->o_node, d->o_arc,
-                    d->o_ac, d->o_finw, d->o_fin, d->o_ctr, d->o_meta};
+                    d->o_ac, d->o_finw, d->o_fin, d->o_ctr, d->o_meta, d->rlog};
     for (void *p : ptrs) cudaFree(p);
     if (d->ev0) cudaEventDestroy(d->ev0);
     if (d->ev1) cudaEventDestroy(d->ev1);
@@ -211,11 +213,11 @@ static int alloc_arena(wb_decoder_s *d, u64 cap) {
 // Lattice workspace: per-lane raw node / arc pools (lat_cap each), per-step metadata and the
 // survivor tags; allocated on the first lattice decode so plain decoding pays nothing.
 static int alloc_lattice(wb_decoder_s *d) {
-    void *ptrs[] = {d->tok_eps, d->stag, d->snode, d->ln_state, d->ln_out, d->ln_flag,
+    void *ptrs[] = {d->tok_eps, d->sbits, d->snode, d->ln_state, d->ln_out, d->ln_flag,
                     d->la_src, d->la_dst, d->la_arc, d->la_ac, d->lstep, d->lstep_eps,
-                    d->lstep_start, d->o_ctr};
+                    d->lstep_start, d->o_ctr, d->rlog};
     for (void *p : ptrs) cudaFree(p);
-    d->tok_eps = nullptr; d->stag = d->snode = d->ln_state = d->ln_out = nullptr;
+    d->tok_eps = nullptr; d->sbits = d->ln_state = d->ln_out = nullptr; d->snode = nullptr; d->rlog = nullptr;
     d->ln_flag = nullptr; d->la_src = d->la_dst = d->la_arc = nullptr; d->la_ac = nullptr;
     d->lstep = nullptr; d->lstep_eps = d->lstep_start = nullptr; d->o_ctr = nullptr;
     d->lat_cap = 0;
@@ -227,8 +229,10 @@ static int alloc_lattice(wb_decoder_s *d) {
     cudaError_t e = cudaSuccess;
 #define DA(p, n) if (e == cudaSuccess) e = dalloc(&d->p, (n), acc)
     DA(tok_eps, slots * 2 * cap);
-    DA(stag, slots * S);
+    DA(sbits, slots * ((S + 31) / 32));
     DA(snode, slots * S);
+    d->rlog_cap = std::min<long long>((long long)L, 16ll * (long long)cap);
+    DA(rlog, slots * (size_t)d->rlog_cap);
     DA(ln_state, slots * L);
     DA(ln_out, slots * L);
     DA(ln_flag, slots * L);
@@ -241,7 +245,7 @@ static int alloc_lattice(wb_decoder_s *d) {
     DA(lstep_start, slots);
     DA(o_ctr, 4);
 #undef DA
-    if (e == cudaSuccess) e = cudaMemset(d->stag, 0, sizeof(u32) * slots * S);
+    if (e == cudaSuccess) e = cudaMemset(d->sbits, 0, sizeof(u32) * slots * ((S + 31) / 32));
     if (e != cudaSuccess)
         return set_err(e == cudaErrorMemoryAllocation ? WB_ERR_NOMEM : WB_ERR_CUDA,
                        std::string("lattice workspace: ") + cudaGetErrorString(e));
@@ -494,7 +498,7 @@ int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row
         if ((rc = grow(&d->o_finw, have, out))) return rc;
         if ((rc = grow(&d->o_meta, d->o_meta_n, (size_t)n * 6))) return rc;
         CUDA_TRY(cudaMemsetAsync(d->o_ctr, 0, sizeof(unsigned long long) * 4, st));
-        wd.tok_eps = d->tok_eps; wd.stag = d->stag; wd.snode = d->snode;
+        wd.tok_eps = d->tok_eps; wd.sbits = d->sbits; wd.snode = d->snode; wd.rlog = d->rlog; wd.rlog_cap = d->rlog_cap;
         wd.ln_state = d->ln_state; wd.ln_flag = d->ln_flag; wd.ln_out = d->ln_out;
         wd.la_src = d->la_src; wd.la_dst = d->la_dst; wd.la_arc = d->la_arc; wd.la_ac = d->la_ac;
         wd.lat_cap = d->lat_cap; wd.lstep = d->lstep; wd.lstep_eps = d->lstep_eps;
