@@ -183,6 +183,19 @@ typedef struct {
     double *final_w;                     /* [n_finals] */
 } wb_lattice_arrays;
 
+/* Canonical order of fetched device lattices (_assemble's numbering, lattice.py:215-230):
+ * inputs are wb_lattice_fetch's pools + meta and the graph's per-arc ilabel / olabel / weight;
+ * outputs are utterance-ordered flat arrays (out_meta rows like meta, offsets into them), node
+ * 0 of each lattice its start node, tie = WFST arc index.  n_threads host threads. */
+int wb_lattice_canonical(int32_t n_utts, const int64_t *meta, const int32_t *nodes,
+                         const uint32_t *arcs, const double *arc_ac, const uint32_t *finals,
+                         const double *final_w, int32_t start_state, const int32_t *g_ilabel,
+                         const int32_t *g_olabel, const double *g_weight, int32_t n_threads,
+                         int64_t *out_meta, int32_t *node_state, int32_t *node_step,
+                         int64_t *arc_from, int64_t *arc_to, int32_t *arc_il, int32_t *arc_ol,
+                         double *arc_g, double *arc_a, int64_t *arc_tie, int64_t *final_node,
+                         double *final_wo);
+
 /* _topo_order's check (lattice.py:295-326): WB_ERR_LATTICE on an epsilon cycle among nodes. */
 int wb_lattice_check(const wb_lattice_arrays *lat);
 /* prune_lattice (lattice.py:359-501): exact forward-backward pruning to paths within `beam`

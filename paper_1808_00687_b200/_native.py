@@ -70,7 +70,8 @@ EXPORTED = ("wb_last_error", "wb_version", "wb_device_count", "wb_graph_create",
             "wb_graph_destroy", "wb_graph_device_bytes", "wb_decoder_create",
             "wb_decoder_destroy", "wb_decoder_device_bytes", "wb_decode", "wb_last_kernel_ms",
             "wb_lattice_totals", "wb_lattice_fetch", "wb_lattice_check", "wb_lattice_prune",
-            "wb_lattice_arrays_free", "wb_lattice_best_path", "wb_last_transfer")
+            "wb_lattice_arrays_free", "wb_lattice_best_path", "wb_last_transfer",
+            "wb_lattice_canonical")
 
 
 def load():
@@ -104,6 +105,8 @@ def load():
     L.wb_lattice_prune.argtypes = [LP, C.c_double, LP]
     L.wb_lattice_arrays_free.argtypes = [LP]
     L.wb_lattice_arrays_free.restype = None
+    L.wb_lattice_canonical.argtypes = [C.c_int32] + [C.c_void_p] * 6 + [C.c_int32] + \
+        [C.c_void_p] * 3 + [C.c_int32] + [C.c_void_p] * 12
     L.wb_lattice_best_path.argtypes = [LP, C.POINTER(C.c_double), C.c_void_p,
                                        C.POINTER(C.c_int32), C.c_void_p, C.POINTER(C.c_int32),
                                        C.c_int32]

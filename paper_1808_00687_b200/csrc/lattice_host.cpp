@@ -14,7 +14,9 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <unordered_set>
 #include <vector>
@@ -441,6 +443,80 @@ int prune(const Lat &L, double beam, Lat &out) {
 }  // namespace
 
 extern "C" {
+
+int wb_lattice_canonical(int32_t n_utts, const int64_t *meta, const int32_t *nodes,
+                         const uint32_t *arcs, const double *arc_ac, const uint32_t *finals,
+                         const double *final_w, int32_t start_state, const int32_t *g_ilabel,
+                         const int32_t *g_olabel, const double *g_weight, int32_t n_threads,
+                         int64_t *out_meta, int32_t *node_state, int32_t *node_step,
+                         int64_t *arc_from, int64_t *arc_to, int32_t *arc_il, int32_t *arc_ol,
+                         double *arc_g, double *arc_a, int64_t *arc_tie, int64_t *final_node,
+                         double *final_wo) {
+    if (n_utts < 0 || (n_utts && (!meta || !out_meta))) return fail(WB_ERR_VALUE, "bad arguments");
+    // output offsets: utterances back to back in utterance order
+    int64_t cn = 0, ca = 0, cf = 0;
+    for (int32_t u = 0; u < n_utts; ++u) {
+        const int64_t *m = meta + 6 * (size_t)u;
+        if (m[0] < 0) return fail(WB_ERR_CAPACITY, "lattice output pool overflowed");
+        int64_t *o = out_meta + 6 * (size_t)u;
+        o[0] = cn; o[1] = m[1]; o[2] = ca; o[3] = m[3]; o[4] = cf; o[5] = m[5];
+        cn += m[1]; ca += m[3]; cf += m[5];
+    }
+    std::atomic<int32_t> next(0);
+    auto work = [&]() {
+        std::vector<int64_t> ord, newid, aord;
+        for (int32_t u; (u = next.fetch_add(1)) < n_utts;) {
+            const int64_t *m = meta + 6 * (size_t)u, *o = out_meta + 6 * (size_t)u;
+            const int64_t nn = m[1], na = m[3], nf = m[5];
+            if (nn == 0) continue;
+            const int32_t *nd = nodes + 2 * (size_t)m[0];
+            const uint32_t *ar = arcs + 4 * (size_t)m[2];
+            // nodes: [start] + (step, state) order (lattice.py:215-216)
+            ord.resize(nn);
+            for (int64_t i = 0; i < nn; ++i) ord[i] = i;
+            auto nkey = [&](int64_t i) {
+                const bool st0 = nd[2 * i] == start_state && nd[2 * i + 1] == 0;
+                return std::make_tuple(st0 ? 0 : 1, nd[2 * i + 1], nd[2 * i]);
+            };
+            std::sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) { return nkey(x) < nkey(y); });
+            newid.resize(nn);
+            for (int64_t r = 0; r < nn; ++r) {
+                newid[ord[r]] = r;
+                node_state[o[0] + r] = nd[2 * ord[r]];
+                node_step[o[0] + r] = nd[2 * ord[r] + 1];
+            }
+            // arcs: (from.step, from.state, to.step, to.state, ilabel, olabel, tie) (:227-230)
+            aord.resize(na);
+            for (int64_t e = 0; e < na; ++e) aord[e] = e;
+            auto akey = [&](int64_t e) {
+                const int64_t f = ar[4 * e], t = ar[4 * e + 1], a = ar[4 * e + 2];
+                return std::make_tuple(nd[2 * f + 1], nd[2 * f], nd[2 * t + 1], nd[2 * t],
+                                       g_ilabel[a], g_olabel[a], a);
+            };
+            std::stable_sort(aord.begin(), aord.end(), [&](int64_t x, int64_t y) { return akey(x) < akey(y); });
+            for (int64_t r = 0; r < na; ++r) {
+                const int64_t e = aord[r], a = ar[4 * e + 2];
+                arc_from[o[2] + r] = newid[ar[4 * e]];
+                arc_to[o[2] + r] = newid[ar[4 * e + 1]];
+                arc_il[o[2] + r] = g_ilabel[a];
+                arc_ol[o[2] + r] = g_olabel[a];
+                arc_g[o[2] + r] = g_weight[a];
+                arc_a[o[2] + r] = arc_ac[m[2] + e];
+                arc_tie[o[2] + r] = a;
+            }
+            for (int64_t q = 0; q < nf; ++q) {
+                final_node[o[4] + q] = newid[finals[m[4] + q]];
+                final_wo[o[4] + q] = final_w[m[4] + q];
+            }
+        }
+    };
+    const int nt = std::max(1, std::min<int>(n_threads > 0 ? n_threads : 1, n_utts));
+    std::vector<std::thread> pool;
+    for (int i = 1; i < nt; ++i) pool.emplace_back(work);
+    work();
+    for (auto &t : pool) t.join();
+    return WB_OK;
+}
 
 int wb_lattice_check(const wb_lattice_arrays *lat) {
     if (!lat) return fail(WB_ERR_VALUE, "null lattice");

@@ -282,7 +282,7 @@ class BatchDecoder:
 
     def fetch_lattices(self, wfst: Wfst) -> list:
         """Trimmed lattices of the last lattice-mode decode, canonically ordered."""
-        from .lattice import canonical_from_device
+        from .lattice import canonical_batch
         L = N.load()
         n = C.c_int32()
         nn, na, nf = C.c_int64(), C.c_int64(), C.c_int64()
@@ -296,14 +296,10 @@ class BatchDecoder:
         finw = np.zeros(max(nf.value, 1), np.float64)
         N.check(L.wb_lattice_fetch(self._h, meta.ctypes.data, nodes.ctypes.data, arcs.ctypes.data,
                                    ac.ctypes.data, fin.ctypes.data, finw.ctypes.data), "lattice")
-        out = []
-        for u in range(n.value):
-            no, cn, ao, ca, fo, cf = (int(x) for x in meta[u])
-            if no < 0:
-                raise N.CapacityError("lattice output pool overflowed")
-            out.append(canonical_from_device(wfst, nodes[no:no + cn], arcs[ao:ao + ca],
-                                             ac[ao:ao + ca], fin[fo:fo + cf], finw[fo:fo + cf]))
-        return out
+        meta = meta[:n.value]
+        if (meta[:, 0] < 0).any():
+            raise N.CapacityError("lattice output pool overflowed")
+        return canonical_batch(wfst, meta, nodes, arcs, ac, fin, finw)
 
     # ------------------------------------------------------------------ device buffers
     def decode_device(self, costs, row_offset, num_frames, blank, cfg, mode: str, results,

@@ -235,6 +235,50 @@ def canonical_from_device(wfst, nodes: np.ndarray, arcs: np.ndarray, arc_ac: np.
                    arc_ac[aord], ai[aord], fo, final_w)
 
 
+def canonical_batch(wfst, meta, nodes, arcs, arc_ac, finals, final_w,
+                    n_threads: int | None = None) -> list:
+    """``canonical_from_device`` for a whole batch: the C++ pass (``wb_lattice_canonical``)
+    orders every utterance's lattice on host threads, then each ``Lattice`` is a view into
+    the flat output arrays.  ``meta`` rows: {node_off, n_nodes, arc_off, n_arcs, final_off,
+    n_finals} into the fetched pools."""
+    import os
+    from . import _native as N
+    n = len(meta)
+    if n == 0:
+        return []
+    meta = np.ascontiguousarray(meta, np.int64)
+    nn, na, nf = (int(meta[:, i].sum()) for i in (1, 3, 5))
+    om = np.zeros((n, 6), np.int64)
+    out = dict(st=np.zeros(max(nn, 1), np.int32), sp=np.zeros(max(nn, 1), np.int32),
+               f=np.zeros(max(na, 1), np.int64), t=np.zeros(max(na, 1), np.int64),
+               il=np.zeros(max(na, 1), np.int32), ol=np.zeros(max(na, 1), np.int32),
+               g=np.zeros(max(na, 1), np.float64), a=np.zeros(max(na, 1), np.float64),
+               tie=np.zeros(max(na, 1), np.int64), fn=np.zeros(max(nf, 1), np.int64),
+               fw=np.zeros(max(nf, 1), np.float64))
+    ins = [np.ascontiguousarray(nodes, np.int32), np.ascontiguousarray(arcs, np.uint32),
+           np.ascontiguousarray(arc_ac, np.float64), np.ascontiguousarray(finals, np.uint32),
+           np.ascontiguousarray(final_w, np.float64)]
+    gi = [np.ascontiguousarray(wfst.ilabel, np.int32), np.ascontiguousarray(wfst.olabel, np.int32),
+          np.ascontiguousarray(wfst.weight, np.float64)]
+    threads = n_threads or len(os.sched_getaffinity(0))
+    rc = N.load().wb_lattice_canonical(
+        n, meta.ctypes.data, *(x.ctypes.data for x in ins), int(wfst.start),
+        *(x.ctypes.data for x in gi), threads, om.ctypes.data,
+        *(out[k].ctypes.data for k in ("st", "sp", "f", "t", "il", "ol", "g", "a", "tie", "fn", "fw")))
+    N.check(rc, "lattice")
+    res = []
+    for u in range(n):
+        n0, c0, a0, c1, f0, c2 = (int(x) for x in om[u])
+        if c0 == 0:
+            res.append(EMPTY_LATTICE)
+            continue
+        ns, as_, fs = slice(n0, n0 + c0), slice(a0, a0 + c1), slice(f0, f0 + c2)
+        res.append(Lattice(out["st"][ns], out["sp"][ns], out["f"][as_], out["t"][as_],
+                           out["il"][as_], out["ol"][as_], out["g"][as_], out["a"][as_],
+                           out["tie"][as_], out["fn"][fs], out["fw"][fs]))
+    return res
+
+
 class LatticeRecorder:
     """Pass as ``recorder=`` to ``decode`` / ``decode_fsd`` / ``decode_lsd`` /
     ``parallel_decode`` (lattice.py:96-135): the device records the raw lattice of that
@@ -407,6 +451,6 @@ def load_lattice(path: str) -> Lattice:
 
 
 __all__ = ["COST_EPS", "EMPTY_LATTICE", "Lattice", "LatticeArc", "LatticeError", "LatticeNode",
-           "LatticeRecorder", "build_lattice", "canonical_from_device", "format_lattice_text",
+           "LatticeRecorder", "build_lattice", "canonical_batch", "canonical_from_device", "format_lattice_text",
            "lattice_best_path", "load_lattice", "parse_lattice_text", "prune_lattice", "prune_lattices",
            "save_lattice"]

@@ -118,3 +118,36 @@ def test_gpu_lattice_capacity_retry(cuda):
     _, lats = _decode_lattices(g, costs, blanks, cfg, dec=small)
     _, ref = _decode_lattices(g, costs, blanks, cfg)
     assert [x.key() for x in lats] == [x.key() for x in ref]
+
+
+def test_gpu_lattice_pipeline_matches_direct(cuda):
+    """LatticePipeline (decode of batch i+1 overlapping host pruning of batch i) returns what
+    the direct decode + fetch + prune_lattice path returns."""
+    from paper_1808_00687_b200.pipeline import LatticePipeline
+    from paper_1808_00687_b200.posteriors import cost_table
+    g = synth.random_wfst(21, 300, 1200, 16, eps_fraction=0.05, final_fraction=0.1)
+    cfg = DecodeConfig(beam=7.0, max_active=40, mode="fsd")
+    batches = []
+    for b in range(3):
+        posts = [synth.random_posteriors(100 * b + i, 20 + 3 * i, 16) for i in range(5)]
+        costs = [cost_table(p) for p in posts]
+        T = np.asarray([len(c) for c in costs], np.int32)
+        off = np.zeros(len(T), np.int64)
+        np.cumsum(T[:-1], out=off[1:])
+        batches.append((np.concatenate(costs), off, T,
+                        np.concatenate([p.rows[:, 0] for p in posts])))
+    dec = BatchDecoder(g, 0, max_utts_in_flight=4)
+    with LatticePipeline(dec, lattice_beam=2.5) as pipe:
+        futs = [pipe.submit(c, o, t, bl, cfg) for c, o, t, bl in batches]
+        got = [f.result() for f in futs]
+    ref = BatchDecoder(g, 0, max_utts_in_flight=4)
+    for (c, o, t, bl), (out, lats) in zip(batches, got):
+        rout = ref.decode_host(c, o, t, bl, cfg, "fsd", lattice=True)
+        rl = ref.fetch_lattices(g)
+        assert rout.decode_results() == out.decode_results()
+        for a, b in zip(rl, lats):
+            try:
+                want = _key(L.prune_lattice(a, 2.5))
+            except L.LatticeError:
+                want = "error"
+            assert ("error" if isinstance(b, L.LatticeError) else _key(b)) == want

@@ -111,3 +111,43 @@ def test_prune_lattices_threaded_matches_serial():
                 want = "error"
             got = "error" if isinstance(p, L.LatticeError) else _key(p)
             assert got == want
+
+
+def test_canonical_batch_matches_per_utterance():
+    """The batch-vectorised canonical ordering of device pools == per-utterance ordering."""
+    from paper_1808_00687_b200 import synth
+    g = synth.random_wfst(1, 50, 300, 8, eps_fraction=0.1)
+    rng = np.random.default_rng(0)
+    parts = []
+    for u in range(8):
+        nn = int(rng.integers(0, 12))
+        if nn:
+            steps = np.sort(rng.integers(0, 4, nn))
+            steps[0] = 0
+            states = rng.choice(50, nn, replace=False).astype(np.int32)
+            states[0] = g.start
+            nodes = np.stack([states, steps], 1).astype(np.int32)[rng.permutation(nn)]
+            na = int(rng.integers(0, 20))
+            arcs = np.stack([rng.integers(0, nn, na), rng.integers(0, nn, na),
+                             rng.integers(0, g.num_arcs, na), np.zeros(na)], 1).astype(np.uint32)
+            ac = rng.random(na)
+            nf = int(rng.integers(1, 3))
+            fin, fw = rng.integers(0, nn, nf).astype(np.uint32), rng.random(nf)
+        else:
+            nodes, arcs = np.zeros((0, 2), np.int32), np.zeros((0, 4), np.uint32)
+            ac, fin, fw = np.zeros(0), np.zeros(0, np.uint32), np.zeros(0)
+        parts.append((nodes, arcs, ac, fin, fw))
+    meta = np.zeros((len(parts), 6), np.int64)
+    pools = [[], [], [], [], []]
+    c = [0, 0, 0]
+    for u in rng.permutation(len(parts)):   # pools filled in arbitrary utterance order
+        nodes, arcs, ac, fin, fw = parts[u]
+        meta[u] = [c[0], len(nodes), c[1], len(arcs), c[2], len(fin)]
+        for p, x in zip(pools, parts[u]):
+            p.append(x)
+        c = [c[0] + len(nodes), c[1] + len(arcs), c[2] + len(fin)]
+    got = L.canonical_batch(g, meta, *(np.concatenate(p) for p in pools))
+    for u, (nodes, arcs, ac, fin, fw) in enumerate(parts):
+        want = L.canonical_from_device(g, nodes, arcs, ac, fin, fw)
+        assert got[u].key() == want.key()
+        assert np.array_equal(got[u].arc_tie, want.arc_tie)
