@@ -48,3 +48,35 @@ def test_medium_graph(cuda, seed):
     posts = [synth.random_posteriors(seed * 7 + k, 120, 50, blank_fraction=0.2) for k in range(8)]
     _check_batch(g, posts, P.DecodeConfig(beam=10.0, max_active=300, mode="fsd"))
     _check_batch(g, posts, P.DecodeConfig(beam=7.0, mode="lsd"))
+
+
+@pytest.mark.parametrize("mode", ["fsd", "lsd"])
+def test_zero_copy_pinned_matches_copy_and_oracle(cuda, mode):
+    """A page-locked cost table is read zero-copy by the kernel (one staged row per step);
+    the results equal the copy path's and the oracle's, and only searched rows cross PCIe."""
+    import torch
+    from paper_1808_00687_b200.decoder import BatchDecoder
+    g = synth.random_wfst(5, 3000, 9000, 40, eps_fraction=0.03, selfloops=mode == "lsd",
+                          final_fraction=0.05)
+    posts = [synth.random_posteriors(40 + k, 150, 40, blank_fraction=0.6 if mode == "lsd" else 0.0)
+             for k in range(7)]
+    T = np.asarray([p.num_frames for p in posts], np.int32)
+    off = np.zeros(len(T), np.int64)
+    np.cumsum(T[:-1], out=off[1:])
+    pinned = torch.empty((int(T.sum()), 41), dtype=torch.float64, pin_memory=True)
+    blank = np.concatenate([p.rows[:, 0] for p in posts])
+    for p, o in zip(posts, off):
+        P.cost_table(p, out=pinned.numpy()[o:o + p.num_frames])
+    cfg = P.DecodeConfig(beam=9.0, max_active=200, mode=mode)
+    dec = BatchDecoder(g, 0)
+    zc = dec.decode_host(pinned.numpy(), off, T, blank, cfg, mode)
+    h2d, was_zc = dec.last_transfer()
+    assert was_zc
+    steps = int(zc.results["search_steps"].sum())
+    assert h2d == steps * 41 * 8 + blank.nbytes + off.nbytes + T.nbytes
+    cp = dec.decode_host(pinned.numpy().copy(), off, T, blank, cfg, mode)   # pageable -> copy
+    assert not dec.last_transfer()[1]
+    assert zc.decode_results() == cp.decode_results()
+    for p, r in zip(posts, zc.decode_results()):
+        o = O.decode(g, P.cost_table(p), p.rows[:, 0], beam=9.0, max_active=200, mode=mode)
+        assert _fields(r) == o.astuple()
