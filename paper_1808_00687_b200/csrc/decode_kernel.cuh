@@ -77,6 +77,7 @@ struct WorkDev {
     u32 *utt_ctr;
     long long S;
     int cap, T_cap, smem_cands, row_in_smem;
+    int stage_off;        // dyn-smem byte offset of the per-lane arc prefetch buffers (0 = off)
     // ---- lattice recording (LatticeRecorder / build_lattice, lattice.py:96-249)
     int *tok_eps;         // [slots][2][cap] epsilon-range start of each token's state
     u32 *sbits;           // [slots][ceil(S/32)] survivor bitmap of the current node step (L2-resident)
@@ -353,6 +354,81 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
     u32 *front0 = c.front(0);
     const int nchunks = (n_live + 31) >> 5;
     const Slot empty = {EMPTY_KEY, 0xFFFFFFFFu, 0xFFFFFFFFu};
+    if (ws.stage_off) {
+        // Software-pipelined: each lane prefetches its next arc record into shared memory
+        // (cp.async, no registers held) while its current relaxation's CAS is in flight, so an
+        // iteration costs one memory round trip instead of two.
+        int4 *stage = reinterpret_cast<int4 *>(dyn_smem() + ws.stage_off) + 2 * threadIdx.x;
+        const u32 s0 = (u32)__cvta_generic_to_shared(stage);
+        for (int ch = w; ch < nchunks; ch += NW) {
+            const int t = (ch << 5) + l;
+            int4 ti = make_int4(0, 0, 0, 0);
+            double tc = 0.0;
+            if (t < n_live) { ti = tinfo[t]; tc = tcost[t]; }
+            const int deg = t < n_live ? ti.w - ti.z : 0;
+            a_emit += deg;
+            const int incl = warp_incl_scan(deg);
+            const int total = __shfl_sync(FULL, incl, 31);
+            const int excl = incl - deg;
+            auto arc_of = [&](int j, int &k) {
+                k = warp_owner(excl, j);
+                return __shfl_sync(FULL, ti.z, k) + j - __shfl_sync(FULL, excl, k);
+            };
+            int k_next, arc_next = arc_of(l, k_next);
+            if (l < total)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s0), "l"(&g.arcs[2 * arc_next]));
+            asm volatile("cp.async.commit_group;");
+            for (int j0 = 0, it = 0; j0 < total; j0 += 32, ++it) {
+                const int j = j0 + l, k = k_next, arc = arc_next;
+                if (j0 + 32 < total) {  // prefetch the next iteration's record
+                    arc_next = arc_of(j + 32, k_next);
+                    if (j + 32 < total)
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s0 + 16u * ((it + 1) & 1)),
+                                     "l"(&g.arcs[2 * arc_next]));
+                }
+                asm volatile("cp.async.commit_group;");
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+                const double cst = __shfl_sync(FULL, tc, k);
+                Slot want;
+                want.pay = (u32)__shfl_sync(FULL, ti.y, k);
+                want.arcp1 = (u32)arc + 1u;
+                bool act = j < total;
+                int4 rec = make_int4(0, 0, 0, 0);
+                if (act) {
+                    rec = stage[it & 1];
+                    const double ac = row[rec.y];
+                    if (ac == INFINITY) {  // decoder.py:219-220: no relaxation, no record
+                        act = false;
+                    } else {
+                        want.key = cost_key(__dadd_rn(__dadd_rn(cst, __hiloint2double(rec.w, rec.z)), ac));
+                    }
+                }
+                if (ws.rlog) {  // lattice mode: log the finite relaxations for record_lattice_step
+                    const u32 m = __ballot_sync(FULL, act);
+                    if (m) {
+                        int base = 0;
+                        if (l == __ffs(m) - 1) base = atomicAdd(&SH<BLOCK>().n_log, __popc(m));
+                        base = __shfl_sync(FULL, base, __ffs(m) - 1);
+                        const long long e = base + __popc(m & lanemask_lt());
+                        if (act && e < ws.rlog_cap)
+                            ws.rlog[(size_t)blockIdx.x * ws.rlog_cap + e] =
+                                make_int4((ch << 5) + k, arc, rec.x, rec.y);
+                    }
+                }
+                bool first = false, dec = false;
+                if (act) {
+                    a_fin++;
+                    const Slot prev = cas_slot(&slot[rec.x], empty, want);
+                    finish_relax(&slot[rec.x], want, prev, &first, &dec);
+                }
+                int4 r1 = make_int4(0, 0, 0, 0);
+                if (first) r1 = __ldg(&g.arcs[2 * arc + 1]);
+                warp_append<BLOCK>(first, (u32)rec.x, r1, true, g, ws, front0);
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+        }
+        return ExpandCounts{a_emit, a_fin};
+    }
     for (int ch = w; ch < nchunks; ch += NW) {
         int t = (ch << 5) + l;
         int4 ti = make_int4(0, 0, 0, 0);

@@ -284,7 +284,12 @@ static cudaError_t launch_decode(int max_grid, int num_sms, int num_cols, cudaSt
     if (zero_copy && row == 0) return cudaErrorNotSupported;  // host rows must be staged
     wd.smem_cands = (int)std::min<size_t>(avail / (sizeof(u64) + sizeof(u32)), (size_t)wd.cap);
     wd.row_in_smem = row > 0;
-    size_t smem = hdr + std::max(row, (size_t)wd.smem_cands * (sizeof(u64) + sizeof(u32)));
+    // per-lane arc prefetch buffers (2 x 16 B) after the staged row, when they fit
+    const size_t row_r = (row + 127) & ~(size_t)127, stage = (size_t)BLOCK * 32;
+    const char *pf = std::getenv("WB_PREFETCH");
+    wd.stage_off = (row > 0 && row_r + stage <= avail && !(pf && pf[0] == '0')) ? (int)(hdr + row_r) : 0;
+    size_t smem = hdr + std::max(wd.stage_off ? row_r + stage : row,
+                                 (size_t)wd.smem_cands * (sizeof(u64) + sizeof(u32)));
     smem = (smem + 15) & ~(size_t)15;
     e = cudaFuncSetAttribute(decode_kernel<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
