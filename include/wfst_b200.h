@@ -35,6 +35,15 @@ extern "C" {
 #define WB_ERR_LATTICE 3
 #define WB_ERR_WFST 4
 #define WB_ERR_CAPACITY 5  /* a device workspace capacity was exceeded; retry with a larger one */
+
+/* wb_utt_result.capacity_flags: which capacity a WB_ERR_CAPACITY utterance exceeded */
+#define WB_CAP_CANDIDATES 1    /* per-step candidates / epsilon frontier (cand_capacity) */
+#define WB_CAP_ARENA 2         /* backpointer records (arena_capacity) */
+#define WB_CAP_FRAMES 4        /* LSD frame list (max_frames) */
+#define WB_CAP_LABELS 8        /* label_capacity of the wb_decode call */
+#define WB_CAP_LATTICE_RAW 16  /* raw lattice pools (lattice_capacity) */
+#define WB_CAP_LATTICE_OUT 32  /* trimmed lattice output pools (lattice_out_capacity) */
+#define WB_CAP_EPS_ROUNDS 64   /* epsilon closure did not converge within 2^20 rounds */
 #define WB_ERR_NOMEM 6
 
 #define WB_MEM_DEVICE 0    /* all batch pointers are device pointers; the call is asynchronous */
@@ -80,6 +89,8 @@ typedef struct {
     int32_t n_olabels;
     int32_t n_ilabels;
     int32_t status;          /* WB_OK or WB_ERR_CAPACITY */
+    int32_t capacity_flags;  /* WB_CAP_* bits of a WB_ERR_CAPACITY utterance */
+    int32_t _pad;
     int64_t best_trace;      /* lane-arena index of the winning token's record */
     /* counters for the roofline: summed over the utterance's steps */
     int64_t n_tok;           /* live tokens expanded */

@@ -37,6 +37,8 @@ constexpr int GCAP = 1024;           // boundary-bucket members ranked in shared
 constexpr int ROW_SMEM_MAX = 16384;  // cost-row columns staged in shared memory (128 KB)
 constexpr u32 F_SURV = 1u, F_MARK = 2u, CA_NONE = 0xFFFFFFFFu;
 constexpr int MAX_EPS_ROUNDS = 1 << 20;
+// Capacity failures carry their cause above the status byte (reported as capacity_flags)
+__host__ __device__ constexpr int wb_cap(int cause) { return WB_ERR_CAPACITY | (cause << 8); }
 // relaxations in flight per lane (expand) / gathers per thread (prune): halved for 1024-thread
 // CTAs, whose register budget is 64 per thread
 #ifndef WB_UNROLL_1024
@@ -530,7 +532,7 @@ __noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev 
         int n_front = sh.n_front;
         __syncthreads();
         if (n_front == 0) break;
-        if (++rounds > MAX_EPS_ROUNDS) { status = WB_ERR_CAPACITY; break; }
+        if (++rounds > MAX_EPS_ROUNDS) { status = wb_cap(WB_CAP_EPS_ROUNDS); break; }
         if (threadIdx.x == 0) {
             sh.n_front = 0;
             sh.tag_round = (int)(tag_cur + 1u);
@@ -730,7 +732,7 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
     Smem<BLOCK> &sh = SH<BLOCK>();
     const Lane c{ws};
     const int n_cand = min(sh.n_cand, ws.cap);
-    int status = sh.overflow ? WB_ERR_CAPACITY : WB_OK;
+    int status = sh.overflow ? wb_cap(WB_CAP_CANDIDATES) : WB_OK;
     const bool in_smem = n_cand <= ws.smem_cands;
     u64 *ckey = in_smem ? s_key<BLOCK>() : c.cand_key();
     u32 *ca = in_smem ? s_ca<BLOCK>(ws) : c.cand_ca();
@@ -856,7 +858,7 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
     }
     __syncthreads();
     const int n_keep = (int)sh.wa[NW], n_surv = (int)sh.wb[NW];
-    if (sh.overflow == 2) { __syncthreads(); return StepOut{0, 0, WB_ERR_CAPACITY}; }
+    if (sh.overflow == 2) { __syncthreads(); return StepOut{0, 0, wb_cap(WB_CAP_ARENA)}; }
     const u64 base = sh.arena_base;
     int4 *tinfo = c.tok_info(nxt);
     double *tcost = c.tok_cost(nxt);
@@ -1034,7 +1036,7 @@ __noinline__ __device__ int record_lattice_step(int k, int nxt, int n_surv, int 
     __syncthreads();
     const bool extra = k == 0 && sh.ng < 0;
     const int n_nodes = n_surv + (extra ? 1 : 0);
-    if ((long long)node_base + n_nodes > ws.lat_cap) return WB_ERR_CAPACITY;
+    if ((long long)node_base + n_nodes > ws.lat_cap) return wb_cap(WB_CAP_LATTICE_RAW);
     for (int j = threadIdx.x; j < n_nodes; j += BLOCK) {
         const u32 st = j < n_surv ? (u32)tn[j].x : (u32)g.start;
         atomicOr(&ws.sbits[bo + (st >> 5)], 1u << (st & 31));
@@ -1054,7 +1056,7 @@ __noinline__ __device__ int record_lattice_step(int k, int nxt, int n_surv, int 
     // emitting arcs from live(k-1): the finite relaxations expand logged, into survivors
     if (k > 0) {
         const int n_log = sh.n_log;
-        if ((long long)n_log > ws.rlog_cap) status = WB_ERR_CAPACITY;
+        if ((long long)n_log > ws.rlog_cap) status = wb_cap(WB_CAP_LATTICE_RAW);
         const int4 *lg = ws.rlog + (size_t)blockIdx.x * ws.rlog_cap;
         const int nl = (int)min((long long)n_log, ws.rlog_cap);
         constexpr int G = 4;  // log entries per thread with their loads in flight
@@ -1147,7 +1149,7 @@ __noinline__ __device__ int record_lattice_step(int k, int nxt, int n_surv, int 
     }
     __syncthreads();
     const int n_all = sh.n_pend;
-    if (n_all > room) status = WB_ERR_CAPACITY;
+    if (n_all > room) status = wb_cap(WB_CAP_LATTICE_RAW);
     for (int j = threadIdx.x; j < n_nodes; j += BLOCK)  // every set bit is one of these nodes
         ws.sbits[bo + (ws.ln_state[lo + node_base + j] >> 5)] = 0u;
     if (threadIdx.x == 0) {
@@ -1408,7 +1410,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
         int nf = T;
         if (cfg.mode == 1) {
             if (T > ws.T_cap) {  // frame list would overflow: report, do not decode
-                status = WB_ERR_CAPACITY;
+                status = wb_cap(WB_CAP_FRAMES);
                 nf = 0;
             } else {
                 nf = lsd_prepass<BLOCK>(b.blank + row0, T, cfg.thr, c.frames());
@@ -1538,7 +1540,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
                 const int4 lk = ws.lstep[(size_t)blockIdx.x * (ws.T_cap + 2) + fstep];
                 lat_arcs = lk.y + lk.w + ws.lstep_eps[(size_t)blockIdx.x * (ws.T_cap + 2) + fstep];
                 trim_lattice<BLOCK>(u, fstep, reached, best_t >= 0 ? tinfo[best_t].x : -1, g, ws);
-                if (ws.o_meta[6 * (size_t)u] < 0) status = WB_ERR_CAPACITY;
+                if (ws.o_meta[6 * (size_t)u] < 0) status = wb_cap(WB_CAP_LATTICE_OUT);
             } else if (threadIdx.x == 0) {
                 ws.o_meta[6 * (size_t)u] = -1;
             }
@@ -1561,9 +1563,13 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             r.best_trace = best_t >= 0 ? (long long)(u32)tinfo[best_t].y : -1;
             backtrace(g, c.arena(), r.best_trace, b.olab + (size_t)u * b.lab_cap,
                       b.ilab + (size_t)u * b.lab_cap, b.lab_cap, &r.n_olabels, &r.n_ilabels);
-            if ((r.n_olabels > b.lab_cap || r.n_ilabels > b.lab_cap) && status == WB_OK)
-                status = WB_ERR_CAPACITY;
-            r.status = status;
+            int capf = status >> 8;
+            if (r.n_olabels > b.lab_cap || r.n_ilabels > b.lab_cap) {
+                capf |= WB_CAP_LABELS;
+                if (status == WB_OK) status = WB_ERR_CAPACITY;
+            }
+            r.status = status & 0xFF;
+            r.capacity_flags = capf;
             r.n_tok = n_tok;
             r.a_emit = t_emit;
             r.a_fin = t_fin;

@@ -185,17 +185,25 @@ class BatchDecoder:
         self._h = h
         self._fin = weakref.finalize(self, N.load().wb_decoder_destroy, h)
 
-    def _grow(self, arena_need: int | None = None, lattice: bool = False,
-              lattice_out_need: int = 0):
+    def _grow(self, flags: int, lattice_out_need: int = 0, max_frames: int = 0):
+        """Recreate the workspace with the capacities named by ``flags`` (WB_CAP_* bits of
+        the failed utterances) enlarged; results are deterministic, so the retry is exact."""
         S = self.graph.wfst.num_states
-        if lattice:
+        if flags & N.WB_CAP_EPS_ROUNDS:
+            raise N.CapacityError("epsilon closure did not converge (2^20 rounds)")
+        if flags & N.WB_CAP_LATTICE_RAW:
             self.opts["lattice_capacity"] = min(2**31 - 2, 4 * (self.opts["lattice_capacity"] or (1 << 20)))
+        if flags & N.WB_CAP_LATTICE_OUT:
             out = self.opts["lattice_out_capacity"] or (1 << 22)
             self.opts["lattice_out_capacity"] = max(2 * out, lattice_out_need * 5 // 4)
-        cap = self.opts["cand_capacity"] or min(S, 1 << 18)
-        self.opts["cand_capacity"] = min(S, cap * 2)
-        arena = self.opts["arena_capacity"] or (1 << 22)
-        self.opts["arena_capacity"] = min(2**31 - 2, max(arena * 2, arena_need or 0))
+        if flags & (N.WB_CAP_CANDIDATES | N.WB_CAP_LATTICE_RAW):  # the relaxation log follows cap
+            cap = self.opts["cand_capacity"] or min(S, 1 << 18)
+            self.opts["cand_capacity"] = min(S, cap * 4)
+        if flags & N.WB_CAP_ARENA:
+            arena = self.opts["arena_capacity"] or (1 << 22)
+            self.opts["arena_capacity"] = min(2**31 - 2, arena * 4)
+        if flags & N.WB_CAP_FRAMES:
+            self.opts["max_frames"] = max(max_frames, 2 * (self.opts["max_frames"] or 2048))
         self._create()
 
     def device_bytes(self) -> int:
@@ -255,7 +263,7 @@ class BatchDecoder:
         self.reserve(int(num_frames.sum()) + n, cfg.max_active, maxT, lattice)
         cap = label_capacity or (maxT + 64)
         ncfg = _native_config(cfg, mode, lattice)
-        for _attempt in range(8):
+        for _attempt in range(16):
             res = np.zeros(n, dtype=N.UTT_RESULT_DTYPE)
             ol = np.zeros((n, cap), dtype=np.int32)
             il = np.zeros((n, cap), dtype=np.int32)
@@ -267,17 +275,17 @@ class BatchDecoder:
             bad = res["status"] != N.WB_OK
             if not bad.any():
                 return BatchOutput(res, ol, il, cap)
-            longest = np.maximum(res["n_olabels"], res["n_ilabels"])
-            if (longest[bad] > cap).any():
-                cap = int(longest.max())          # labels did not fit: rerun with exact room
-            if (bad & (longest <= cap)).any():
+            flags = int(np.bitwise_or.reduce(res["capacity_flags"][bad]))
+            if flags & N.WB_CAP_LABELS:           # labels did not fit: rerun with exact room
+                cap = int(np.maximum(res["n_olabels"], res["n_ilabels"]).max())
+            if flags & ~N.WB_CAP_LABELS:
                 need = 0
-                if lattice:                       # exact output-pool need from the counters
+                if flags & N.WB_CAP_LATTICE_OUT:  # exact output-pool need from the counters
                     nu, nn, na, nf = C.c_int32(), C.c_int64(), C.c_int64(), C.c_int64()
                     N.check(N.load().wb_lattice_totals(self._h, C.byref(nu), C.byref(nn),
                                                        C.byref(na), C.byref(nf)), "lattice")
                     need = max(nn.value, na.value, nf.value)
-                self._grow(lattice=lattice, lattice_out_need=need)
+                self._grow(flags, lattice_out_need=need, max_frames=maxT)
         raise N.CapacityError("decode workspace kept overflowing")
 
     def fetch_lattices(self, wfst: Wfst) -> list:

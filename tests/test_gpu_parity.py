@@ -80,3 +80,34 @@ def test_zero_copy_pinned_matches_copy_and_oracle(cuda, mode):
     for p, r in zip(posts, zc.decode_results()):
         o = O.decode(g, P.cost_table(p), p.rows[:, 0], beam=9.0, max_active=200, mode=mode)
         assert _fields(r) == o.astuple()
+
+
+def test_capacity_flags_and_targeted_retry(cuda):
+    """Undersized workspaces report which capacity overflowed (WB_CAP_*) and decode_host
+    grows exactly that one; the retried batch equals a decode with ample room."""
+    from paper_1808_00687_b200 import _native as N
+    from paper_1808_00687_b200.decoder import BatchDecoder, _native_config
+    import ctypes as C
+    g = synth.random_wfst(8, 2000, 7000, 30, eps_fraction=0.05, final_fraction=0.1)
+    posts = [synth.random_posteriors(70 + k, 60, 30) for k in range(5)]
+    T = np.asarray([p.num_frames for p in posts], np.int32)
+    off = np.zeros(len(T), np.int64)
+    np.cumsum(T[:-1], out=off[1:])
+    costs = np.concatenate([P.cost_table(p) for p in posts])
+    blank = np.concatenate([p.rows[:, 0] for p in posts])
+    cfg = P.DecodeConfig(beam=9.0, max_active=150, mode="fsd")
+    want = BatchDecoder(g, 0).decode_host(costs, off, T, blank, cfg, "fsd").decode_results()
+    # raw call on a tiny workspace: every utterance fails with a named cause
+    tiny = BatchDecoder(g, 0, cand_capacity=16, arena_capacity=1024)
+    res = np.zeros(len(T), dtype=N.UTT_RESULT_DTYPE)
+    lab = np.zeros((len(T), 2), np.int32)
+    ncfg = _native_config(cfg, "fsd")
+    N.check(N.load().wb_decode(tiny._h, len(T), costs.ctypes.data, off.ctypes.data,
+                               T.ctypes.data, costs.shape[1], blank.ctypes.data, C.byref(ncfg),
+                               res.ctypes.data, lab.ctypes.data, lab.ctypes.data, 1,
+                               N.WB_MEM_HOST, None))
+    assert (res["status"] == N.WB_ERR_CAPACITY).all()
+    assert (res["capacity_flags"] & (N.WB_CAP_CANDIDATES | N.WB_CAP_ARENA)).all()
+    # the Python entry point retries until it fits, with identical results
+    got = tiny.decode_host(costs, off, T, blank, cfg, "fsd", label_capacity=1).decode_results()
+    assert got == want
