@@ -325,7 +325,7 @@ def main():
 
     def step():
         dec.decode_device(costs_d, off_d, T_d, blank_d, dcfg, cfg["mode"], res_d, ol_d, il_d, cap,
-                          lattice=lat_on)
+                          lattice=lat_on, lattice_beam=cfg.get("lattice_beam"))
 
     for _ in range(max(args.warmup, 0)):
         step()

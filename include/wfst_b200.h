@@ -75,6 +75,8 @@ typedef struct {
     int32_t mode;            /* 0 = fsd, 1 = lsd */
     int32_t lattice;         /* 1 = record the raw lattice (LatticeRecorder) */
     int32_t _pad;
+    double lattice_beam;     /* >= 0 (lattice mode): also beam-prune the lattices on the device
+                                (stage one of prune_lattice, see wb_lattice_pruned_fetch); < 0 off */
 } wb_config;
 
 /* Per-utterance result (DecodeResult, decoder.py:97-105) plus device counters. */
@@ -213,10 +215,28 @@ int wb_lattice_check(const wb_lattice_arrays *lat);
  * of the best, then the path-exact split; WB_ERR_LATTICE past 500,000 split nodes. */
 int wb_lattice_prune(const wb_lattice_arrays *lat, double beam, wb_lattice_arrays *out);
 void wb_lattice_arrays_free(wb_lattice_arrays *a);
+/* _enforce_path_soundness (lattice.py:430-501) on a lattice already cut at `cutoff` (stage one,
+ * e.g. from wb_lattice_pruned_fetch): splits nodes whose prefix/suffix recombination could
+ * exceed the cutoff; WB_ERR_LATTICE past 500,000 keys. */
+int wb_lattice_split(const wb_lattice_arrays *lat, double cutoff, wb_lattice_arrays *out);
 /* lattice_best_path (lattice.py:504-559): tie-exact minimum-cost path and its labels. */
 int wb_lattice_best_path(const wb_lattice_arrays *lat, double *cost, int32_t *olabels,
                          int32_t *n_olabels, int32_t *ilabels, int32_t *n_ilabels,
                          int32_t capacity);
+
+/*
+ * Device lattice-beam pruning (cfg.lattice_beam >= 0): stage one of prune_lattice
+ * (lattice.py:359-394) -- exact forward-backward costs, the cut at (best + beam) + 1e-9 and the
+ * re-trim -- runs in a second kernel on the trimmed lattices.  Pools as in wb_lattice_fetch;
+ * meta rows have 8 fields: {node_off, n_nodes, arc_off, n_arcs, final_off, n_finals,
+ * best (float64 bits: the lattice's best path cost), status (WB_OK, WB_ERR_LATTICE for an
+ * epsilon cycle among lattice nodes, WB_ERR_CAPACITY)}.  The path-exact second stage is
+ * wb_lattice_split with cutoff = (best + beam) + 1e-9.
+ */
+int wb_lattice_pruned_totals(wb_decoder_t d, int32_t *n_utts, int64_t *n_nodes, int64_t *n_arcs,
+                             int64_t *n_finals);
+int wb_lattice_pruned_fetch(wb_decoder_t d, int64_t *meta, int32_t *nodes, uint32_t *arcs,
+                            double *arc_ac, uint32_t *finals, double *final_w);
 
 /* Host->device bytes of the last WB_MEM_HOST wb_decode call and whether its cost table was
  * read zero-copy (page-locked host memory, one staged row per search step: the transfer

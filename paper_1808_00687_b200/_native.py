@@ -39,7 +39,7 @@ class GraphDesc(C.Structure):
 class Config(C.Structure):
     _fields_ = [("beam", C.c_double), ("blank_threshold", C.c_double),
                 ("max_active", C.c_int32), ("mode", C.c_int32), ("lattice", C.c_int32),
-                ("_pad", C.c_int32)]
+                ("_pad", C.c_int32), ("lattice_beam", C.c_double)]
 
 
 class DecoderOpts(C.Structure):
@@ -74,7 +74,8 @@ EXPORTED = ("wb_last_error", "wb_version", "wb_device_count", "wb_graph_create",
             "wb_decoder_destroy", "wb_decoder_device_bytes", "wb_decode", "wb_last_kernel_ms",
             "wb_lattice_totals", "wb_lattice_fetch", "wb_lattice_check", "wb_lattice_prune",
             "wb_lattice_arrays_free", "wb_lattice_best_path", "wb_last_transfer",
-            "wb_lattice_canonical")
+            "wb_lattice_canonical", "wb_lattice_pruned_totals", "wb_lattice_pruned_fetch",
+            "wb_lattice_split")
 
 
 def load():
@@ -103,10 +104,13 @@ def load():
     L.wb_lattice_totals.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int64),
                                     C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     L.wb_lattice_fetch.argtypes = [C.c_void_p] + [C.c_void_p] * 6
+    L.wb_lattice_pruned_totals.argtypes = L.wb_lattice_totals.argtypes
+    L.wb_lattice_pruned_fetch.argtypes = [C.c_void_p] + [C.c_void_p] * 6
     LP = C.POINTER(LatticeArrays)
     L.wb_lattice_check.argtypes = [LP]
     L.wb_lattice_prune.argtypes = [LP, C.c_double, LP]
     L.wb_lattice_arrays_free.argtypes = [LP]
+    L.wb_lattice_split.argtypes = [LP, C.c_double, LP]
     L.wb_lattice_arrays_free.restype = None
     L.wb_lattice_canonical.argtypes = [C.c_int32] + [C.c_void_p] * 6 + [C.c_int32] + \
         [C.c_void_p] * 3 + [C.c_int32] + [C.c_void_p] * 12

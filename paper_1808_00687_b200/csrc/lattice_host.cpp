@@ -537,6 +537,17 @@ int wb_lattice_prune(const wb_lattice_arrays *lat, double beam, wb_lattice_array
     return WB_OK;
 }
 
+int wb_lattice_split(const wb_lattice_arrays *lat, double cutoff, wb_lattice_arrays *out) {
+    if (!lat || !out) return fail(WB_ERR_VALUE, "null lattice");
+    std::memset(out, 0, sizeof(*out));
+    Lat L = from_view(lat), P;
+    if (L.empty) return WB_OK;
+    int rc = soundness(L, cutoff, P);
+    if (rc) return rc;
+    to_view(P, out);
+    return WB_OK;
+}
+
 void wb_lattice_arrays_free(wb_lattice_arrays *a) {
     if (!a) return;
     void *ptrs[] = {a->node_state, a->node_step, a->arc_from, a->arc_to, a->arc_tie, a->arc_il,

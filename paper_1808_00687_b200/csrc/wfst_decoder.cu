@@ -12,6 +12,7 @@
 
 #include "../../include/wfst_b200.h"
 #include "decode_kernel.cuh"
+#include "prune_kernel.cuh"
 
 using namespace wb;
 
@@ -88,6 +89,20 @@ struct wb_decoder_s {
     unsigned long long *o_ctr = nullptr;
     long long *o_meta = nullptr;
     int lat_n = 0;                 // utterances of the last lattice decode
+    // device lattice-beam pruning (pools sized like the o_* pools; scratch per pool node / arc)
+    int2 *p_node = nullptr;
+    uint4 *p_arc = nullptr;
+    double *p_ac = nullptr, *p_finw = nullptr;
+    u32 *p_fin = nullptr;
+    u64 *p_fw = nullptr, *p_bw = nullptr;
+    unsigned char *p_nflag = nullptr, *p_aflag = nullptr;
+    int *p_depth = nullptr, *p_steps = nullptr;
+    unsigned long long *p_ctr = nullptr;
+    long long *p_meta = nullptr;
+    size_t p_node_n = 0, p_arc_n = 0, p_fin_n = 0, p_meta_n = 0, p_steps_n = 0;
+    size_t p_fw_n = 0, p_bw_n = 0, p_nflag_n = 0, p_depth_n = 0, p_aflag_n = 0, p_ac_n = 0,
+           p_finw_n = 0, p_ctr_n = 0;
+    int pruned_n = 0;
     cudaStream_t lat_stream = nullptr;
     size_t lat_bytes = 0;
 };
@@ -182,7 +197,9 @@ static void free_decoder(wb_decoder_s *d) {
                     d->h_off, d->h_T, d->h_res, d->h_lab, d->tok_eps, d->sbits, d->snode,
                     d->ln_state, d->ln_out, d->ln_flag, d->la_src, d->la_dst, d->la_arc,
                     d->la_ac, d->lstep, d->lstep_eps, d->lstep_start, d->o_node, d->o_arc,
-                    d->o_ac, d->o_finw, d->o_fin, d->o_ctr, d->o_meta, d->rlog};
+                    d->o_ac, d->o_finw, d->o_fin, d->o_ctr, d->o_meta, d->rlog, d->p_node,
+                    d->p_arc, d->p_ac, d->p_finw, d->p_fin, d->p_fw, d->p_bw, d->p_nflag,
+                    d->p_aflag, d->p_depth, d->p_steps, d->p_ctr, d->p_meta};
     for (void *p : ptrs) cudaFree(p);
     if (d->ev0) cudaEventDestroy(d->ev0);
     if (d->ev1) cudaEventDestroy(d->ev1);
@@ -517,6 +534,10 @@ int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row
     }
     BatchDev bd{dc, doff, dT, db, num_cols, n, dol, dil, lcap};
     CfgDev cd{cfg->beam, cfg->blank_threshold, cfg->max_active, cfg->mode, cfg->lattice};
+    const bool prune = cfg->lattice && cfg->lattice_beam >= 0;
+    if (cfg->lattice && !(cfg->lattice_beam < 0) && std::isnan(cfg->lattice_beam))
+        return set_err(WB_ERR_VALUE, "lattice_beam must be >= 0");
+    d->pruned_n = 0;
     // 1024 threads per CTA, one persistent CTA (utterance lane) per SM
     int block = d->block ? d->block : 1024;
     int max_grid = std::min(n, d->slots);
@@ -541,6 +562,34 @@ int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row
         e = launch();
     }
     d->last_zero_copy = zc ? 1 : 0;
+    if (e == cudaSuccess && prune) {
+        const size_t nn = d->o_node_n, na = d->o_arc_n, nf = d->o_fin_n;
+        const size_t T2 = (size_t)d->T_cap + 3;
+        int rc;
+        if ((rc = grow(&d->p_node, d->p_node_n, nn)) || (rc = grow(&d->p_arc, d->p_arc_n, na)) ||
+            (rc = grow(&d->p_ac, d->p_ac_n, na)) || (rc = grow(&d->p_fin, d->p_fin_n, nf)) ||
+            (rc = grow(&d->p_finw, d->p_finw_n, nf)) || (rc = grow(&d->p_fw, d->p_fw_n, nn)) ||
+            (rc = grow(&d->p_bw, d->p_bw_n, nn)) || (rc = grow(&d->p_nflag, d->p_nflag_n, nn + 4)) ||
+            (rc = grow(&d->p_depth, d->p_depth_n, nn)) || (rc = grow(&d->p_aflag, d->p_aflag_n, na)) ||
+            (rc = grow(&d->p_steps, d->p_steps_n, (size_t)n * T2 * 3)) ||
+            (rc = grow(&d->p_ctr, d->p_ctr_n, 4)) || (rc = grow(&d->p_meta, d->p_meta_n, (size_t)n * 8)))
+            return rc;
+        CUDA_TRY(cudaMemsetAsync(d->p_ctr, 0, sizeof(unsigned long long) * 4, st));
+        PruneDev P;
+        std::memset(&P, 0, sizeof(P));
+        P.node = d->o_node; P.arc = d->o_arc; P.ac = d->o_ac; P.fin = d->o_fin; P.finw = d->o_finw;
+        P.meta = d->o_meta; P.garcs = g->arcs; P.n = n; P.start = g->start; P.T2 = (int)T2;
+        P.lbeam = cfg->lattice_beam;
+        P.fw = d->p_fw; P.bw = d->p_bw; P.nflag = d->p_nflag; P.aflag = d->p_aflag;
+        P.depth = d->p_depth;
+        P.nstart = d->p_steps; P.gstart = d->p_steps + (size_t)n * T2; P.gsplit = d->p_steps + 2 * (size_t)n * T2;
+        P.p_node = d->p_node; P.p_arc = d->p_arc; P.p_ac = d->p_ac; P.p_fin = d->p_fin;
+        P.p_finw = d->p_finw; P.p_node_cap = (long long)d->p_node_n; P.p_arc_cap = (long long)d->p_arc_n;
+        P.p_fin_cap = (long long)d->p_fin_n; P.p_ctr = d->p_ctr; P.p_meta = d->p_meta;
+        prune_kernel<128><<<n, 128, 0, st>>>(P);
+        CUDA_TRY(cudaGetLastError());
+        d->pruned_n = n;
+    }
     if (e != cudaSuccess)
         return set_err(WB_ERR_CUDA, std::string("decode launch: ") + cudaGetErrorString(e));
     CUDA_TRY(cudaEventRecord(d->ev1, st));
@@ -559,6 +608,42 @@ int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row
             d->last_h2d += steps * (long long)num_cols * (long long)sizeof(double) * (cfg->lattice ? 2 : 1);
         }
     }
+    return WB_OK;
+}
+
+int wb_lattice_pruned_totals(wb_decoder_t d, int32_t *n_utts, int64_t *n_nodes, int64_t *n_arcs,
+                             int64_t *n_finals) {
+    if (!d || !n_utts || !n_nodes || !n_arcs || !n_finals) return set_err(WB_ERR_VALUE, "null argument");
+    *n_utts = 0; *n_nodes = *n_arcs = *n_finals = 0;
+    if (!d->p_ctr || d->pruned_n == 0) return WB_OK;
+    CUDA_TRY(cudaSetDevice(d->g->device));
+    CUDA_TRY(cudaStreamSynchronize(d->lat_stream));
+    unsigned long long c[4];
+    CUDA_TRY(cudaMemcpy(c, d->p_ctr, sizeof(c), cudaMemcpyDeviceToHost));
+    *n_utts = d->pruned_n;
+    *n_nodes = (int64_t)c[0];
+    *n_arcs = (int64_t)c[1];
+    *n_finals = (int64_t)c[2];
+    return WB_OK;
+}
+
+int wb_lattice_pruned_fetch(wb_decoder_t d, int64_t *meta, int32_t *nodes, uint32_t *arcs,
+                            double *arc_ac, uint32_t *finals, double *final_w) {
+    if (!d || !meta) return set_err(WB_ERR_VALUE, "null argument");
+    int32_t n;
+    int64_t nn, na, nf;
+    int rc = wb_lattice_pruned_totals(d, &n, &nn, &na, &nf);
+    if (rc) return rc;
+    if (n == 0) return WB_OK;
+    nn = std::min<int64_t>(nn, (int64_t)d->p_node_n);
+    na = std::min<int64_t>(na, (int64_t)d->p_arc_n);
+    nf = std::min<int64_t>(nf, (int64_t)d->p_fin_n);
+    CUDA_TRY(cudaMemcpy(meta, d->p_meta, sizeof(long long) * 8 * (size_t)n, cudaMemcpyDeviceToHost));
+    if (nn && nodes) CUDA_TRY(cudaMemcpy(nodes, d->p_node, sizeof(int2) * nn, cudaMemcpyDeviceToHost));
+    if (na && arcs) CUDA_TRY(cudaMemcpy(arcs, d->p_arc, sizeof(uint4) * na, cudaMemcpyDeviceToHost));
+    if (na && arc_ac) CUDA_TRY(cudaMemcpy(arc_ac, d->p_ac, sizeof(double) * na, cudaMemcpyDeviceToHost));
+    if (nf && finals) CUDA_TRY(cudaMemcpy(finals, d->p_fin, sizeof(u32) * nf, cudaMemcpyDeviceToHost));
+    if (nf && final_w) CUDA_TRY(cudaMemcpy(final_w, d->p_finw, sizeof(double) * nf, cudaMemcpyDeviceToHost));
     return WB_OK;
 }
 

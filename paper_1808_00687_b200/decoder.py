@@ -60,9 +60,11 @@ class SearchDied(RuntimeError):
     """For callers that treat an emptied beam as fatal (decoder.py:108-110)."""
 
 
-def _native_config(cfg, mode: str, lattice: bool = False) -> N.Config:
+def _native_config(cfg, mode: str, lattice: bool = False,
+                   lattice_beam: float | None = None) -> N.Config:
     return N.Config(float(cfg.beam), float(cfg.blank_threshold), int(cfg.max_active or 0),
-                    0 if mode == "fsd" else 1, int(bool(lattice)), 0)
+                    0 if mode == "fsd" else 1, int(bool(lattice)), 0,
+                    -1.0 if lattice_beam is None else float(lattice_beam))
 
 
 # ---------------------------------------------------------------- graph residency
@@ -249,7 +251,7 @@ class BatchDecoder:
     # ------------------------------------------------------------------ host buffers (e2e)
     def decode_host(self, costs: np.ndarray, row_offset: np.ndarray, num_frames: np.ndarray,
                     blank: np.ndarray, cfg, mode: str, label_capacity: int | None = None,
-                    lattice: bool = False) -> BatchOutput:
+                    lattice: bool = False, lattice_beam: float | None = None) -> BatchOutput:
         """Decode from host arrays: H2D copies, kernel, D2H results inside one C call."""
         costs = np.ascontiguousarray(costs, dtype=np.float64)
         if costs.ndim == 1:
@@ -262,7 +264,9 @@ class BatchDecoder:
         maxT = int(num_frames.max()) if n else 0
         self.reserve(int(num_frames.sum()) + n, cfg.max_active, maxT, lattice)
         cap = label_capacity or (maxT + 64)
-        ncfg = _native_config(cfg, mode, lattice)
+        if lattice_beam is not None and not lattice_beam >= 0:
+            raise ValueError(f"lattice_beam must be >= 0, got {lattice_beam}")
+        ncfg = _native_config(cfg, mode, lattice, lattice_beam)
         for _attempt in range(16):
             res = np.zeros(n, dtype=N.UTT_RESULT_DTYPE)
             ol = np.zeros((n, cap), dtype=np.int32)
@@ -309,14 +313,69 @@ class BatchDecoder:
             raise N.CapacityError("lattice output pool overflowed")
         return canonical_batch(wfst, meta, nodes, arcs, ac, fin, finw)
 
+    def fetch_pruned_lattices(self, wfst: Wfst, lattice_beam: float,
+                              max_workers: int | None = None, split: bool = True) -> list:
+        """Lattices of the last decode made with ``lattice_beam``: stage one of prune_lattice
+        ran on the device; the path-exact split runs here on host threads.  Each element is
+        a pruned ``Lattice`` or the ``LatticeError`` the reference would raise for it.  With
+        ``split=False`` the stage-one items are returned as (Lattice, cutoff) for the caller
+        to finish with ``lattice.split_lattice``."""
+        import os
+        from concurrent.futures import ThreadPoolExecutor
+        from .lattice import LatticeError, canonical_batch, split_lattice, EMPTY_LATTICE, COST_EPS
+        L = N.load()
+        n = C.c_int32()
+        nn, na, nf = C.c_int64(), C.c_int64(), C.c_int64()
+        N.check(L.wb_lattice_pruned_totals(self._h, C.byref(n), C.byref(nn), C.byref(na),
+                                           C.byref(nf)), "lattice")
+        meta = np.zeros((max(n.value, 1), 8), np.int64)
+        nodes = np.zeros((max(nn.value, 1), 2), np.int32)
+        arcs = np.zeros((max(na.value, 1), 4), np.uint32)
+        ac = np.zeros(max(na.value, 1), np.float64)
+        fin = np.zeros(max(nf.value, 1), np.uint32)
+        finw = np.zeros(max(nf.value, 1), np.float64)
+        N.check(L.wb_lattice_pruned_fetch(self._h, meta.ctypes.data, nodes.ctypes.data,
+                                          arcs.ctypes.data, ac.ctypes.data, fin.ctypes.data,
+                                          finw.ctypes.data), "lattice")
+        meta = meta[:n.value]
+        status = meta[:, 7].copy()
+        if ((meta[:, 0] < 0) | (status == N.WB_ERR_CAPACITY)).any():
+            raise N.CapacityError("lattice output pool overflowed")
+        m6 = meta[:, :6].copy()
+        m6[status != N.WB_OK] = 0
+        stage1 = canonical_batch(wfst, m6, nodes, arcs, ac, fin, finw)
+        best = meta[:, 6].view(np.float64)
+        out = []
+        for u in range(n.value):
+            if status[u] == N.WB_ERR_LATTICE:
+                out.append(LatticeError("epsilon cycle among lattice nodes"))
+            elif stage1[u].start_id is None:
+                out.append(EMPTY_LATTICE)
+            else:   # cutoff = best + lattice_beam + COST_EPS (lattice.py:380)
+                out.append((stage1[u], (float(best[u]) + float(lattice_beam)) + COST_EPS))
+        if not split:
+            return out
+
+        def one(item):
+            if not isinstance(item, tuple):
+                return item
+            try:
+                return split_lattice(*item)
+            except LatticeError as exc:
+                return exc
+        workers = max_workers or len(os.sched_getaffinity(0))
+        with ThreadPoolExecutor(workers) as ex:
+            return list(ex.map(one, out))
+
     # ------------------------------------------------------------------ device buffers
     def decode_device(self, costs, row_offset, num_frames, blank, cfg, mode: str, results,
-                      olabels, ilabels, label_capacity: int, stream=None, lattice: bool = False):
+                      olabels, ilabels, label_capacity: int, stream=None, lattice: bool = False,
+                      lattice_beam: float | None = None):
         """Enqueue a decode on device-resident torch tensors (no host sync besides the
         frame-count read); ``results`` is a uint8 CUDA tensor of n * itemsize bytes.  With
         ``lattice`` the trimmed lattices stay on the device until ``fetch_lattices``."""
         n = int(num_frames.numel())
-        ncfg = _native_config(cfg, mode, lattice)
+        ncfg = _native_config(cfg, mode, lattice, lattice_beam if lattice else None)
         if stream is None:
             import torch
             stream = torch.cuda.current_stream(self.device).cuda_stream

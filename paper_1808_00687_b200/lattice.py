@@ -338,6 +338,22 @@ def prune_lattice(lat: Lattice, lattice_beam: float) -> Lattice:
         N.load().wb_lattice_arrays_free(C.byref(out))
 
 
+def split_lattice(lat: Lattice, cutoff: float) -> Lattice:
+    """The path-exact second stage of prune_lattice (_enforce_path_soundness,
+    lattice.py:430-501) on a lattice already cut at ``cutoff`` (device stage one)."""
+    from . import _native as N
+    if lat.is_empty:
+        return lat if lat.start_id is not None else EMPTY_LATTICE
+    v = lat._view()
+    out = N.LatticeArrays()
+    rc = N.load().wb_lattice_split(C.byref(v), float(cutoff), C.byref(out))
+    try:
+        N.check(rc, "prune_lattice")
+        return Lattice._from_native(out)
+    finally:
+        N.load().wb_lattice_arrays_free(C.byref(out))
+
+
 def prune_lattices(lats, lattice_beam: float, max_workers: int | None = None) -> list:
     """``prune_lattice`` over many lattices on host threads (the C++ pass runs without the
     GIL).  A lattice whose split exceeds the cap yields its ``LatticeError`` in its slot."""
@@ -453,4 +469,5 @@ def load_lattice(path: str) -> Lattice:
 __all__ = ["COST_EPS", "EMPTY_LATTICE", "Lattice", "LatticeArc", "LatticeError", "LatticeNode",
            "LatticeRecorder", "build_lattice", "canonical_batch", "canonical_from_device", "format_lattice_text",
            "lattice_best_path", "load_lattice", "parse_lattice_text", "prune_lattice", "prune_lattices",
+           "split_lattice",
            "save_lattice"]

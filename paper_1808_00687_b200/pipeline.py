@@ -22,20 +22,29 @@ import os
 import threading
 from concurrent.futures import Future, ThreadPoolExecutor
 
-from .lattice import LatticeError, prune_lattice
+from .lattice import LatticeError, prune_lattice, split_lattice
 
 
 class LatticePipeline:
-    def __init__(self, decoder, lattice_beam: float | None = None, workers: int | None = None):
+    def __init__(self, decoder, lattice_beam: float | None = None, workers: int | None = None,
+                 device_prune: bool = True):
         self.decoder = decoder
         self.lattice_beam = lattice_beam
+        # stage one of prune_lattice in the decode launch (prune_kernel); host threads only
+        # run the path-exact split
+        self.device_prune = device_prune and lattice_beam is not None
         n = workers or max(1, len(os.sched_getaffinity(0)) - 1)
         self._gpu = ThreadPoolExecutor(1, thread_name_prefix="wb-decode")
         self._host = ThreadPoolExecutor(n, thread_name_prefix="wb-lattice")
         self._lock = threading.Lock()
 
     def _prune(self, lat):
-        if self.lattice_beam is None:
+        if isinstance(lat, tuple):       # device stage one done: (lattice, cutoff)
+            try:
+                return split_lattice(*lat)
+            except LatticeError as exc:
+                return exc
+        if self.lattice_beam is None or isinstance(lat, LatticeError) or lat.start_id is None:
             return lat
         try:
             return prune_lattice(lat, self.lattice_beam)
@@ -45,9 +54,14 @@ class LatticePipeline:
     def _decode(self, costs, row_offset, num_frames, blank, cfg, mode, fut: Future):
         try:
             dec = self.decoder
-            out = dec.decode_host(costs, row_offset, num_frames, blank, cfg, mode or cfg.mode,
-                                  lattice=True)
-            lats = dec.fetch_lattices(dec.graph.wfst)
+            if self.device_prune:
+                out = dec.decode_host(costs, row_offset, num_frames, blank, cfg, mode or cfg.mode,
+                                      lattice=True, lattice_beam=self.lattice_beam)
+                lats = dec.fetch_pruned_lattices(dec.graph.wfst, self.lattice_beam, split=False)
+            else:
+                out = dec.decode_host(costs, row_offset, num_frames, blank, cfg, mode or cfg.mode,
+                                      lattice=True)
+                lats = dec.fetch_lattices(dec.graph.wfst)
         except BaseException as exc:  # surfaced through the future
             fut.set_exception(exc)
             return

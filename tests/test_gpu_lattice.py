@@ -151,3 +151,59 @@ def test_gpu_lattice_pipeline_matches_direct(cuda):
             except L.LatticeError:
                 want = "error"
             assert ("error" if isinstance(b, L.LatticeError) else _key(b)) == want
+
+
+def test_gpu_device_prune_matches_reference_golden(cuda):
+    """Device lattice-beam pruning (stage one in prune_kernel, the path-exact split on the
+    host) == the reference's prune_lattice on its own built lattice, at every golden beam."""
+    beams = GC.prune_beams()
+    n = 0
+    for case in GC.cases():
+        if not case.pruned:
+            continue
+        g = case.graph.to_wfst()
+        cfg = DecodeConfig(beam=case.cfg.get("beam", INF), max_active=case.cfg.get("max_active"),
+                           mode=case.cfg.get("mode", "lsd"))
+        dec = BatchDecoder(g, 0, max_utts_in_flight=2)
+        T = np.asarray([case.costs.shape[0]], np.int32)
+        costs = case.costs if len(case.costs) else np.zeros((1, case.costs.shape[1]))
+        blank = case.blank if len(case.blank) else np.zeros(1)
+        for b, exp in zip(beams, case.pruned):
+            dec.decode_host(costs, np.zeros(1, np.int64), T, blank, cfg, cfg.mode, lattice=True,
+                            lattice_beam=b)
+            got = dec.fetch_pruned_lattices(g, b)[0]
+            key = "error" if isinstance(got, L.LatticeError) else _key(got)
+            assert key == exp, (case.kind, case.seed, b)
+            n += 1
+    assert n > 200
+
+
+def test_gpu_device_prune_batch_matches_host_prune(cuda):
+    """Many utterances per launch: device-pruned lattices == host prune_lattice of the same
+    device lattices (random graphs with epsilon arcs, several beams)."""
+    from paper_1808_00687_b200.posteriors import cost_table
+    for seed in range(3):
+        g = synth.random_wfst(30 + seed, 400, 1600, 16, eps_fraction=0.08, selfloops=seed == 1,
+                              final_fraction=0.1)
+        posts = [synth.random_posteriors(500 * seed + i, 15 + 4 * i, 16, blank_fraction=0.3)
+                 for i in range(9)]
+        costs = [cost_table(p) for p in posts]
+        blanks = [np.ascontiguousarray(p.rows[:, 0]) for p in posts]
+        T = np.asarray([len(c) for c in costs], np.int32)
+        off = np.zeros(len(T), np.int64)
+        np.cumsum(T[:-1], out=off[1:])
+        C_, B_ = np.concatenate(costs), np.concatenate(blanks)
+        for mode in ("fsd", "lsd"):
+            cfg = DecodeConfig(beam=8.0, max_active=60, mode=mode)
+            dec = BatchDecoder(g, 0, max_utts_in_flight=4)
+            dec.decode_host(C_, off, T, B_, cfg, mode, lattice=True)
+            full = dec.fetch_lattices(g)
+            for lb in (0.5, 3.0, 8.0):
+                dec.decode_host(C_, off, T, B_, cfg, mode, lattice=True, lattice_beam=lb)
+                got = dec.fetch_pruned_lattices(g, lb)
+                for a, b in zip(full, got):
+                    try:
+                        want = _key(L.prune_lattice(a, lb))
+                    except L.LatticeError:
+                        want = "error"
+                    assert ("error" if isinstance(b, L.LatticeError) else _key(b)) == want, (seed, mode, lb)
