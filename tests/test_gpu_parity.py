@@ -111,3 +111,18 @@ def test_capacity_flags_and_targeted_retry(cuda):
     # the Python entry point retries until it fits, with identical results
     got = tiny.decode_host(costs, off, T, blank, cfg, "fsd", label_capacity=1).decode_results()
     assert got == want
+
+
+def test_ctc_lsd_blank_skip_at_scale(cuda):
+    """Config-4 shape at test size: CTC-style graph (self-loops on every state), blank-peaked
+    posteriors (80 % blank frames above the 0.98 threshold), LSD blank skipping."""
+    g = synth.random_wfst(44, 4000, 16000, 200, eps_fraction=0.01, selfloops=True,
+                          final_fraction=0.02)
+    posts = [synth.random_posteriors(900 + k, 400, 200, blank_fraction=0.8) for k in range(10)]
+    cfg = P.DecodeConfig(beam=13.0, max_active=500, mode="lsd")
+    _check_batch(g, posts, cfg)
+    got = P.decode_batch(g, posts, cfg)
+    # blank skipping really happened: steps == non-blank frames (+0 / the dying step)
+    for p, r in zip(posts, got):
+        nonblank = int((p.rows[:, 0] <= cfg.blank_threshold).sum())
+        assert r.search_steps <= nonblank < p.num_frames
