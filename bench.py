@@ -277,11 +277,19 @@ def main():
         return
 
     import torch
+    # WB_BENCH_SAME_DEVICE / WB_BENCH_BACKEND: plumbing test of the multi-rank path on a
+    # one-GPU box (every rank on cuda:0, gloo); never used for reported numbers
+    if os.environ.get("WB_BENCH_SAME_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        backend = os.environ.get("WB_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
 
     import __graft_entry__
     __graft_entry__.build()
@@ -464,7 +472,9 @@ def main():
         value = frames_all * args.steps / (total_ms / 1e3)
         traffic = None
         tfile = os.path.join(ROOT, "profiles", "decode_traffic.json")
-        if os.path.exists(tfile):
+        default_size = (not args.utts and not args.frames and not args.max_active
+                        and not cfg.get("strong"))
+        if os.path.exists(tfile) and default_size:   # measured for the config's own sizes
             try:
                 with open(tfile) as fh:
                     traffic = json.load(fh).get(cfg["name"])
