@@ -44,6 +44,7 @@ extern "C" {
 #define WB_CAP_LATTICE_RAW 16  /* raw lattice pools (lattice_capacity) */
 #define WB_CAP_LATTICE_OUT 32  /* trimmed lattice output pools (lattice_out_capacity) */
 #define WB_CAP_EPS_ROUNDS 64   /* epsilon closure did not converge within 2^20 rounds */
+#define WB_CAP_STREAM 128      /* wb_decode_stream: a cost row was not published within ~60 s */
 #define WB_ERR_NOMEM 6
 
 #define WB_MEM_DEVICE 0    /* all batch pointers are device pointers; the call is asynchronous */
@@ -242,6 +243,22 @@ int wb_lattice_pruned_fetch(wb_decoder_t d, int64_t *meta, int32_t *nodes, uint3
  * read zero-copy (page-locked host memory, one staged row per search step: the transfer
  * overlaps the search and LSD reads only the non-blank rows).  Pageable tables are copied. */
 int wb_last_transfer(wb_decoder_t d, int64_t *h2d_bytes, int32_t *zero_copy);
+
+/*
+ * Streaming host decode: launch a batch whose cost table is still being written.  `costs`
+ * (page-locked, read zero-copy) and `ready` (page-locked int32[n_utts]) are host buffers; the
+ * kernel stages frame f of utterance u only once ready[u] > f, so the caller computes the rows
+ * (frame_costs) while the GPU already searches.  The caller raises each ready[u]
+ * monotonically after the rows below it are written (x86 stores are seen in order), must
+ * eventually set ready[u] = num_frames[u] (for LSD only non-blank rows need real values), and
+ * then calls wb_decode_finish, which copies the results out and synchronises.  `blank` is read
+ * up front (the LSD pre-pass).  Labels land in decoder-owned buffers until wb_decode_finish.
+ */
+int wb_decode_stream(wb_decoder_t d, int32_t n_utts, const double *costs, const int64_t *row_offset,
+                     const int32_t *num_frames, int32_t num_cols, const double *blank,
+                     const wb_config *cfg, int32_t label_capacity, const int32_t *ready,
+                     void *stream);
+int wb_decode_finish(wb_decoder_t d, wb_utt_result *results, int32_t *olabels, int32_t *ilabels);
 
 /* Device time (ms) of the decode kernel of the last wb_decode call (CUDA events on its stream). */
 int wb_last_kernel_ms(wb_decoder_t d, float *ms);

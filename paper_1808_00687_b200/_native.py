@@ -6,8 +6,10 @@ raises -- the product path never silently runs on the CPU.
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import os
+import threading
 
 import numpy as np
 
@@ -17,7 +19,7 @@ LIB_PATH = os.environ.get("WB_LIB") or os.path.join(_HERE, "_lib", "libwfstb200.
 WB_OK, WB_ERR_CUDA, WB_ERR_VALUE, WB_ERR_LATTICE, WB_ERR_WFST, WB_ERR_CAPACITY, WB_ERR_NOMEM = range(7)
 WB_MEM_DEVICE, WB_MEM_HOST = 0, 1
 (WB_CAP_CANDIDATES, WB_CAP_ARENA, WB_CAP_FRAMES, WB_CAP_LABELS, WB_CAP_LATTICE_RAW,
- WB_CAP_LATTICE_OUT, WB_CAP_EPS_ROUNDS) = (1, 2, 4, 8, 16, 32, 64)
+ WB_CAP_LATTICE_OUT, WB_CAP_EPS_ROUNDS, WB_CAP_STREAM) = (1, 2, 4, 8, 16, 32, 64, 128)
 
 
 class NativeError(RuntimeError):
@@ -75,7 +77,7 @@ EXPORTED = ("wb_last_error", "wb_version", "wb_device_count", "wb_graph_create",
             "wb_lattice_totals", "wb_lattice_fetch", "wb_lattice_check", "wb_lattice_prune",
             "wb_lattice_arrays_free", "wb_lattice_best_path", "wb_last_transfer",
             "wb_lattice_canonical", "wb_lattice_pruned_totals", "wb_lattice_pruned_fetch",
-            "wb_lattice_split")
+            "wb_lattice_split", "wb_decode_stream", "wb_decode_finish")
 
 
 def load():
@@ -100,6 +102,10 @@ def load():
                             C.c_void_p, C.POINTER(Config), C.c_void_p, C.c_void_p, C.c_void_p,
                             C.c_int32, C.c_int32, C.c_void_p]
     L.wb_last_kernel_ms.argtypes = [C.c_void_p, C.POINTER(C.c_float)]
+    L.wb_decode_stream.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_int32, C.c_void_p, C.POINTER(Config), C.c_int32,
+                                   C.c_void_p, C.c_void_p]
+    L.wb_decode_finish.argtypes = [C.c_void_p] + [C.c_void_p] * 3
     L.wb_last_transfer.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
     L.wb_lattice_totals.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int64),
                                     C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
@@ -137,6 +143,35 @@ def check(rc: int, what: str = "") -> None:
     if rc == WB_ERR_CAPACITY:
         raise CapacityError(text)
     raise NativeError(text)
+
+
+# ---------------------------------------------------------------- deferred destruction
+# Freeing device memory synchronises the device.  A finalizer that runs while a streaming
+# decode waits for the host to publish cost rows (wb_decode_stream) would deadlock, so handle
+# destruction is queued and done at safe points (before a launch, on workspace re-creation,
+# at exit).  Decoders go before graphs (a decoder refers to its graph).
+_PENDING: list = []
+_PENDING_LOCK = threading.Lock()
+
+
+def defer_destroy(kind: str, handle) -> None:
+    with _PENDING_LOCK:
+        _PENDING.append((kind, handle))
+
+
+def flush_destroy() -> None:
+    with _PENDING_LOCK:
+        items = list(_PENDING)
+        _PENDING.clear()
+    if not items or _lib is None:
+        return
+    for kind in ("wb_decoder_destroy", "wb_graph_destroy"):
+        for k, h in items:
+            if k == kind:
+                getattr(_lib, k)(h)
+
+
+atexit.register(flush_destroy)
 
 
 def device_count() -> int:

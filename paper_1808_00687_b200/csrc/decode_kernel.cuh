@@ -37,6 +37,7 @@ constexpr int GCAP = 1024;           // boundary-bucket members ranked in shared
 constexpr int ROW_SMEM_MAX = 16384;  // cost-row columns staged in shared memory (128 KB)
 constexpr u32 F_SURV = 1u, F_MARK = 2u, CA_NONE = 0xFFFFFFFFu;
 constexpr int MAX_EPS_ROUNDS = 1 << 20;
+constexpr long long STREAM_WAIT_CYCLES = 60ll * 2000000000ll;  // ~60 s at ~2 GHz
 // Capacity failures carry their cause above the status byte (reported as capacity_flags)
 __host__ __device__ constexpr int wb_cap(int cause) { return WB_ERR_CAPACITY | (cause << 8); }
 // relaxations in flight per lane (expand) / gathers per thread (prune): halved for 1024-thread
@@ -115,6 +116,8 @@ struct BatchDev {
     int L1, n;
     int *olab, *ilab;  // [n][lab_cap] best-path labels
     int lab_cap;
+    const int *ready;  // streaming: frames of utterance u whose cost rows the host has written
+                       // (page-locked, mapped); null = all rows present
 };
 
 struct CfgDev {
@@ -131,6 +134,7 @@ struct Smem {
     int n_cand, n_front, overflow, utt, tag_round, ng, thr_bucket, thr_below, n_pend;
     int flag, lat_bad;  // lattice sweeps: change flag / output-pool overflow
     int n_log;          // relaxations logged this step (lattice mode)
+    int ready_seen;     // streaming: last ready count read for the current utterance
     u64 thr_key;
     u32 thr_state;
     u64 arena_base;
@@ -529,7 +533,7 @@ __noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev 
     int which = 0;
     int rounds = 0;
     for (;;) {
-        int n_front = sh.n_front;
+        int n_front = min(sh.n_front, ws.cap);  // overflowed pushes were dropped (flagged)
         __syncthreads();
         if (n_front == 0) break;
         if (++rounds > MAX_EPS_ROUNDS) { status = wb_cap(WB_CAP_EPS_ROUNDS); break; }
@@ -1363,10 +1367,10 @@ __noinline__ __device__ void trim_lattice(int u, int K, int reached, int final_s
 // the lane takes its next utterance; labels are written back to front so they land in path
 // order without a second walk.
 __device__ __noinline__ void backtrace(const GraphDev &g, const u64 *arena, long long best,
-                                       int *ob, int *ib, int cap, int *n_o, int *n_i) {
+                                       u64 used, int *ob, int *ib, int cap, int *n_o, int *n_i) {
     int po = cap, pi = cap, no = 0, ni = 0;
     u32 idx = best < 0 ? ROOT_PREV : (u32)best;
-    while (idx != ROOT_PREV) {
+    while (idx != ROOT_PREV && (u64)idx < used) {  // records point backwards: bounded walk
         const u64 rec = __ldcg(&arena[idx]);
         const u32 a1 = (u32)rec;
         idx = (u32)(rec >> 32);
@@ -1401,7 +1405,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
         const int u = sh.utt;
         if (u >= b.n) break;
         if (threadIdx.x < 8) sh.pc[threadIdx.x] = 0;
-        if (threadIdx.x == 0) { sh.t_mark = clock64(); sh.arena_used = 0; }
+        if (threadIdx.x == 0) { sh.t_mark = clock64(); sh.arena_used = 0; sh.ready_seen = 0; }
         const int T = b.T[u];
         const long long row0 = b.row_off[u];
         int status = WB_OK;
@@ -1459,6 +1463,25 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             const int f = cfg.mode == 1 ? c.frames()[s] : s;
             const double *grow = b.costs + (size_t)(row0 + f) * b.L1;
             const double *row = grow;
+            if (b.ready) {  // streaming input: wait until the host has written row f
+                if (threadIdx.x == 0) {
+                    int seen = sh.ready_seen;
+                    const long long t0 = clock64();
+                    while (seen <= f) {
+                        asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(seen) : "l"(b.ready + u) : "memory");
+                        if (seen <= f) {
+                            __nanosleep(500);
+                            if (clock64() - t0 > STREAM_WAIT_CYCLES) { seen = -1; break; }
+                        }
+                    }
+                    sh.ready_seen = seen;
+                }
+                __syncthreads();
+                if (sh.ready_seen < 0) {  // the host never published this row: give up
+                    status = wb_cap(WB_CAP_STREAM);
+                    break;
+                }
+            }
             if (row_in_smem) {
                 for (int q = threadIdx.x; q < b.L1; q += BLOCK) srow[q] = __ldg(&grow[q]);
                 row = srow;
@@ -1561,8 +1584,9 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             r.final_state = best_t >= 0 ? tinfo[best_t].x : -1;
             r.final_step = died_at < 0 ? steps_run : died_at;
             r.best_trace = best_t >= 0 ? (long long)(u32)tinfo[best_t].y : -1;
-            backtrace(g, c.arena(), r.best_trace, b.olab + (size_t)u * b.lab_cap,
-                      b.ilab + (size_t)u * b.lab_cap, b.lab_cap, &r.n_olabels, &r.n_ilabels);
+            if (status == WB_OK)  // a failed utterance's tokens / arena are not a valid chain
+                backtrace(g, c.arena(), r.best_trace, sh.arena_used, b.olab + (size_t)u * b.lab_cap,
+                          b.ilab + (size_t)u * b.lab_cap, b.lab_cap, &r.n_olabels, &r.n_ilabels);
             int capf = status >> 8;
             if (r.n_olabels > b.lab_cap || r.n_ilabels > b.lab_cap) {
                 capf |= WB_CAP_LABELS;

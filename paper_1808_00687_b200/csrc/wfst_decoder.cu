@@ -103,6 +103,10 @@ struct wb_decoder_s {
     size_t p_fw_n = 0, p_bw_n = 0, p_nflag_n = 0, p_depth_n = 0, p_aflag_n = 0, p_ac_n = 0,
            p_finw_n = 0, p_ctr_n = 0;
     int pruned_n = 0;
+    // the last host-mode launch, for wb_decode_finish
+    int pend_n = 0, pend_label_cap = 0, pend_lcap = 1, pend_cols = 0, pend_lattice = 0;
+    bool pend_zc = false;
+    cudaStream_t pend_stream = nullptr;
     cudaStream_t lat_stream = nullptr;
     size_t lat_bytes = 0;
 };
@@ -418,10 +422,18 @@ int wb_last_kernel_ms(wb_decoder_t d, float *ms) {
     return WB_OK;
 }
 
-int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row_offset,
-              const int32_t *num_frames, int32_t num_cols, const double *blank, const wb_config *cfg,
-              wb_utt_result *results, int32_t *olabels, int32_t *ilabels, int32_t label_cap,
-              int32_t memory_kind, void *stream) {
+}  // extern "C"
+
+static int finish_impl(wb_decoder_t d, wb_utt_result *results, int32_t *olabels, int32_t *ilabels);
+
+// The body of wb_decode / wb_decode_stream.  `ready` (streaming, host mode only): page-locked
+// per-utterance counts of frames whose cost rows are written; `defer` leaves the result copy
+// and the synchronisation to wb_decode_finish.
+static int decode_impl(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row_offset,
+                       const int32_t *num_frames, int32_t num_cols, const double *blank,
+                       const wb_config *cfg, wb_utt_result *results, int32_t *olabels,
+                       int32_t *ilabels, int32_t label_cap, int32_t memory_kind, void *stream,
+                       const int32_t *ready, bool defer) {
     if (!d || !cfg) return set_err(WB_ERR_VALUE, "null argument");
     if (n < 0 || num_cols < 1 || label_cap < 0) return set_err(WB_ERR_VALUE, "bad batch dimensions");
     if (cfg->beam < 0 || std::isnan(cfg->beam)) return set_err(WB_ERR_VALUE, "beam must be >= 0");
@@ -439,6 +451,7 @@ int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row
     const bool host = memory_kind == WB_MEM_HOST;
     bool zc = false;
     const double *zc_ptr = nullptr;
+    const int *ready_dev = nullptr;
     const double *dc = costs, *db = blank;
     const long long *doff = (const long long *)row_offset;
     const int *dT = num_frames;
@@ -478,6 +491,15 @@ int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row
                 zc = true, zc_ptr = (const double *)pa.devicePointer;
             else
                 cudaGetLastError();
+        }
+        if (ready) {
+            cudaPointerAttributes pr;
+            if (!zc || cudaPointerGetAttributes(&pr, ready) != cudaSuccess ||
+                pr.type != cudaMemoryTypeHost || !pr.devicePointer) {
+                cudaGetLastError();
+                return set_err(WB_ERR_VALUE, "streaming decode needs page-locked cost and ready buffers");
+            }
+            ready_dev = (const int *)pr.devicePointer;
         }
         if (ncost && !zc)
             CUDA_TRY(cudaMemcpyAsync(d->h_costs, costs, sizeof(double) * ncost, cudaMemcpyHostToDevice, st));
@@ -532,7 +554,7 @@ int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row
         d->lat_n = n;
         d->lat_stream = st;
     }
-    BatchDev bd{dc, doff, dT, db, num_cols, n, dol, dil, lcap};
+    BatchDev bd{dc, doff, dT, db, num_cols, n, dol, dil, lcap, ready_dev};
     CfgDev cd{cfg->beam, cfg->blank_threshold, cfg->max_active, cfg->mode, cfg->lattice};
     const bool prune = cfg->lattice && cfg->lattice_beam >= 0;
     if (cfg->lattice && !(cfg->lattice_beam < 0) && std::isnan(cfg->lattice_beam))
@@ -551,6 +573,8 @@ int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row
         }
     };
     e = launch();
+    if (e == cudaErrorNotSupported && zc && ready_dev)
+        return set_err(WB_ERR_VALUE, "streaming decode: cost rows too wide to stage in shared memory");
     if (e == cudaErrorNotSupported && zc) {  // rows too wide to stage: copy the table instead
         zc = false;
         long long rows = 0;
@@ -593,22 +617,63 @@ int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row
     if (e != cudaSuccess)
         return set_err(WB_ERR_CUDA, std::string("decode launch: ") + cudaGetErrorString(e));
     CUDA_TRY(cudaEventRecord(d->ev1, st));
-    if (host) {
-        CUDA_TRY(cudaMemcpyAsync(results, dres, sizeof(wb_utt_result) * n, cudaMemcpyDeviceToHost, st));
-        if (label_cap > 0) {
-            CUDA_TRY(cudaMemcpyAsync(olabels, dol, sizeof(int) * (size_t)n * label_cap,
-                                     cudaMemcpyDeviceToHost, st));
-            CUDA_TRY(cudaMemcpyAsync(ilabels, dil, sizeof(int) * (size_t)n * label_cap,
-                                     cudaMemcpyDeviceToHost, st));
-        }
-        CUDA_TRY(cudaStreamSynchronize(st));
-        if (zc) {  // rows the kernel staged from host memory: one per search step (+ lattice)
-            long long steps = 0;
-            for (int i = 0; i < n; ++i) steps += results[i].search_steps;
-            d->last_h2d += steps * (long long)num_cols * (long long)sizeof(double) * (cfg->lattice ? 2 : 1);
-        }
-    }
+    d->pend_n = 0;
+    if (!host) return WB_OK;
+    d->pend_n = n;
+    d->pend_label_cap = label_cap;
+    d->pend_lcap = lcap;
+    d->pend_cols = num_cols;
+    d->pend_lattice = cfg->lattice;
+    d->pend_zc = zc;
+    d->pend_stream = st;
+    if (host && !defer) return finish_impl(d, results, olabels, ilabels);
     return WB_OK;
+}
+
+// Copy a host-mode decode's results out and synchronise (wb_decode; wb_decode_finish).
+static int finish_impl(wb_decoder_t d, wb_utt_result *results, int32_t *olabels, int32_t *ilabels) {
+    const int n = d->pend_n;
+    cudaStream_t st = d->pend_stream;
+    if (n <= 0) return WB_OK;
+    CUDA_TRY(cudaMemcpyAsync(results, d->h_res, sizeof(wb_utt_result) * n, cudaMemcpyDeviceToHost, st));
+    if (d->pend_label_cap > 0) {
+        CUDA_TRY(cudaMemcpyAsync(olabels, d->h_lab, sizeof(int) * (size_t)n * d->pend_label_cap,
+                                 cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(ilabels, d->h_lab + (size_t)n * d->pend_lcap,
+                                 sizeof(int) * (size_t)n * d->pend_label_cap, cudaMemcpyDeviceToHost, st));
+    }
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (d->pend_zc) {  // rows the kernel staged from host memory: one per search step (+ lattice)
+        long long steps = 0;
+        for (int i = 0; i < n; ++i) steps += results[i].search_steps;
+        d->last_h2d += steps * (long long)d->pend_cols * (long long)sizeof(double) * (d->pend_lattice ? 2 : 1);
+    }
+    d->pend_n = 0;
+    return WB_OK;
+}
+
+extern "C" {
+
+int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row_offset,
+              const int32_t *num_frames, int32_t num_cols, const double *blank, const wb_config *cfg,
+              wb_utt_result *results, int32_t *olabels, int32_t *ilabels, int32_t label_cap,
+              int32_t memory_kind, void *stream) {
+    return decode_impl(d, n, costs, row_offset, num_frames, num_cols, blank, cfg, results,
+                       olabels, ilabels, label_cap, memory_kind, stream, nullptr, false);
+}
+
+int wb_decode_stream(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row_offset,
+                     const int32_t *num_frames, int32_t num_cols, const double *blank,
+                     const wb_config *cfg, int32_t label_capacity, const int32_t *ready,
+                     void *stream) {
+    if (!ready) return set_err(WB_ERR_VALUE, "null ready counters");
+    return decode_impl(d, n, costs, row_offset, num_frames, num_cols, blank, cfg, nullptr,
+                       nullptr, nullptr, label_capacity, WB_MEM_HOST, stream, ready, true);
+}
+
+int wb_decode_finish(wb_decoder_t d, wb_utt_result *results, int32_t *olabels, int32_t *ilabels) {
+    if (!d || !results) return set_err(WB_ERR_VALUE, "null argument");
+    return finish_impl(d, results, olabels, ilabels);
 }
 
 int wb_lattice_pruned_totals(wb_decoder_t d, int32_t *n_utts, int64_t *n_nodes, int64_t *n_arcs,

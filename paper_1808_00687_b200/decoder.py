@@ -114,7 +114,7 @@ class DeviceGraph:
         h = C.c_void_p()
         N.check(N.load().wb_graph_create(C.byref(desc), self.device, C.byref(h)), "graph upload")
         self._h = h
-        self._fin = weakref.finalize(self, N.load().wb_graph_destroy, h)
+        self._fin = weakref.finalize(self, N.defer_destroy, "wb_graph_destroy", h)
 
     @property
     def handle(self):
@@ -177,6 +177,7 @@ class BatchDecoder:
     def _create(self):
         if self._h is not None:
             self._fin()
+        N.flush_destroy()
         o = self.opts
         opts = N.DecoderOpts(o["max_utts_in_flight"], o["cand_capacity"], o["arena_capacity"],
                              o["max_frames"], o["block_threads"], o["lattice_capacity"],
@@ -185,7 +186,7 @@ class BatchDecoder:
         N.check(N.load().wb_decoder_create(self.graph.handle, C.byref(opts), C.byref(h)),
                 "decoder workspace")
         self._h = h
-        self._fin = weakref.finalize(self, N.load().wb_decoder_destroy, h)
+        self._fin = weakref.finalize(self, N.defer_destroy, "wb_decoder_destroy", h)
 
     def _grow(self, flags: int, lattice_out_need: int = 0, max_frames: int = 0):
         """Recreate the workspace with the capacities named by ``flags`` (WB_CAP_* bits of
@@ -193,6 +194,8 @@ class BatchDecoder:
         S = self.graph.wfst.num_states
         if flags & N.WB_CAP_EPS_ROUNDS:
             raise N.CapacityError("epsilon closure did not converge (2^20 rounds)")
+        if flags & N.WB_CAP_STREAM:
+            raise N.NativeError("streaming decode: cost rows were not published in time")
         if flags & N.WB_CAP_LATTICE_RAW:
             self.opts["lattice_capacity"] = min(2**31 - 2, 4 * (self.opts["lattice_capacity"] or (1 << 20)))
         if flags & N.WB_CAP_LATTICE_OUT:
@@ -291,6 +294,103 @@ class BatchDecoder:
                     need = max(nn.value, na.value, nf.value)
                 self._grow(flags, lattice_out_need=need, max_frames=maxT)
         raise N.CapacityError("decode workspace kept overflowing")
+
+    # ------------------------------------------------------------------ posteriors in (e2e)
+    def _pinned(self, name: str, shape, dtype):
+        """Grow-only page-locked host buffers owned by the decoder (torch is plumbing)."""
+        import torch
+        n = int(np.prod(shape))
+        buf = getattr(self, name, None)
+        if buf is None or buf.numel() < n:
+            tdt = {np.float64: torch.float64, np.int32: torch.int32}[dtype]
+            buf = torch.empty(max(n, 1), dtype=tdt, pin_memory=True)
+            setattr(self, name, buf)
+        return buf.numpy()[:n].reshape(shape)
+
+    def decode_posteriors(self, posts_list, cfg, mode: str | None = None,
+                          label_capacity: int | None = None, lattice: bool = False,
+                          lattice_beam: float | None = None, block_frames: int = 32,
+                          workers: int | None = None) -> BatchOutput:
+        """Decode from posterior matrices (the public path): host threads compute the
+        frame_costs rows straight into a page-locked table in frame-block order while the
+        kernel already searches, reading each row zero-copy once its block is published
+        (``wb_decode_stream``).  LSD computes only the non-blank rows (select_frames,
+        posteriors.py:109-110).  Bit-identical to ``decode_host`` on ``cost_table``."""
+        import os
+        import threading
+        from concurrent.futures import ThreadPoolExecutor
+        from .posteriors import cost_rows
+        mode = mode or cfg.mode
+        posts_list = list(posts_list)
+        n = len(posts_list)
+        if n == 0:
+            return BatchOutput(np.zeros(0, dtype=N.UTT_RESULT_DTYPE), np.zeros((0, 1), np.int32),
+                               np.zeros((0, 1), np.int32), 1)
+        L1 = posts_list[0].rows.shape[1]
+        T = np.asarray([p.num_frames for p in posts_list], np.int32)
+        off = np.zeros(n, np.int64)
+        np.cumsum(T[:-1], out=off[1:])
+        R = max(int(T.sum()), 1)
+        costs = self._pinned("_pin_costs", (R, L1), np.float64)
+        ready = self._pinned("_pin_ready", (n,), np.int32)
+        ready[:] = 0
+        blank = np.zeros(R, np.float64)
+        for p, o, t in zip(posts_list, off, T):
+            blank[o:o + t] = p.rows[:, p.blank_col]
+        maxT = int(T.max())
+        self.reserve(int(T.sum()) + n, cfg.max_active, maxT, lattice)
+        cap = label_capacity or (maxT + 64)
+        if lattice_beam is not None and not lattice_beam >= 0:
+            raise ValueError(f"lattice_beam must be >= 0, got {lattice_beam}")
+        ncfg = _native_config(cfg, mode, lattice, lattice_beam)
+        self._last_max_active = cfg.max_active
+        N.flush_destroy()   # nothing may free device memory while the kernel waits on us
+        # rows each utterance needs: all frames (FSD) or the non-blank ones (LSD)
+        need = []
+        for p in posts_list:
+            if mode == "lsd":
+                need.append(np.flatnonzero(~(p.rows[:, p.blank_col] > cfg.blank_threshold)))
+            else:
+                need.append(None)
+        N.check(N.load().wb_decode_stream(self._h, n, costs.ctypes.data, off.ctypes.data,
+                                          T.ctypes.data, L1, blank.ctypes.data, C.byref(ncfg),
+                                          cap, ready.ctypes.data, None), "decode")
+        # producers: frame blocks in block-major order, each utterance's ready count advanced
+        # over its contiguous finished prefix
+        lock = threading.Lock()
+        done = [dict() for _ in range(n)]
+        nxt = [0] * n
+        nblk = [(int(t) + block_frames - 1) // block_frames for t in T]
+
+        def work(u, b):
+            lo, hi = b * block_frames, min(int(T[u]), (b + 1) * block_frames)
+            view = costs[off[u]:off[u] + T[u]]
+            if need[u] is None:
+                cost_rows(posts_list[u], np.arange(lo, hi), view, cfg.acoustic_scale)
+            else:
+                sel = need[u][(need[u] >= lo) & (need[u] < hi)]
+                if len(sel):
+                    cost_rows(posts_list[u], sel, view, cfg.acoustic_scale)
+            with lock:
+                done[u][b] = hi
+                while nxt[u] in done[u]:
+                    ready[u] = done[u].pop(nxt[u])
+                    nxt[u] += 1
+        tasks = [(u, b) for b in range(max(nblk)) for u in range(n) if b < nblk[u]]
+        nw = workers or min(8, len(os.sched_getaffinity(0)))
+        try:
+            with ThreadPoolExecutor(nw) as ex:
+                list(ex.map(lambda ub: work(*ub), tasks))
+        finally:
+            ready[:] = T      # every row is written (or the kernel must not wait forever)
+        res = np.zeros(n, dtype=N.UTT_RESULT_DTYPE)
+        ol = np.zeros((n, cap), dtype=np.int32)
+        il = np.zeros((n, cap), dtype=np.int32)
+        N.check(N.load().wb_decode_finish(self._h, res.ctypes.data, ol.ctypes.data,
+                                          il.ctypes.data), "decode")
+        if (res["status"] != N.WB_OK).any():   # capacity: rerun on the finished table
+            return self.decode_host(costs, off, T, blank, cfg, mode, cap, lattice, lattice_beam)
+        return BatchOutput(res, ol, il, cap)
 
     def fetch_lattices(self, wfst: Wfst) -> list:
         """Trimmed lattices of the last lattice-mode decode, canonically ordered."""
@@ -425,24 +525,14 @@ def decode_batch(wfst, posts_list, cfg: DecodeConfig, mode: str | None = None,
     L1s = {p.rows.shape[1] for p in posts_list}
     if len(L1s) != 1:
         raise ValueError("all posterior matrices of a batch must share the label alphabet")
-    L1 = L1s.pop()
-    T = np.asarray([p.num_frames for p in posts_list], dtype=np.int32)
-    off = np.zeros(len(T), dtype=np.int64)
-    np.cumsum(T[:-1], out=off[1:])
-    R = int(T.sum())
-    costs = np.empty((max(R, 1), L1), dtype=np.float64)
-    blank = np.empty(max(R, 1), dtype=np.float64)
-    for p, o, t in zip(posts_list, off, T):
-        if t:
-            cost_table(p, cfg.acoustic_scale, out=costs[o:o + t])
-            blank[o:o + t] = p.rows[:, p.blank_col]
     recorders = None
     if recorder is not None:
         recorders = list(recorder) if isinstance(recorder, (list, tuple)) else [recorder]
         if len(recorders) != len(posts_list):
             raise ValueError("pass one LatticeRecorder per utterance")
     dec = _decoder_for(w)
-    out = dec.decode_host(costs, off, T, blank, cfg, mode, lattice=recorders is not None)
+    # cost rows are computed on host threads while the kernel already decodes (streaming)
+    out = dec.decode_posteriors(posts_list, cfg, mode, lattice=recorders is not None)
     results = out.decode_results()
     if recorders is not None:
         lats = dec.fetch_lattices(w)

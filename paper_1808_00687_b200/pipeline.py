@@ -65,6 +65,9 @@ class LatticePipeline:
         except BaseException as exc:  # surfaced through the future
             fut.set_exception(exc)
             return
+        self._finish_batch(out, lats, fut)
+
+    def _finish_batch(self, out, lats, fut: Future):
         parts = [self._host.submit(self._prune, lat) for lat in lats]
 
         def finish(_):
@@ -76,6 +79,27 @@ class LatticePipeline:
             fut.set_result((out, []))
         for p in parts:
             p.add_done_callback(finish)
+
+    def _decode_posts(self, posts, cfg, mode, fut: Future):
+        try:
+            dec = self.decoder
+            if self.device_prune:
+                out = dec.decode_posteriors(posts, cfg, mode or cfg.mode, lattice=True,
+                                            lattice_beam=self.lattice_beam)
+                lats = dec.fetch_pruned_lattices(dec.graph.wfst, self.lattice_beam, split=False)
+            else:
+                out = dec.decode_posteriors(posts, cfg, mode or cfg.mode, lattice=True)
+                lats = dec.fetch_lattices(dec.graph.wfst)
+        except BaseException as exc:  # surfaced through the future
+            fut.set_exception(exc)
+            return
+        self._finish_batch(out, lats, fut)
+
+    def submit_posteriors(self, posts, cfg, mode: str | None = None) -> Future:
+        """Queue one batch given as posterior matrices (``decode_posteriors``)."""
+        fut: Future = Future()
+        self._gpu.submit(self._decode_posts, list(posts), cfg, mode, fut)
+        return fut
 
     def submit(self, costs, row_offset, num_frames, blank, cfg, mode: str | None = None) -> Future:
         """Queue one batch; the future yields (BatchOutput, lattices)."""

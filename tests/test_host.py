@@ -141,3 +141,20 @@ def test_reference_graph_conversion_roundtrip():
     g = as_wfst(w)
     assert as_wfst(w) is g
     assert g.arc_offsets == w.arc_offsets and g.eps_split == w.eps_split
+
+
+def test_cost_rows_is_bit_identical_to_cost_table():
+    """The streaming producer's in-place row runs == cost_table == frame_costs arithmetic."""
+    import numpy as np
+    from paper_1808_00687_b200 import synth
+    from paper_1808_00687_b200.posteriors import PosteriorMatrix, cost_rows, cost_table
+    for bc in (0, 3):
+        rows = synth.random_posterior_rows(5, 200, 40, blank_fraction=0.5, blank_col=bc)
+        p = PosteriorMatrix(rows, bc, validate=False)
+        ref = cost_table(p, 0.7)
+        out = np.full_like(ref, 123.0)
+        idx = np.sort(np.random.default_rng(1).choice(200, 90, replace=False))
+        cost_rows(p, idx, out, 0.7)
+        assert np.array_equal(out[idx], ref[idx])
+        assert (np.signbit(out[idx]) == np.signbit(ref[idx])).all()
+        assert (out[np.setdiff1d(np.arange(200), idx)] == 123.0).all()
