@@ -534,8 +534,12 @@ __noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev 
     int rounds = 0;
     for (;;) {
         int n_front = min(sh.n_front, ws.cap);  // overflowed pushes were dropped (flagged)
+        const int ovf = sh.overflow;
         __syncthreads();
         if (n_front == 0) break;
+        // a candidate overflow leaves frontier states without a candidate index: the step
+        // has failed (WB_CAP_CANDIDATES), stop before following stale indices
+        if (ovf) { status = wb_cap(WB_CAP_CANDIDATES); break; }
         if (++rounds > MAX_EPS_ROUNDS) { status = wb_cap(WB_CAP_EPS_ROUNDS); break; }
         if (threadIdx.x == 0) {
             sh.n_front = 0;
@@ -555,7 +559,7 @@ __noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev 
             if (i < n_front) {
                 uu = fin[i];
                 Slot us = ld_slot(&slot[uu]);
-                ui = c.cand_of()[uu];
+                ui = min(c.cand_of()[uu], (u32)ws.cap - 1u);
                 int4 rg = c.cand_rng()[ui];
                 lo = rg.x;
                 deg = rg.y - rg.x;

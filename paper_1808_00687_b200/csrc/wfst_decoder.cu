@@ -377,6 +377,7 @@ int wb_decoder_create(wb_graph_t g, const wb_decoder_opts *o, wb_decoder_t *out)
 #undef DA
     if (e == cudaSuccess) e = cudaMemset(d->slot, 0xFF, sizeof(Slot) * slots * S);
     if (e == cudaSuccess && g->has_eps) e = cudaMemset(d->qtag, 0, sizeof(u32) * slots * S);
+    if (e == cudaSuccess && g->has_eps) e = cudaMemset(d->cand_of, 0, sizeof(u32) * slots * S);
     if (e == cudaSuccess) e = cudaMemset(d->tag_ctr, 0, sizeof(u32) * slots);
     if (e == cudaSuccess) e = cudaEventCreate(&d->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&d->ev1);
