@@ -1526,6 +1526,14 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             cur ^= 1;
             n_live = so.n_surv;
         }
+        if (status != WB_OK) {
+            // a failed step may leave slots beyond the candidate capacity dirty: restore the
+            // lane's whole slot array so later utterances on this lane start clean
+            __syncthreads();
+            Slot *sl = c.slot();
+            for (long long q = threadIdx.x; q < ws.S; q += BLOCK) st_slot_empty(&sl[q]);
+            __syncthreads();
+        }
         // ---- final transition / death fallback (decoder.py:252-273, 327-333)
         const int4 *tinfo = c.tok_info(cur);
         const double *tcost = c.tok_cost(cur);
