@@ -47,6 +47,8 @@ extern "C" {
 #define WB_CAP_STREAM 128      /* wb_decode_stream: a cost row was not published within ~60 s */
 #define WB_ERR_NOMEM 6
 
+#define WB_PARSE_FALLBACK 7 /* wb_wfst_parse_text: text needs the full (Python) parser */
+
 #define WB_MEM_DEVICE 0    /* all batch pointers are device pointers; the call is asynchronous */
 #define WB_MEM_HOST 1      /* all batch pointers are host pointers; the call copies and syncs */
 
@@ -259,6 +261,25 @@ int wb_decode_stream(wb_decoder_t d, int32_t n_utts, const double *costs, const 
                      const wb_config *cfg, int32_t label_capacity, const int32_t *ready,
                      void *stream);
 int wb_decode_finish(wb_decoder_t d, wb_utt_result *results, int32_t *olabels, int32_t *ilabels);
+
+/*
+ * parse_wfst_text fast path (wfst.py:315-378) for ASCII AT&T text with integer labels: arcs in
+ * file order, finals in first-mention order (last weight wins), start = first state
+ * mentioned.  Returns WB_PARSE_FALLBACK for anything it does not reproduce exactly (symbols,
+ * non-ASCII, Python numeric extras, malformed lines) -- the caller then runs the full parser.
+ * Arrays are owned by the caller: wb_parsed_wfst_free.
+ */
+typedef struct {
+    int32_t num_states, start;
+    int64_t num_arcs, num_finals;
+    int32_t *src, *dst, *ilabel, *olabel;
+    double *weight;
+    int32_t *final_state;
+    double *final_weight;
+} wb_parsed_wfst;
+int wb_wfst_parse_text(const char *text, int64_t len, int32_t allow_negative_weights,
+                       wb_parsed_wfst *out);
+void wb_parsed_wfst_free(wb_parsed_wfst *p);
 
 /* Device time (ms) of the decode kernel of the last wb_decode call (CUDA events on its stream). */
 int wb_last_kernel_ms(wb_decoder_t d, float *ms);

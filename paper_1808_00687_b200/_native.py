@@ -17,6 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("WB_LIB") or os.path.join(_HERE, "_lib", "libwfstb200.so")
 
 WB_OK, WB_ERR_CUDA, WB_ERR_VALUE, WB_ERR_LATTICE, WB_ERR_WFST, WB_ERR_CAPACITY, WB_ERR_NOMEM = range(7)
+WB_PARSE_FALLBACK = 7
 WB_MEM_DEVICE, WB_MEM_HOST = 0, 1
 (WB_CAP_CANDIDATES, WB_CAP_ARENA, WB_CAP_FRAMES, WB_CAP_LABELS, WB_CAP_LATTICE_RAW,
  WB_CAP_LATTICE_OUT, WB_CAP_EPS_ROUNDS, WB_CAP_STREAM) = (1, 2, 4, 8, 16, 32, 64, 128)
@@ -51,6 +52,13 @@ class DecoderOpts(C.Structure):
                 ("hash_entries", C.c_int64), ("lattice_out_capacity", C.c_int64)]
 
 
+class ParsedWfst(C.Structure):
+    _fields_ = [("num_states", C.c_int32), ("start", C.c_int32), ("num_arcs", C.c_int64),
+                ("num_finals", C.c_int64), ("src", C.c_void_p), ("dst", C.c_void_p),
+                ("ilabel", C.c_void_p), ("olabel", C.c_void_p), ("weight", C.c_void_p),
+                ("final_state", C.c_void_p), ("final_weight", C.c_void_p)]
+
+
 class LatticeArrays(C.Structure):
     _fields_ = [("n_nodes", C.c_int64), ("n_arcs", C.c_int64), ("n_finals", C.c_int64),
                 ("node_state", C.c_void_p), ("node_step", C.c_void_p), ("arc_from", C.c_void_p),
@@ -77,7 +85,8 @@ EXPORTED = ("wb_last_error", "wb_version", "wb_device_count", "wb_graph_create",
             "wb_lattice_totals", "wb_lattice_fetch", "wb_lattice_check", "wb_lattice_prune",
             "wb_lattice_arrays_free", "wb_lattice_best_path", "wb_last_transfer",
             "wb_lattice_canonical", "wb_lattice_pruned_totals", "wb_lattice_pruned_fetch",
-            "wb_lattice_split", "wb_decode_stream", "wb_decode_finish")
+            "wb_lattice_split", "wb_decode_stream", "wb_decode_finish", "wb_wfst_parse_text",
+            "wb_parsed_wfst_free")
 
 
 def load():
@@ -106,6 +115,9 @@ def load():
                                    C.c_int32, C.c_void_p, C.POINTER(Config), C.c_int32,
                                    C.c_void_p, C.c_void_p]
     L.wb_decode_finish.argtypes = [C.c_void_p] + [C.c_void_p] * 3
+    L.wb_wfst_parse_text.argtypes = [C.c_char_p, C.c_int64, C.c_int32, C.POINTER(ParsedWfst)]
+    L.wb_parsed_wfst_free.argtypes = [C.POINTER(ParsedWfst)]
+    L.wb_parsed_wfst_free.restype = None
     L.wb_last_transfer.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
     L.wb_lattice_totals.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int64),
                                     C.POINTER(C.c_int64), C.POINTER(C.c_int64)]

@@ -16,6 +16,7 @@ The same arrays are what ``DeviceGraph`` uploads to the GPU.
 """
 from __future__ import annotations
 
+import ctypes as C
 import math
 from dataclasses import dataclass
 
@@ -322,12 +323,47 @@ def _find_cycle(succ: dict[int, list[int]], num_states: int):
     return None
 
 
+def _parse_fast(text: str, allow_negative_weights: bool):
+    """The C++ fast path (csrc/wfst_text.cpp); None when the text needs this module's parser
+    (symbols, non-ASCII, malformed lines -- which then raise exactly as the reference)."""
+    try:
+        from . import _native as N
+        L = N.load()
+    except Exception:   # library not built: the Python parser is exact, only slower
+        return None
+    data = text.encode("ascii", errors="replace") if text.isascii() else None
+    if data is None:
+        return None
+    out = N.ParsedWfst()
+    rc = L.wb_wfst_parse_text(data, len(data), int(bool(allow_negative_weights)), C.byref(out))
+    if rc != N.WB_OK:
+        return None
+    try:
+        def arr(ptr, n, t):
+            if n == 0:
+                return np.zeros(0, t)
+            ct = np.ctypeslib.as_ctypes_type(t)
+            return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ct)), shape=(n,)).copy()
+        na, nfin = out.num_arcs, out.num_finals
+        fw = np.full(out.num_states, np.inf)
+        fw[arr(out.final_state, nfin, np.int32)] = arr(out.final_weight, nfin, np.float64)
+        return Wfst.from_arrays(out.num_states, out.start, arr(out.src, na, np.int32),
+                                arr(out.dst, na, np.int32), arr(out.ilabel, na, np.int32),
+                                arr(out.olabel, na, np.int32), arr(out.weight, na, np.float64),
+                                fw)
+    finally:
+        L.wb_parsed_wfst_free(C.byref(out))
+
+
 def parse_wfst_text(text: str, allow_negative_weights: bool = False) -> Wfst:
     """AT&T-style text with integer labels (wfst.py:315-378, symbol tables not supported).
 
     Arc lines ``src dst ilabel olabel [weight]``, final lines ``state [weight]``; the first
     state mentioned is the start state.
     """
+    fast = _parse_fast(text, allow_negative_weights)
+    if fast is not None:
+        return fast
     arcs: list[Arc] = []
     finals: dict[int, float] = {}
     start = None

@@ -158,3 +158,73 @@ def test_cost_rows_is_bit_identical_to_cost_table():
         assert np.array_equal(out[idx], ref[idx])
         assert (np.signbit(out[idx]) == np.signbit(ref[idx])).all()
         assert (out[np.setdiff1d(np.arange(200), idx)] == 123.0).all()
+
+
+def _wfst_key(w):
+    import numpy as np
+    return (w.num_states, w.start, w.row_ptr.tolist(), w.eps_end.tolist(), w.dst.tolist(),
+            w.ilabel.tolist(), w.olabel.tolist(), w.weight.tolist(),
+            np.where(np.isinf(w.final_w), -1.0, w.final_w).tolist())
+
+
+def _texts():
+    import numpy as np
+    rng = np.random.default_rng(3)
+    out = []
+    for k in range(30):
+        S = int(rng.integers(1, 40))
+        lines = []
+        for _ in range(int(rng.integers(0, 120))):
+            a, b = rng.integers(0, S, 2)
+            i, o = rng.integers(0, 6, 2)
+            w = float(np.round(rng.uniform(0, 3), int(rng.integers(0, 8))))
+            form = rng.integers(0, 4)
+            lines.append(f"{a} {b} {i} {o}" if form == 0 else
+                         f"{a}\t{b}  {i} {o} {w!r}" if form == 1 else
+                         f"  {a} {b} {i} {o} {w:.3e}  " if form == 2 else f"{a} {b} {i} {o} {w}")
+            if rng.random() < 0.1:
+                lines.append("# comment")
+            if rng.random() < 0.1:
+                lines.append("")
+        for s in rng.integers(0, S, int(rng.integers(1, 4))):
+            lines.append(f"{s} {float(rng.uniform(0, 2))!r}" if rng.random() < 0.7 else f"{s}")
+        if rng.random() < 0.3:
+            lines.insert(0, f"{int(rng.integers(0, S))} inf")
+        sep = "\r\n" if k % 5 == 0 else "\n"
+        out.append(sep.join(lines) + (sep if k % 2 else ""))
+    return out
+
+
+def test_native_wfst_parser_matches_python_parser():
+    """The C++ fast path (csrc/wfst_text.cpp) builds the same Wfst as the Python parser; a
+    non-ASCII comment forces the Python path on the same content."""
+    from paper_1808_00687_b200 import wfst as W
+    for t in _texts():
+        fast = W._parse_fast(t, False)
+        assert fast is not None
+        slow = parse_wfst_text(t + "\n# é\n")
+        assert _wfst_key(fast) == _wfst_key(slow)
+
+
+def test_native_wfst_parser_falls_back_exactly():
+    """Malformed / unusual text goes to the Python parser, which raises like the reference."""
+    from paper_1808_00687_b200 import wfst as W
+    from paper_1808_00687_b200.wfst import ParseError
+    for bad in ("0 1 2\n", "0 1 a b\n", "0 1 2 3 nan\n", "0 1 2 3 -1\n", "", "# only\n",
+                "0 1 2 3 0x1p3\n", "-1 2 3 4\n"):
+        assert W._parse_fast(bad, False) is None
+        with pytest.raises((ParseError, ValueError)):
+            parse_wfst_text(bad)
+    assert W._parse_fast("0 1 2 3 1_0\n", False) is None        # Python's float accepts it
+    assert parse_wfst_text("0 1 2 3 1_0\n").weight.tolist() == [10.0]
+    ok = W._parse_fast("0 1 2 3 -1.5\n1\n", True)
+    assert ok is not None and ok.weight.tolist() == [-1.5]
+
+
+@needs_ref
+def test_native_wfst_parser_matches_reference():
+    L = refutil.ref()
+    for t in _texts()[:10]:
+        mine = parse_wfst_text(t)
+        ref = L.wfst.parse_wfst_text(t)
+        assert _wfst_key(mine) == _wfst_key(Wfst.from_reference(ref))
