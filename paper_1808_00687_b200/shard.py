@@ -59,4 +59,41 @@ def decode_sharded(wfst, posts_list, cfg, *, rank: int | None = None, world: int
     return out
 
 
-__all__ = ["decode_sharded", "shard_utterances"]
+def decode_multi_device(wfst, posts_list, cfg, devices, mode: str | None = None) -> list:
+    """One process, one host thread per device: utterances are balanced over
+    ``devices`` by frame count, each thread drives its own graph replica and decoder through
+    the C ABI (ctypes releases the GIL, so the devices run concurrently), results come back
+    in input order.  A device may be listed twice (two decoders share it)."""
+    import threading
+    import torch
+    from .decoder import BatchDecoder, as_wfst
+    w = as_wfst(wfst)
+    posts_list = list(posts_list)
+    devices = list(devices)
+    shards = shard_utterances([p.num_frames for p in posts_list], len(devices))
+    out: list = [None] * len(posts_list)
+    errors: list = []
+
+    def run(k, dev):
+        try:
+            torch.cuda.set_device(dev)
+            if not shards[k]:
+                return
+            dec = BatchDecoder(w, dev)
+            res = dec.decode_posteriors([posts_list[i] for i in shards[k]], cfg,
+                                        mode or cfg.mode).decode_results()
+            for i, r in zip(shards[k], res):
+                out[i] = r
+        except BaseException as exc:  # re-raised in the caller
+            errors.append(exc)
+    threads = [threading.Thread(target=run, args=(k, d)) for k, d in enumerate(devices)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
+    return out
+
+
+__all__ = ["decode_multi_device", "decode_sharded", "shard_utterances"]

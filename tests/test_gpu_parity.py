@@ -150,3 +150,15 @@ def test_streaming_posteriors_equal_cost_table_path(cuda, mode):
     assert got == want
     h2d, zc = dec.last_transfer()
     assert zc
+
+
+def test_multi_device_threads_equal_single_batch(cuda):
+    """decode_multi_device (one host thread + decoder per device entry; here both entries
+    are cuda:0, so two decoders run concurrently on one GPU) == one decode_batch."""
+    from paper_1808_00687_b200.shard import decode_multi_device
+    g = synth.random_wfst(17, 2000, 7000, 30, eps_fraction=0.05, final_fraction=0.1)
+    posts = [synth.random_posteriors(800 + k, 40 + 9 * k, 30) for k in range(11)]
+    cfg = P.DecodeConfig(beam=9.0, max_active=100, mode="fsd")
+    want = P.decode_batch(g, posts, cfg)
+    got = decode_multi_device(g, posts, cfg, devices=[0, 0])
+    assert got == want
