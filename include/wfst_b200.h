@@ -259,7 +259,13 @@ int wb_last_transfer(wb_decoder_t d, int64_t *h2d_bytes, int32_t *zero_copy);
 int wb_decode_stream(wb_decoder_t d, int32_t n_utts, const double *costs, const int64_t *row_offset,
                      const int32_t *num_frames, int32_t num_cols, const double *blank,
                      const wb_config *cfg, int32_t label_capacity, const int32_t *ready,
-                     void *stream);
+                     const int64_t *step_row_offset, void *stream);
+/* LSD with step_row_offset (host, page-locked not required): `costs` holds only the searched
+ * (non-blank) frames, utterance u's search step s at row step_row_offset[u] + s, and ready[u]
+ * counts such rows.  wb_gather_rows copies rows idx[i] (columns col0.., ncols) of a row-major
+ * matrix into dst rows i (from column dst_col0): the producer's row compaction. */
+void wb_gather_rows(const double *src, int64_t src_ld, const int32_t *idx, int64_t n, int32_t col0,
+                    int32_t ncols, double *dst, int64_t dst_ld, int32_t dst_col0);
 int wb_decode_finish(wb_decoder_t d, wb_utt_result *results, int32_t *olabels, int32_t *ilabels);
 
 /*

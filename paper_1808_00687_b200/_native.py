@@ -86,7 +86,7 @@ EXPORTED = ("wb_last_error", "wb_version", "wb_device_count", "wb_graph_create",
             "wb_lattice_arrays_free", "wb_lattice_best_path", "wb_last_transfer",
             "wb_lattice_canonical", "wb_lattice_pruned_totals", "wb_lattice_pruned_fetch",
             "wb_lattice_split", "wb_decode_stream", "wb_decode_finish", "wb_wfst_parse_text",
-            "wb_parsed_wfst_free")
+            "wb_parsed_wfst_free", "wb_gather_rows")
 
 
 def load():
@@ -113,7 +113,10 @@ def load():
     L.wb_last_kernel_ms.argtypes = [C.c_void_p, C.POINTER(C.c_float)]
     L.wb_decode_stream.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_int32, C.c_void_p, C.POINTER(Config), C.c_int32,
-                                   C.c_void_p, C.c_void_p]
+                                   C.c_void_p, C.c_void_p, C.c_void_p]
+    L.wb_gather_rows.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32,
+                                 C.c_int32, C.c_void_p, C.c_int64, C.c_int32]
+    L.wb_gather_rows.restype = None
     L.wb_decode_finish.argtypes = [C.c_void_p] + [C.c_void_p] * 3
     L.wb_wfst_parse_text.argtypes = [C.c_char_p, C.c_int64, C.c_int32, C.POINTER(ParsedWfst)]
     L.wb_parsed_wfst_free.argtypes = [C.POINTER(ParsedWfst)]

@@ -118,6 +118,8 @@ struct BatchDev {
     int lab_cap;
     const int *ready;  // streaming: frames of utterance u whose cost rows the host has written
                        // (page-locked, mapped); null = all rows present
+    const long long *crow_off;  // streaming LSD: rows hold only the searched (non-blank) frames,
+                                // utterance u's step s at row crow_off[u] + s; null = by frame
 };
 
 struct CfgDev {
@@ -1465,15 +1467,16 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
         long long expanded = 0;
         for (int s = 0; s < nf && status == WB_OK; ++s) {
             const int f = cfg.mode == 1 ? c.frames()[s] : s;
-            const double *grow = b.costs + (size_t)(row0 + f) * b.L1;
+            const int ridx = b.crow_off ? s : f;  // compacted rows are indexed by search step
+            const double *grow = b.costs + (size_t)((b.crow_off ? b.crow_off[u] : row0) + ridx) * b.L1;
             const double *row = grow;
-            if (b.ready) {  // streaming input: wait until the host has written row f
+            if (b.ready) {  // streaming input: wait until the host has written row ridx
                 if (threadIdx.x == 0) {
                     int seen = sh.ready_seen;
                     const long long t0 = clock64();
-                    while (seen <= f) {
+                    while (seen <= ridx) {
                         asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(seen) : "l"(b.ready + u) : "memory");
-                        if (seen <= f) {
+                        if (seen <= ridx) {
                             __nanosleep(500);
                             if (clock64() - t0 > STREAM_WAIT_CYCLES) { seen = -1; break; }
                         }

@@ -60,7 +60,8 @@ struct wb_decoder_s {
     // host-mode staging buffers (grown on demand)
     double *h_costs = nullptr, *h_blank = nullptr;
     size_t h_costs_n = 0, h_blank_n = 0;
-    long long *h_off = nullptr;
+    long long *h_off = nullptr, *h_crow = nullptr;
+    size_t h_crow_n = 0;
     int *h_T = nullptr;
     wb_utt_result *h_res = nullptr;
     int *h_lab = nullptr;
@@ -198,7 +199,7 @@ static void free_decoder(wb_decoder_s *d) {
     void *ptrs[] = {d->slot, d->cand_of, d->qtag, d->tag_ctr, d->cand_state, d->cand_rng,
                     d->cand_arc, d->cand_pay, d->cand_key, d->cand_ca, d->front, d->tok_info,
                     d->tok_cost, d->frames, d->arena, d->counters, d->h_costs, d->h_blank,
-                    d->h_off, d->h_T, d->h_res, d->h_lab, d->tok_eps, d->sbits, d->snode,
+                    d->h_off, d->h_crow, d->h_T, d->h_res, d->h_lab, d->tok_eps, d->sbits, d->snode,
                     d->ln_state, d->ln_out, d->ln_flag, d->la_src, d->la_dst, d->la_arc,
                     d->la_ac, d->lstep, d->lstep_eps, d->lstep_start, d->o_node, d->o_arc,
                     d->o_ac, d->o_finw, d->o_fin, d->o_ctr, d->o_meta, d->rlog, d->p_node,
@@ -434,7 +435,7 @@ static int decode_impl(wb_decoder_t d, int32_t n, const double *costs, const int
                        const int32_t *num_frames, int32_t num_cols, const double *blank,
                        const wb_config *cfg, wb_utt_result *results, int32_t *olabels,
                        int32_t *ilabels, int32_t label_cap, int32_t memory_kind, void *stream,
-                       const int32_t *ready, bool defer) {
+                       const int32_t *ready, bool defer, const int64_t *crow = nullptr) {
     if (!d || !cfg) return set_err(WB_ERR_VALUE, "null argument");
     if (n < 0 || num_cols < 1 || label_cap < 0) return set_err(WB_ERR_VALUE, "bad batch dimensions");
     if (cfg->beam < 0 || std::isnan(cfg->beam)) return set_err(WB_ERR_VALUE, "beam must be >= 0");
@@ -555,7 +556,14 @@ static int decode_impl(wb_decoder_t d, int32_t n, const double *costs, const int
         d->lat_n = n;
         d->lat_stream = st;
     }
-    BatchDev bd{dc, doff, dT, db, num_cols, n, dol, dil, lcap, ready_dev};
+    const long long *crow_dev = nullptr;
+    if (crow) {  // compacted-row streaming (LSD): per-utterance row offsets to the device
+        int rc;
+        if ((rc = grow(&d->h_crow, d->h_crow_n, (size_t)n))) return rc;
+        CUDA_TRY(cudaMemcpyAsync(d->h_crow, crow, sizeof(long long) * n, cudaMemcpyHostToDevice, st));
+        crow_dev = d->h_crow;
+    }
+    BatchDev bd{dc, doff, dT, db, num_cols, n, dol, dil, lcap, ready_dev, crow_dev};
     CfgDev cd{cfg->beam, cfg->blank_threshold, cfg->max_active, cfg->mode, cfg->lattice};
     const bool prune = cfg->lattice && cfg->lattice_beam >= 0;
     if (cfg->lattice && !(cfg->lattice_beam < 0) && std::isnan(cfg->lattice_beam))
@@ -666,10 +674,20 @@ int wb_decode(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row
 int wb_decode_stream(wb_decoder_t d, int32_t n, const double *costs, const int64_t *row_offset,
                      const int32_t *num_frames, int32_t num_cols, const double *blank,
                      const wb_config *cfg, int32_t label_capacity, const int32_t *ready,
-                     void *stream) {
+                     const int64_t *step_row_offset, void *stream) {
     if (!ready) return set_err(WB_ERR_VALUE, "null ready counters");
+    if (step_row_offset && cfg && cfg->mode != 1)
+        return set_err(WB_ERR_VALUE, "compacted rows are for label-synchronous decoding");
     return decode_impl(d, n, costs, row_offset, num_frames, num_cols, blank, cfg, nullptr,
-                       nullptr, nullptr, label_capacity, WB_MEM_HOST, stream, ready, true);
+                       nullptr, nullptr, label_capacity, WB_MEM_HOST, stream, ready, true,
+                       step_row_offset);
+}
+
+void wb_gather_rows(const double *src, int64_t src_ld, const int32_t *idx, int64_t n, int32_t col0,
+                    int32_t ncols, double *dst, int64_t dst_ld, int32_t dst_col0) {
+    for (int64_t i = 0; i < n; ++i)
+        std::memcpy(dst + i * dst_ld + dst_col0, src + (int64_t)idx[i] * src_ld + col0,
+                    sizeof(double) * (size_t)ncols);
 }
 
 int wb_decode_finish(wb_decoder_t d, wb_utt_result *results, int32_t *olabels, int32_t *ilabels) {

@@ -310,12 +310,13 @@ class BatchDecoder:
     def decode_posteriors(self, posts_list, cfg, mode: str | None = None,
                           label_capacity: int | None = None, lattice: bool = False,
                           lattice_beam: float | None = None, block_frames: int = 32,
-                          workers: int | None = None) -> BatchOutput:
+                          workers: int | None = None, _attempt: int = 0) -> BatchOutput:
         """Decode from posterior matrices (the public path): host threads compute the
         frame_costs rows straight into a page-locked table in frame-block order while the
         kernel already searches, reading each row zero-copy once its block is published
         (``wb_decode_stream``).  LSD computes only the non-blank rows (select_frames,
-        posteriors.py:109-110).  Bit-identical to ``decode_host`` on ``cost_table``."""
+        posteriors.py:109-110), gathered into a compacted table indexed by search step.
+        Bit-identical to ``decode_host`` on ``cost_table``."""
         import os
         import threading
         from concurrent.futures import ThreadPoolExecutor
@@ -330,13 +331,27 @@ class BatchDecoder:
         T = np.asarray([p.num_frames for p in posts_list], np.int32)
         off = np.zeros(n, np.int64)
         np.cumsum(T[:-1], out=off[1:])
-        R = max(int(T.sum()), 1)
+        blank = np.zeros(max(int(T.sum()), 1), np.float64)
+        for p, o, t in zip(posts_list, off, T):
+            blank[o:o + t] = p.rows[:, p.blank_col]
+        # LSD: only the frames the device pre-pass will search (blank <= threshold, strict >
+        # for blank), compacted per utterance in search-step order when the label columns
+        # are contiguous (blank column 0); otherwise rows stay indexed by frame
+        compact = mode == "lsd" and all(p.blank_col == 0 for p in posts_list)
+        need = [np.flatnonzero(~(p.rows[:, p.blank_col] > cfg.blank_threshold)).astype(np.int32)
+                if mode == "lsd" else None for p in posts_list]
+        if compact:
+            nrow = np.asarray([len(x) for x in need], np.int64)
+            crow = np.zeros(n, np.int64)
+            np.cumsum(nrow[:-1], out=crow[1:])
+            R = max(int(nrow.sum()), 1)
+            total = nrow.astype(np.int32)
+        else:
+            R = max(int(T.sum()), 1)
+            total = T
         costs = self._pinned("_pin_costs", (R, L1), np.float64)
         ready = self._pinned("_pin_ready", (n,), np.int32)
         ready[:] = 0
-        blank = np.zeros(R, np.float64)
-        for p, o, t in zip(posts_list, off, T):
-            blank[o:o + t] = p.rows[:, p.blank_col]
         maxT = int(T.max())
         self.reserve(int(T.sum()) + n, cfg.max_active, maxT, lattice)
         cap = label_capacity or (maxT + 64)
@@ -345,51 +360,74 @@ class BatchDecoder:
         ncfg = _native_config(cfg, mode, lattice, lattice_beam)
         self._last_max_active = cfg.max_active
         N.flush_destroy()   # nothing may free device memory while the kernel waits on us
-        # rows each utterance needs: all frames (FSD) or the non-blank ones (LSD)
-        need = []
-        for p in posts_list:
-            if mode == "lsd":
-                need.append(np.flatnonzero(~(p.rows[:, p.blank_col] > cfg.blank_threshold)))
-            else:
-                need.append(None)
-        N.check(N.load().wb_decode_stream(self._h, n, costs.ctypes.data, off.ctypes.data,
-                                          T.ctypes.data, L1, blank.ctypes.data, C.byref(ncfg),
-                                          cap, ready.ctypes.data, None), "decode")
-        # producers: frame blocks in block-major order, each utterance's ready count advanced
+        L = N.load()
+        N.check(L.wb_decode_stream(self._h, n, costs.ctypes.data, off.ctypes.data, T.ctypes.data,
+                                   L1, blank.ctypes.data, C.byref(ncfg), cap, ready.ctypes.data,
+                                   crow.ctypes.data if compact else None, None), "decode")
+        # producers: row blocks in block-major order; each utterance's ready count advances
         # over its contiguous finished prefix
         lock = threading.Lock()
         done = [dict() for _ in range(n)]
         nxt = [0] * n
-        nblk = [(int(t) + block_frames - 1) // block_frames for t in T]
+        nblk = [(int(t) + block_frames - 1) // block_frames for t in total]
+        neg = -cfg.acoustic_scale
 
         def work(u, b):
-            lo, hi = b * block_frames, min(int(T[u]), (b + 1) * block_frames)
-            view = costs[off[u]:off[u] + T[u]]
-            if need[u] is None:
-                cost_rows(posts_list[u], np.arange(lo, hi), view, cfg.acoustic_scale)
+            lo, hi = b * block_frames, min(int(total[u]), (b + 1) * block_frames)
+            p = posts_list[u]
+            if compact:   # gather the searched rows (C++, no GIL), then -scale*log in place
+                r0 = int(crow[u]) + lo
+                idx = need[u][lo:hi]
+                src = p.rows if p.rows.flags.c_contiguous else np.ascontiguousarray(p.rows)
+                L.wb_gather_rows(src.ctypes.data, L1, idx.ctypes.data, hi - lo, 1, L1 - 1,
+                                 costs[r0:].ctypes.data, L1, 1)
+                dst = costs[r0:r0 + hi - lo, 1:]
+                with np.errstate(divide="ignore"):
+                    np.log(dst, out=dst)
+                np.multiply(dst, neg, out=dst)
+                costs[r0:r0 + hi - lo, 0] = np.inf
             else:
-                sel = need[u][(need[u] >= lo) & (need[u] < hi)]
-                if len(sel):
-                    cost_rows(posts_list[u], sel, view, cfg.acoustic_scale)
+                view = costs[off[u]:off[u] + T[u]]
+                if need[u] is None:
+                    cost_rows(p, np.arange(lo, hi), view, cfg.acoustic_scale)
+                else:
+                    sel = need[u][(need[u] >= lo) & (need[u] < hi)]
+                    if len(sel):
+                        cost_rows(p, sel, view, cfg.acoustic_scale)
             with lock:
                 done[u][b] = hi
                 while nxt[u] in done[u]:
                     ready[u] = done[u].pop(nxt[u])
                     nxt[u] += 1
-        tasks = [(u, b) for b in range(max(nblk)) for u in range(n) if b < nblk[u]]
+        tasks = [(u, b) for b in range(max(nblk) if nblk else 0) for u in range(n) if b < nblk[u]]
         nw = workers or min(8, len(os.sched_getaffinity(0)))
         try:
             with ThreadPoolExecutor(nw) as ex:
                 list(ex.map(lambda ub: work(*ub), tasks))
         finally:
-            ready[:] = T      # every row is written (or the kernel must not wait forever)
+            ready[:] = total  # every row is written (or the kernel must not wait forever)
         res = np.zeros(n, dtype=N.UTT_RESULT_DTYPE)
         ol = np.zeros((n, cap), dtype=np.int32)
         il = np.zeros((n, cap), dtype=np.int32)
-        N.check(N.load().wb_decode_finish(self._h, res.ctypes.data, ol.ctypes.data,
-                                          il.ctypes.data), "decode")
-        if (res["status"] != N.WB_OK).any():   # capacity: rerun on the finished table
-            return self.decode_host(costs, off, T, blank, cfg, mode, cap, lattice, lattice_beam)
+        N.check(L.wb_decode_finish(self._h, res.ctypes.data, ol.ctypes.data, il.ctypes.data),
+                "decode")
+        bad = res["status"] != N.WB_OK
+        if bad.any():   # a capacity ran out: grow exactly that one and decode again
+            if _attempt >= 16:
+                raise N.CapacityError("decode workspace kept overflowing")
+            flags = int(np.bitwise_or.reduce(res["capacity_flags"][bad]))
+            if flags & N.WB_CAP_LABELS:
+                cap = int(np.maximum(res["n_olabels"], res["n_ilabels"]).max())
+            if flags & ~N.WB_CAP_LABELS:
+                need_out = 0
+                if flags & N.WB_CAP_LATTICE_OUT:
+                    nu, nn, na, nf = C.c_int32(), C.c_int64(), C.c_int64(), C.c_int64()
+                    N.check(L.wb_lattice_totals(self._h, C.byref(nu), C.byref(nn), C.byref(na),
+                                                C.byref(nf)), "lattice")
+                    need_out = max(nn.value, na.value, nf.value)
+                self._grow(flags, lattice_out_need=need_out, max_frames=maxT)
+            return self.decode_posteriors(posts_list, cfg, mode, cap, lattice, lattice_beam,
+                                          block_frames, workers, _attempt + 1)
         return BatchOutput(res, ol, il, cap)
 
     def fetch_lattices(self, wfst: Wfst) -> list:
