@@ -128,24 +128,25 @@ def test_ctc_lsd_blank_skip_at_scale(cuda):
         assert r.search_steps <= nonblank < p.num_frames
 
 
+@pytest.mark.parametrize("blank_col", [0, 5])
 @pytest.mark.parametrize("mode", ["fsd", "lsd"])
-def test_streaming_posteriors_equal_cost_table_path(cuda, mode):
+def test_streaming_posteriors_equal_cost_table_path(cuda, mode, blank_col):
     """decode_posteriors (rows computed by host threads while the kernel already runs,
     ready counters in page-locked memory) == decode_host on the finished cost table."""
     from paper_1808_00687_b200.decoder import BatchDecoder
     g = synth.random_wfst(13, 3000, 9000, 60, eps_fraction=0.03, selfloops=mode == "lsd",
                           final_fraction=0.05)
-    posts = [synth.random_posteriors(300 + k, 100 + 37 * k, 60,
+    posts = [synth.random_posteriors(300 + k, 100 + 37 * k, 60, blank_col=blank_col,
                                      blank_fraction=0.7 if mode == "lsd" else 0.0)
-             for k in range(9)] + [synth.random_posteriors(999, 0, 60)]
-    cfg = P.DecodeConfig(beam=10.0, max_active=300, mode=mode)
+             for k in range(9)] + [synth.random_posteriors(999, 0, 60, blank_col=blank_col)]
+    cfg = P.DecodeConfig(beam=10.0, max_active=300, mode=mode, acoustic_scale=0.8)
     dec = BatchDecoder(g, 0)
     got = dec.decode_posteriors(posts, cfg, mode, block_frames=8, workers=3).decode_results()
     T = np.asarray([p.num_frames for p in posts], np.int32)
     off = np.zeros(len(T), np.int64)
     np.cumsum(T[:-1], out=off[1:])
-    costs = np.concatenate([P.cost_table(p) for p in posts if p.num_frames])
-    blank = np.concatenate([p.rows[:, 0] for p in posts])
+    costs = np.concatenate([P.cost_table(p, 0.8) for p in posts if p.num_frames])
+    blank = np.concatenate([p.rows[:, p.blank_col] for p in posts])
     want = BatchDecoder(g, 0).decode_host(costs, off, T, blank, cfg, mode).decode_results()
     assert got == want
     h2d, zc = dec.last_transfer()
