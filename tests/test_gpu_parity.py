@@ -163,3 +163,23 @@ def test_multi_device_threads_equal_single_batch(cuda):
     want = P.decode_batch(g, posts, cfg)
     got = decode_multi_device(g, posts, cfg, devices=[0, 0])
     assert got == want
+
+
+def test_edge_cases_vs_oracle(cuda):
+    """Empty and degenerate inputs: zero frames, all-blank LSD utterances (no search step),
+    one frame, beam 0, max-active 1, a graph whose start state has no arcs."""
+    g = synth.random_wfst(23, 300, 1200, 12, eps_fraction=0.1, final_fraction=0.2)
+    allblank = synth.random_posteriors(5, 20, 12, blank_fraction=1.0)
+    posts = [synth.random_posteriors(1, 0, 12), allblank, synth.random_posteriors(2, 1, 12),
+             synth.random_posteriors(3, 50, 12, blank_fraction=0.5)]
+    for mode in ("fsd", "lsd"):
+        for beam, ma in ((0.0, None), (INF, 1), (5.0, 2), (INF, None)):
+            _check_batch(g, posts, P.DecodeConfig(beam=beam, max_active=ma, mode=mode))
+    r = P.decode(g, allblank, P.DecodeConfig(beam=9.0, mode="lsd"))
+    assert r.search_steps == 0 and r.tokens_expanded == 0
+    # a start state without arcs: the search dies at the first step
+    from paper_1808_00687_b200.wfst import Wfst
+    w = Wfst.from_arrays(3, 2, [0, 1], [1, 0], [1, 2], [1, 2], [0.5, 0.5],
+                         np.array([np.inf, 0.0, np.inf]))
+    p = synth.random_posteriors(4, 5, 2)
+    _check_batch(w, [p], P.DecodeConfig(beam=INF, mode="fsd"))
