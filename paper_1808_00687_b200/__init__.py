@@ -12,7 +12,11 @@ from .decoder import (BatchDecoder, BatchOutput, DecodeConfig, DecodeResult, Dev
                       parallel_decode)
 from .lattice import LatticeError, LatticeRecorder
 from .posteriors import (BlankMask, PosteriorFormatError, PosteriorMatrix, acoustic_cost,
-                         classify_blank_frames, cost_table, frame_costs)
+                         classify_blank_frames, cost_table, frame_costs, load_posteriors,
+                         save_posteriors)
+from .lattice import (EMPTY_LATTICE, Lattice, build_lattice, lattice_best_path, prune_lattice)
+from .pipeline import LatticePipeline
+from .shard import decode_multi_device, decode_sharded, shard_utterances
 from .wfst import (Arc, EpsilonCycle, ParseError, Wfst, WfstError, parse_wfst_text,
                    validate_epsilon_acyclic)
 
@@ -22,5 +26,7 @@ __all__ = [
     "PosteriorFormatError", "PosteriorMatrix", "SearchDied", "Wfst", "WfstError",
     "acoustic_cost", "as_wfst", "classify_blank_frames", "cost_table", "decode",
     "decode_batch", "decode_fsd", "decode_lsd", "frame_costs", "parallel_decode",
-    "parse_wfst_text", "validate_epsilon_acyclic",
+    "parse_wfst_text", "validate_epsilon_acyclic", "load_posteriors", "save_posteriors",
+    "EMPTY_LATTICE", "Lattice", "build_lattice", "lattice_best_path", "prune_lattice",
+    "LatticePipeline", "decode_multi_device", "decode_sharded", "shard_utterances",
 ]

@@ -228,3 +228,26 @@ def test_native_wfst_parser_matches_reference():
         mine = parse_wfst_text(t)
         ref = L.wfst.parse_wfst_text(t)
         assert _wfst_key(mine) == _wfst_key(Wfst.from_reference(ref))
+
+
+def test_posterior_files_roundtrip_and_match_reference(tmp_path):
+    """load_posteriors / save_posteriors (posteriors.py:147-238): text and POST1 binary round
+    trips, and (build container) the reference reads our files and we read its files."""
+    import numpy as np
+    from paper_1808_00687_b200 import synth
+    from paper_1808_00687_b200.posteriors import (PosteriorMatrix, format_posteriors_binary,
+                                                   format_posteriors_text, load_posteriors,
+                                                   save_posteriors)
+    p = synth.random_posteriors(9, 17, 6, blank_col=2)
+    for binary in (False, True):
+        path = str(tmp_path / f"p{int(binary)}")
+        save_posteriors(p, path, binary=binary)
+        q = load_posteriors(path)
+        assert q.blank_col == 2 and q.rows.tobytes() == p.rows.tobytes()
+    assert load_posteriors(format_posteriors_binary(p)).rows.tobytes() == p.rows.tobytes()
+    if refutil.HAVE_REF:
+        L = refutil.ref()
+        ref = L.posteriors.load_posteriors(format_posteriors_text(p).encode())
+        assert ref.rows.tobytes() == p.rows.tobytes()
+        mine = load_posteriors(L.posteriors.format_posteriors_text(ref).encode())
+        assert mine.rows.tobytes() == p.rows.tobytes()
