@@ -1021,7 +1021,7 @@ __device__ __forceinline__ bool surv_bit(const u32 *bits, u32 s) {
 // recorder is needed.  Node / arc indices are utterance-global positions in this lane's pool.
 template <int BLOCK>
 __noinline__ __device__ int record_lattice_step(int k, int nxt, int n_surv, int prv, int n_prev,
-                                                const double *grow, int L1, u32 tagL,
+                                                const double *grow, int L1,
                                                 const GraphDev &g, const WorkDev &ws) {
     Smem<BLOCK> &sh = SH<BLOCK>();
     const Lane c{ws};
@@ -1457,8 +1457,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
         n_rec += so.n_keep;
         long long lat_arcs = 0;
         if (cfg.lattice && status == WB_OK) {
-            ++tag;
-            const int rs = record_lattice_step<BLOCK>(0, cur, so.n_surv, 0, 0, nullptr, 0, tag, g, ws);
+            const int rs = record_lattice_step<BLOCK>(0, cur, so.n_surv, 0, 0, nullptr, 0, g, ws);
             if (rs) status = rs;
         }
         int n_live = so.n_surv;
@@ -1521,9 +1520,8 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             }
             n_surv_tot += so.n_surv;
             if (cfg.lattice && status == WB_OK) {
-                ++tag;
                 const int rs = record_lattice_step<BLOCK>(s + 1, cur ^ 1, so.n_surv, cur, n_live, grow,
-                                                          b.L1, tag, g, ws);
+                                                          b.L1, g, ws);
                 if (rs) status = rs;
             }
             cur ^= 1;
