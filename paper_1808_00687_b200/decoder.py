@@ -400,7 +400,7 @@ class BatchDecoder:
                     ready[u] = done[u].pop(nxt[u])
                     nxt[u] += 1
         tasks = [(u, b) for b in range(max(nblk) if nblk else 0) for u in range(n) if b < nblk[u]]
-        nw = workers or min(8, len(os.sched_getaffinity(0)))
+        nw = workers or int(os.environ.get("WB_PRODUCERS", 0)) or min(8, len(os.sched_getaffinity(0)))
         try:
             with ThreadPoolExecutor(nw) as ex:
                 list(ex.map(lambda ub: work(*ub), tasks))
