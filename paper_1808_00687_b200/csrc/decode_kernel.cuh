@@ -58,6 +58,7 @@ struct GraphDev {
     int4 start_rng;         // {eps_lo, eps_hi (= emit_lo), emit_hi, 0} of the start state
     const int4 *arcs;       // [2*A]: {dst, ilabel, w_lo, w_hi}, {d_eps_lo, d_emit_lo, d_emit_hi, olabel}
     const double *final_w;  // [S] (+inf = not final)
+    int nonneg;             // every arc weight >= 0 (enables the in-expand beam skip)
 };
 
 struct WorkDev {
@@ -81,6 +82,7 @@ struct WorkDev {
     long long S;
     int cap, T_cap, smem_cands, row_in_smem;
     int stage_off;        // dyn-smem byte offset of the per-lane arc prefetch buffers (0 = off)
+    int beam_skip;        // expand skips relaxations provably outside the beam
     // ---- lattice recording (LatticeRecorder / build_lattice, lattice.py:96-249)
     int *tok_eps;         // [slots][2][cap] epsilon-range start of each token's state
     u32 *sbits;           // [slots][ceil(S/32)] survivor bitmap of the current node step (L2-resident)
@@ -136,6 +138,7 @@ struct Smem {
     int n_cand, n_front, overflow, utt, tag_round, ng, thr_bucket, thr_below, n_pend;
     int flag, lat_bad;  // lattice sweeps: change flag / output-pool overflow
     int n_log;          // relaxations logged this step (lattice mode)
+    u64 run_min;        // smallest emitting relaxation key seen so far this step
     int ready_seen;     // streaming: last ready count read for the current utterance
     u64 thr_key;
     u32 thr_state;
@@ -350,7 +353,8 @@ struct ExpandCounts {
 
 template <int BLOCK>
 __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const double *row,
-                                                     const GraphDev &g, const WorkDev &ws) {
+                                                     const GraphDev &g, const WorkDev &ws,
+                                                     double beam) {
     const Lane c{ws};
     u32 a_emit = 0, a_fin = 0;
     constexpr int NW = BLOCK / 32;
@@ -367,6 +371,8 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
         // (cp.async, no registers held) while its current relaxation's CAS is in flight, so an
         // iteration costs one memory round trip instead of two.
         int4 *stage = reinterpret_cast<int4 *>(dyn_smem() + ws.stage_off) + 2 * threadIdx.x;
+        const bool skip_on = g.nonneg && beam < INFINITY && ws.beam_skip;
+        auto sh_run_min = [&]() -> u64 { return *(volatile u64 *)&SH<BLOCK>().run_min; };
         const u32 s0 = (u32)__cvta_generic_to_shared(stage);
         for (int ch = w; ch < nchunks; ch += NW) {
             const int t = (ch << 5) + l;
@@ -424,8 +430,21 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
                     }
                 }
                 bool first = false, dec = false;
-                if (act) {
-                    a_fin++;
+                bool relax = act;
+                if (skip_on) {
+                    // Beam skip (exact): the step's best cost is at most the smallest key seen
+                    // so far, so a relaxation above (that + beam) lands above the final cutoff
+                    // best + beam (decoder.py:186) and its state cannot survive; with
+                    // non-negative weights nothing reached from it can either.  The lattice
+                    // log above still records it.
+                    const u64 wm = warp_min_u64(act ? want.key : EMPTY_KEY);
+                    if (l == 0 && wm < sh_run_min()) atomicMin(reinterpret_cast<unsigned long long *>(&SH<BLOCK>().run_min), wm);
+                    const u64 rm = sh_run_min();
+                    if (relax && rm != EMPTY_KEY && want.key > cost_key(__dadd_rn(key_cost(rm), beam)))
+                        relax = false;
+                }
+                if (act) a_fin++;
+                if (relax) {
                     const Slot prev = cas_slot(&slot[rec.x], empty, want);
                     finish_relax(&slot[rec.x], want, prev, &first, &dec);
                 }
@@ -1492,12 +1511,14 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
                 for (int q = threadIdx.x; q < b.L1; q += BLOCK) srow[q] = __ldg(&grow[q]);
                 row = srow;
             }
-            if (threadIdx.x == 0) { sh.n_cand = 0; sh.n_front = 0; sh.overflow = 0; sh.n_log = 0; }
+            if (threadIdx.x == 0) {
+                sh.n_cand = 0; sh.n_front = 0; sh.overflow = 0; sh.n_log = 0; sh.run_min = EMPTY_KEY;
+            }
             __syncthreads();
             tick<BLOCK>(0);
             expanded += n_live;
             n_tok += n_live;
-            ExpandCounts ec = expand_emitting<BLOCK>(n_live, cur, row, g, ws);
+            ExpandCounts ec = expand_emitting<BLOCK>(n_live, cur, row, g, ws, cfg.beam);
             a_emit += ec.a_emit;
             a_fin += ec.a_fin;
             __syncthreads();

@@ -35,7 +35,7 @@ int wb_internal_set_error(int code, const char *msg) { return set_err(code, msg)
 
 struct wb_graph_s {
     int device = 0;
-    int S = 0, A = 0, start = 0, has_eps = 0, max_ilabel = 0;
+    int S = 0, A = 0, start = 0, has_eps = 0, max_ilabel = 0, nonneg = 1;
     int4 start_rng{0, 0, 0, 0};
     int4 *arcs = nullptr;      // [2*A] 32-byte arc records
     double *final_w = nullptr;
@@ -130,7 +130,7 @@ int wb_graph_create(const wb_graph_desc *d, int32_t device, wb_graph_t *out) {
         return set_err(WB_ERR_VALUE, "bad graph dimensions");
     const int S = d->num_states, A = d->num_arcs;
     if (d->row_ptr[0] != 0 || d->row_ptr[S] != A) return set_err(WB_ERR_VALUE, "row_ptr mismatch");
-    int has_eps = 0, max_il = 0;
+    int has_eps = 0, max_il = 0, nonneg = 1;
     for (int s = 0; s < S; ++s) {
         int lo = d->row_ptr[s], mid = d->eps_end[s], hi = d->row_ptr[s + 1];
         if (lo > mid || mid > hi) return set_err(WB_ERR_VALUE, "eps_end outside the state's arc range");
@@ -149,6 +149,7 @@ int wb_graph_create(const wb_graph_desc *d, int32_t device, wb_graph_t *out) {
         arcs[2 * (size_t)a + 1] =
             make_int4(d->row_ptr[dst], d->eps_end[dst], d->row_ptr[dst + 1], d->olabel[a]);
         max_il = std::max(max_il, d->ilabel[a]);
+        if (!(d->weight[a] >= 0.0)) nonneg = 0;
     }
     for (int s = 0; s < S; ++s)
         if (std::isnan(d->final_w[s])) return set_err(WB_ERR_VALUE, "NaN final weight");
@@ -160,6 +161,7 @@ int wb_graph_create(const wb_graph_desc *d, int32_t device, wb_graph_t *out) {
     g->start = d->start;
     g->has_eps = has_eps;
     g->max_ilabel = max_il;
+    g->nonneg = nonneg;
     g->start_rng = make_int4(d->row_ptr[d->start], d->eps_end[d->start], d->row_ptr[d->start + 1], 0);
     cudaError_t e = cudaMalloc(&g->arcs, sizeof(int4) * arcs.size());
     if (e == cudaSuccess) e = cudaMalloc(&g->final_w, sizeof(double) * S);
@@ -310,6 +312,8 @@ static cudaError_t launch_decode(int max_grid, int num_sms, int num_cols, cudaSt
     const size_t row_r = (row + 127) & ~(size_t)127, stage = (size_t)BLOCK * 32;
     const char *pf = std::getenv("WB_PREFETCH");
     wd.stage_off = (row > 0 && row_r + stage <= avail && !(pf && pf[0] == '0')) ? (int)(hdr + row_r) : 0;
+    const char *bs = std::getenv("WB_BEAM_SKIP");
+    wd.beam_skip = (bs && bs[0] == '0') ? 0 : 1;
     size_t smem = hdr + std::max(wd.stage_off ? row_r + stage : row,
                                  (size_t)wd.smem_cands * (sizeof(u64) + sizeof(u32)));
     smem = (smem + 15) & ~(size_t)15;
@@ -517,7 +521,7 @@ static int decode_impl(wb_decoder_t d, int32_t n, const double *costs, const int
     // device mode: frame counts stay on the device; an LSD utterance longer than the frame
     // list capacity reports WB_ERR_CAPACITY (callers size it with max_frames)
     CUDA_TRY(cudaMemsetAsync(d->counters, 0, sizeof(u64) * 4, st));
-    GraphDev gd{g->S, g->A, g->start, g->has_eps, g->start_rng, g->arcs, g->final_w};
+    GraphDev gd{g->S, g->A, g->start, g->has_eps, g->start_rng, g->arcs, g->final_w, g->nonneg};
     WorkDev wd;
     std::memset(&wd, 0, sizeof(wd));
     wd.slot = d->slot; wd.cand_of = d->cand_of; wd.qtag = d->qtag; wd.tag_ctr = d->tag_ctr;
