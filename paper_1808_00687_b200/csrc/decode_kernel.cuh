@@ -542,9 +542,15 @@ struct EpsOut {
 };
 
 template <int BLOCK>
-__noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev &ws, u32 tag_in) {
+__noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev &ws, u32 tag_in,
+                                               double beam) {
     Smem<BLOCK> &sh = SH<BLOCK>();
     const Lane c{ws};
+    // beam skip as in expand: with non-negative weights every candidate of this step costs at
+    // least run_min (the emitting minimum), so run_min + beam is the step's final cutoff
+    const u64 rm = sh.run_min;
+    const bool skip_on = g.nonneg && ws.beam_skip && beam < INFINITY && rm != EMPTY_KEY;
+    const u64 thr = skip_on ? cost_key(__dadd_rn(key_cost(rm), beam)) : EMPTY_KEY;
     u32 tag_cur = tag_in, e_eps = 0;
     int status = WB_OK;
     constexpr int NW = BLOCK / 32;
@@ -611,8 +617,10 @@ __noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev 
                     want.key = cost_key(__dadd_rn(uc_k, __hiloint2double(rec.w, rec.z)));
                     want.arcp1 = (u32)a + 1u;
                     want.pay = ui_k | EPS_BIT;
-                    Slot prev = cas_slot(&slot[rec.x], empty, want);
-                    finish_relax(&slot[rec.x], want, prev, &first, &dec);
+                    if (want.key <= thr) {
+                        Slot prev = cas_slot(&slot[rec.x], empty, want);
+                        finish_relax(&slot[rec.x], want, prev, &first, &dec);
+                    }
                 }
                 int4 r1 = make_int4(0, 0, 0, 0);
                 if (dec) r1 = __ldg(&g.arcs[2 * a + 1]);
@@ -1430,7 +1438,9 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
         const int u = sh.utt;
         if (u >= b.n) break;
         if (threadIdx.x < 8) sh.pc[threadIdx.x] = 0;
-        if (threadIdx.x == 0) { sh.t_mark = clock64(); sh.arena_used = 0; sh.ready_seen = 0; }
+        if (threadIdx.x == 0) {
+            sh.t_mark = clock64(); sh.arena_used = 0; sh.ready_seen = 0; sh.run_min = EMPTY_KEY;
+        }
         const int T = b.T[u];
         const long long row0 = b.row_off[u];
         int status = WB_OK;
@@ -1464,7 +1474,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
         }
         __syncthreads();
         if (g.has_eps) {
-            EpsOut eo = epsilon_closure<BLOCK>(g, ws, tag);
+            EpsOut eo = epsilon_closure<BLOCK>(g, ws, tag, cfg.beam);
             tag = eo.tag;
             e_eps += eo.e_eps;
             if (eo.status) status = eo.status;
@@ -1524,7 +1534,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             __syncthreads();
             tick<BLOCK>(1);
             if (g.has_eps) {
-                EpsOut eo = epsilon_closure<BLOCK>(g, ws, tag);
+                EpsOut eo = epsilon_closure<BLOCK>(g, ws, tag, cfg.beam);
                 tag = eo.tag;
                 e_eps += eo.e_eps;
                 if (eo.status) status = eo.status;
