@@ -139,6 +139,7 @@ struct Smem {
     int flag, lat_bad;  // lattice sweeps: change flag / output-pool overflow
     int n_log;          // relaxations logged this step (lattice mode)
     u64 run_min;        // smallest emitting relaxation key seen so far this step
+    int best_tok;       // a live token of minimal cost (its arcs seed run_min); -1 = unknown
     int ready_seen;     // streaming: last ready count read for the current utterance
     u64 thr_key;
     u32 thr_state;
@@ -373,6 +374,28 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
         int4 *stage = reinterpret_cast<int4 *>(dyn_smem() + ws.stage_off) + 2 * threadIdx.x;
         const bool skip_on = g.nonneg && beam < INFINITY && ws.beam_skip;
         auto sh_run_min = [&]() -> u64 { return *(volatile u64 *)&SH<BLOCK>().run_min; };
+        if (skip_on) {
+            // pilot: relax-evaluate (no CAS) the arcs of a cheapest live token first, so the
+            // running minimum -- an upper bound of the step's best cost -- is tight from the
+            // start and the beam skip bites on the first relaxations already
+            const int bt = SH<BLOCK>().best_tok;
+            if (w == 0 && bt >= 0 && bt < n_live) {
+                const int4 ti = tinfo[bt];
+                const double tc = tcost[bt];
+                u64 m = EMPTY_KEY;
+                for (int a = ti.z + l; a < ti.w; a += 32) {
+                    const int4 r = ld_arc(&g.arcs[2 * a]);
+                    const double ac = row[r.y];
+                    if (ac != INFINITY) {
+                        const u64 k = cost_key(__dadd_rn(__dadd_rn(tc, __hiloint2double(r.w, r.z)), ac));
+                        m = k < m ? k : m;
+                    }
+                }
+                m = warp_min_u64(m);
+                if (l == 0 && m < sh_run_min()) atomicMin(reinterpret_cast<unsigned long long *>(&SH<BLOCK>().run_min), m);
+            }
+            __syncthreads();
+        }
         const u32 s0 = (u32)__cvta_generic_to_shared(stage);
         for (int ch = w; ch < nchunks; ch += NW) {
             const int t = (ch << 5) + l;
@@ -776,6 +799,7 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
     volatile u32 *vca = ca;
 
     // P1: gather slot contents (batched loads), reset slots, min / max
+    if (threadIdx.x == 0) sh.best_tok = -1;
     u64 mn = EMPTY_KEY, mx = 0;
     for (int i0 = threadIdx.x; i0 < n_cand; i0 += BLOCK * Tune<BLOCK>::GATHER) {
         u32 st[Tune<BLOCK>::GATHER];
@@ -947,6 +971,7 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
                     int4 rg = rng_[i];
                     tinfo[tj[q]] = make_int4((int)cst_[i], (int)rec[q], rg.y, rg.z);
                     tcost[tj[q]] = key_cost(ckey[i]);
+                    if (ckey[i] == mn) sh.best_tok = (int)tj[q];  // any minimal token will do
                     if (ws.tok_eps) ws.tok_eps[2 * c.co() + (size_t)nxt * ws.cap + tj[q]] = rg.x;
                 }
                 if (rec[q] != CA_NONE) {
