@@ -83,7 +83,7 @@ struct WorkDev {
     int cap, T_cap, smem_cands, row_in_smem;
     int stage_off;        // dyn-smem byte offset of the per-lane arc prefetch buffers (0 = off)
     int beam_skip;        // expand skips relaxations provably outside the beam
-    int exact_min;        // emitting-minimum pre-pass: 0 never, 1 always, 2 for steps >= 4096 tokens
+    int exact_min;        // token-filtered exact emitting-minimum pass (needs a non-negative row)
     // ---- lattice recording (LatticeRecorder / build_lattice, lattice.py:96-249)
     int *tok_eps;         // [slots][2][cap] epsilon-range start of each token's state
     u32 *sbits;           // [slots][ceil(S/32)] survivor bitmap of the current node step (L2-resident)
@@ -356,7 +356,7 @@ struct ExpandCounts {
 template <int BLOCK>
 __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const double *row,
                                                      const GraphDev &g, const WorkDev &ws,
-                                                     double beam) {
+                                                     double beam, bool row_nonneg) {
     const Lane c{ws};
     u32 a_emit = 0, a_fin = 0;
     constexpr int NW = BLOCK / 32;
@@ -375,44 +375,9 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
         int4 *stage = reinterpret_cast<int4 *>(dyn_smem() + ws.stage_off) + 2 * threadIdx.x;
         const bool skip_on = g.nonneg && beam < INFINITY && ws.beam_skip;
         auto sh_run_min = [&]() -> u64 { return *(volatile u64 *)&SH<BLOCK>().run_min; };
-        // exact minimum pre-pass for wide steps (pays off once the slots are contended:
-        // measured on 148+ lanes), the cheap pilot otherwise
-        const bool exact = skip_on && (ws.exact_min == 1 || (ws.exact_min == 2 && n_live >= 4096));
-        if (exact) {
-            // exact variant: one CAS-free pass computes the step's emitting minimum, so the
-            // skip uses the final cutoff from the first relaxation on
-            u64 m = EMPTY_KEY;
-            for (int ch = w; ch < nchunks; ch += NW) {
-                const int t = (ch << 5) + l;
-                int4 ti = make_int4(0, 0, 0, 0);
-                double tc = 0.0;
-                if (t < n_live) { ti = tinfo[t]; tc = tcost[t]; }
-                const int deg = t < n_live ? ti.w - ti.z : 0;
-                const int incl = warp_incl_scan(deg);
-                const int total = __shfl_sync(FULL, incl, 31);
-                const int excl = incl - deg;
-                for (int j0 = 0; j0 < total; j0 += 32) {
-                    const int j = j0 + l;
-                    const int k = warp_owner(excl, j);
-                    const int arc = __shfl_sync(FULL, ti.z, k) + j - __shfl_sync(FULL, excl, k);
-                    const double cst = __shfl_sync(FULL, tc, k);
-                    if (j < total) {
-                        const int4 r = ld_arc(&g.arcs[2 * arc]);
-                        const double ac = row[r.y];
-                        if (ac != INFINITY) {
-                            const u64 kk = cost_key(__dadd_rn(__dadd_rn(cst, __hiloint2double(r.w, r.z)), ac));
-                            m = kk < m ? kk : m;
-                        }
-                    }
-                }
-            }
-            m = warp_min_u64(m);
-            if (l == 0 && m != EMPTY_KEY) atomicMin(reinterpret_cast<unsigned long long *>(&SH<BLOCK>().run_min), m);
-            __syncthreads();
-        } else if (skip_on) {
-            // pilot: relax-evaluate (no CAS) the arcs of a cheapest live token first, so the
-            // running minimum -- an upper bound of the step's best cost -- is tight from the
-            // start and the beam skip bites on the first relaxations already
+        if (skip_on) {
+            // (1) pilot: evaluate (no CAS) the arcs of a cheapest live token, so the running
+            // minimum -- an upper bound of the step's best cost -- is tight from the start
             const int bt = SH<BLOCK>().best_tok;
             if (w == 0 && bt >= 0 && bt < n_live) {
                 const int4 ti = tinfo[bt];
@@ -430,6 +395,42 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
                 if (l == 0 && m < sh_run_min()) atomicMin(reinterpret_cast<unsigned long long *>(&SH<BLOCK>().run_min), m);
             }
             __syncthreads();
+            // (2) exact minimum: with non-negative weights and acoustic costs a relaxation of
+            // token t costs at least c_t, so only tokens cheaper than the pilot's minimum can
+            // lower it -- usually a handful -- and the skip below then uses the step's final
+            // cutoff from the first relaxation on
+            if (ws.exact_min && row_nonneg && n_live >= 1024) {  // (small steps: pilot only)
+                const u64 rm0 = sh_run_min();
+                const double bound = rm0 == EMPTY_KEY ? INFINITY : key_cost(rm0);
+                u64 m = EMPTY_KEY;
+                for (int ch = w; ch < nchunks; ch += NW) {
+                    const int t = (ch << 5) + l;
+                    int4 ti = make_int4(0, 0, 0, 0);
+                    double tc = 0.0;
+                    if (t < n_live) { ti = tinfo[t]; tc = tcost[t]; }
+                    const int deg = (t < n_live && tc < bound && t != bt) ? ti.w - ti.z : 0;
+                    const int incl = warp_incl_scan(deg);
+                    const int total = __shfl_sync(FULL, incl, 31);
+                    const int excl = incl - deg;
+                    for (int j0 = 0; j0 < total; j0 += 32) {
+                        const int j = j0 + l;
+                        const int k = warp_owner(excl, j);
+                        const int arc = __shfl_sync(FULL, ti.z, k) + j - __shfl_sync(FULL, excl, k);
+                        const double cst = __shfl_sync(FULL, tc, k);
+                        if (j < total) {
+                            const int4 r = ld_arc(&g.arcs[2 * arc]);
+                            const double ac = row[r.y];
+                            if (ac != INFINITY) {
+                                const u64 kk = cost_key(__dadd_rn(__dadd_rn(cst, __hiloint2double(r.w, r.z)), ac));
+                                m = kk < m ? kk : m;
+                            }
+                        }
+                    }
+                }
+                m = warp_min_u64(m);
+                if (l == 0 && m < sh_run_min()) atomicMin(reinterpret_cast<unsigned long long *>(&SH<BLOCK>().run_min), m);
+                __syncthreads();
+            }
         }
         const u32 s0 = (u32)__cvta_generic_to_shared(stage);
         for (int ch = w; ch < nchunks; ch += NW) {
@@ -1577,18 +1578,23 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
                     break;
                 }
             }
+            int neg = !row_in_smem;  // acoustic costs of this row all >= 0? (checked while staging)
             if (row_in_smem) {
-                for (int q = threadIdx.x; q < b.L1; q += BLOCK) srow[q] = __ldg(&grow[q]);
+                for (int q = threadIdx.x; q < b.L1; q += BLOCK) {
+                    const double v = __ldg(&grow[q]);
+                    neg |= v < 0.0;
+                    srow[q] = v;
+                }
                 row = srow;
             }
             if (threadIdx.x == 0) {
                 sh.n_cand = 0; sh.n_front = 0; sh.overflow = 0; sh.n_log = 0; sh.run_min = EMPTY_KEY;
             }
-            __syncthreads();
+            const bool row_nonneg = !__syncthreads_or(neg);
             tick<BLOCK>(0);
             expanded += n_live;
             n_tok += n_live;
-            ExpandCounts ec = expand_emitting<BLOCK>(n_live, cur, row, g, ws, cfg.beam);
+            ExpandCounts ec = expand_emitting<BLOCK>(n_live, cur, row, g, ws, cfg.beam, row_nonneg);
             a_emit += ec.a_emit;
             a_fin += ec.a_fin;
             __syncthreads();

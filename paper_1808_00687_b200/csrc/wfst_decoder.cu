@@ -315,7 +315,7 @@ static cudaError_t launch_decode(int max_grid, int num_sms, int num_cols, cudaSt
     const char *bs = std::getenv("WB_BEAM_SKIP");
     wd.beam_skip = (bs && bs[0] == '0') ? 0 : 1;
     const char *em = std::getenv("WB_EXACT_MIN");
-    wd.exact_min = !em ? 2 : (em[0] == '1' ? 1 : (em[0] == '0' ? 0 : 2));
+    wd.exact_min = (em && em[0] == '0') ? 0 : 1;
     size_t smem = hdr + std::max(wd.stage_off ? row_r + stage : row,
                                  (size_t)wd.smem_cands * (sizeof(u64) + sizeof(u32)));
     smem = (smem + 15) & ~(size_t)15;
