@@ -375,6 +375,7 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
         int4 *stage = reinterpret_cast<int4 *>(dyn_smem() + ws.stage_off) + 2 * threadIdx.x;
         const bool skip_on = g.nonneg && beam < INFINITY && ws.beam_skip;
         auto sh_run_min = [&]() -> u64 { return *(volatile u64 *)&SH<BLOCK>().run_min; };
+        bool exact = false;
         if (skip_on) {
             // (1) pilot: evaluate (no CAS) the arcs of a cheapest live token, so the running
             // minimum -- an upper bound of the step's best cost -- is tight from the start
@@ -400,6 +401,7 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
             // lower it -- usually a handful -- and the skip below then uses the step's final
             // cutoff from the first relaxation on
             if (ws.exact_min && row_nonneg && n_live >= 1024) {  // (small steps: pilot only)
+                exact = true;
                 const u64 rm0 = sh_run_min();
                 const double bound = rm0 == EMPTY_KEY ? INFINITY : key_cost(rm0);
                 u64 m = EMPTY_KEY;
@@ -431,6 +433,12 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
                 if (l == 0 && m < sh_run_min()) atomicMin(reinterpret_cast<unsigned long long *>(&SH<BLOCK>().run_min), m);
                 __syncthreads();
             }
+        }
+        // the final cutoff key when the exact minimum is known (EMPTY_KEY: running bound)
+        u64 exact_thr = EMPTY_KEY;
+        if (exact) {
+            const u64 rm = sh_run_min();
+            if (rm != EMPTY_KEY) exact_thr = cost_key(__dadd_rn(key_cost(rm), beam));
         }
         const u32 s0 = (u32)__cvta_generic_to_shared(stage);
         for (int ch = w; ch < nchunks; ch += NW) {
@@ -490,12 +498,15 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
                 }
                 bool first = false, dec = false;
                 bool relax = act;
-                if (skip_on) {
-                    // Beam skip (exact): the step's best cost is at most the smallest key seen
-                    // so far, so a relaxation above (that + beam) lands above the final cutoff
-                    // best + beam (decoder.py:186) and its state cannot survive; with
-                    // non-negative weights nothing reached from it can either.  The lattice
-                    // log above still records it.
+                if (exact_thr != EMPTY_KEY) {
+                    // Beam skip (exact) against the step's final cutoff best + beam
+                    // (decoder.py:186): such a state cannot survive and, with non-negative
+                    // weights, nothing reached from it can either.  The lattice log above
+                    // still records it.
+                    relax = act && want.key <= exact_thr;
+                } else if (skip_on) {
+                    // same skip against a running bound: the step's best cost is at most the
+                    // smallest key seen so far
                     const u64 wm = warp_min_u64(act ? want.key : EMPTY_KEY);
                     if (l == 0 && wm < sh_run_min()) atomicMin(reinterpret_cast<unsigned long long *>(&SH<BLOCK>().run_min), wm);
                     const u64 rm = sh_run_min();
