@@ -17,7 +17,8 @@ from .posteriors import (BlankMask, PosteriorFormatError, PosteriorMatrix, acous
 from .lattice import (EMPTY_LATTICE, Lattice, build_lattice, lattice_best_path, prune_lattice)
 from .pipeline import LatticePipeline
 from .shard import decode_multi_device, decode_sharded, shard_utterances
-from .wfst import (Arc, EpsilonCycle, ParseError, Wfst, WfstError, parse_wfst_text,
+from .wfst import (Arc, EpsilonCycle, ParseError, SymbolError, SymbolTable, Wfst, WfstError,
+                   format_wfst_text, load_wfst_binary, parse_wfst_text, save_wfst_binary,
                    validate_epsilon_acyclic)
 
 __all__ = [
@@ -29,4 +30,5 @@ __all__ = [
     "parse_wfst_text", "validate_epsilon_acyclic", "load_posteriors", "save_posteriors",
     "EMPTY_LATTICE", "Lattice", "build_lattice", "lattice_best_path", "prune_lattice",
     "LatticePipeline", "decode_multi_device", "decode_sharded", "shard_utterances",
+    "SymbolError", "SymbolTable", "format_wfst_text", "load_wfst_binary", "save_wfst_binary",
 ]

@@ -39,6 +39,91 @@ class ParseError(WfstError):
         self.line_no = line_no
 
 
+class SymbolError(WfstError):
+    """A label token could not be resolved against a symbol table (wfst.py:46-47)."""
+
+
+class SymbolTable:
+    """Label id <-> symbol string map (reference ``SymbolTable``, wfst.py:67-151).
+
+    Id 0 is always ``<eps>``; a ``<blank>`` entry's id is kept as ``blank_id``.  Remapping a
+    symbol or an id to a different partner raises ``SymbolError`` (``ParseError`` from
+    ``parse``, with the line number).
+    """
+
+    EPS_SYMBOL = "<eps>"
+    BLANK_SYMBOL = "<blank>"
+
+    def __init__(self, symbols: dict[str, int] | None = None):
+        self._by_sym: dict[str, int] = {self.EPS_SYMBOL: 0}
+        self._by_id: dict[int, str] = {0: self.EPS_SYMBOL}
+        self.blank_id: int | None = None
+        for sym, idx in (symbols or {}).items():
+            self.add(sym, idx)
+
+    def add(self, symbol: str, idx: int | None = None) -> int:
+        if idx is None:
+            idx = max(self._by_id) + 1
+        if idx == 0 or symbol == self.EPS_SYMBOL:
+            if idx == 0 and symbol == self.EPS_SYMBOL:
+                return 0
+            raise SymbolError(f"id 0 is reserved for {self.EPS_SYMBOL!r}, got {symbol!r} = {idx}")
+        have = self._by_sym.get(symbol)
+        if have is not None and have != idx:
+            raise SymbolError(f"symbol {symbol!r} already mapped to {have}, cannot remap to {idx}")
+        other = self._by_id.get(idx)
+        if other is not None and other != symbol:
+            raise SymbolError(f"id {idx} already mapped to {other!r}, cannot remap to {symbol!r}")
+        self._by_sym[symbol] = idx
+        self._by_id[idx] = symbol
+        if symbol == self.BLANK_SYMBOL:
+            self.blank_id = idx
+        return idx
+
+    def find_id(self, symbol: str) -> int | None:
+        return self._by_sym.get(symbol)
+
+    def find_symbol(self, idx: int) -> str | None:
+        return self._by_id.get(idx)
+
+    def __len__(self) -> int:
+        return len(self._by_sym)
+
+    def __contains__(self, symbol: str) -> bool:
+        return symbol in self._by_sym
+
+    def __iter__(self):
+        return iter(sorted(self._by_id.items()))
+
+    @classmethod
+    def parse(cls, text: str) -> "SymbolTable":
+        """``symbol id`` lines; ``#`` comments and blank lines skipped; id 0 must be <eps>."""
+        table = cls()
+        for line_no, raw in enumerate(text.splitlines(), start=1):
+            line = raw.strip()
+            if not line or line.startswith("#"):
+                continue
+            f = line.split()
+            if len(f) != 2:
+                raise ParseError(f"expected 'symbol id', got {raw!r}", line_no)
+            try:
+                idx = int(f[1])
+            except ValueError:
+                raise ParseError(f"bad id {f[1]!r}", line_no) from None
+            if idx == 0:
+                if f[0] != cls.EPS_SYMBOL:
+                    raise ParseError(f"id 0 must be {cls.EPS_SYMBOL!r}, got {f[0]!r}", line_no)
+                continue
+            try:
+                table.add(f[0], idx)
+            except SymbolError as exc:
+                raise ParseError(str(exc), line_no) from None
+        return table
+
+    def format(self) -> str:
+        return "".join(f"{sym} {idx}\n" for idx, sym in sorted(self._by_id.items()))
+
+
 @dataclass(frozen=True)
 class Arc:
     src: int
@@ -355,54 +440,147 @@ def _parse_fast(text: str, allow_negative_weights: bool):
         L.wb_parsed_wfst_free(C.byref(out))
 
 
-def parse_wfst_text(text: str, allow_negative_weights: bool = False) -> Wfst:
-    """AT&T-style text with integer labels (wfst.py:315-378, symbol tables not supported).
+def _label(tok: str, table: SymbolTable | None, line_no: int) -> int:
+    """Symbol lookup first, then a bare non-negative integer id (wfst.py:300-312)."""
+    if table is not None:
+        idx = table.find_id(tok)
+        if idx is not None:
+            return idx
+    try:
+        idx = int(tok)
+    except ValueError:
+        raise SymbolError(f"line {line_no}: unknown symbol {tok!r}") from None
+    if idx < 0:
+        raise SymbolError(f"line {line_no}: negative label id {idx}")
+    return idx
 
-    Arc lines ``src dst ilabel olabel [weight]``, final lines ``state [weight]``; the first
-    state mentioned is the start state.
+
+def parse_wfst_text(text: str, isyms: SymbolTable | None = None,
+                    osyms: SymbolTable | None = None,
+                    allow_negative_weights: bool = False) -> Wfst:
+    """AT&T-style transducer text (reference ``parse_wfst_text``, wfst.py:315-378).
+
+    Arc lines ``src dst ilabel olabel [weight]``, final lines ``state [weight]`` (missing
+    weight = 0.0); the first state mentioned is the start state; ``#`` comment lines and
+    blank lines are skipped.  Labels resolve through ``isyms`` / ``osyms`` when given, with
+    bare non-negative integers accepted as raw ids.  Without symbol tables the text goes
+    through the C++ fast path (csrc/wfst_text.cpp) when it can reproduce this parser exactly.
     """
-    fast = _parse_fast(text, allow_negative_weights)
-    if fast is not None:
-        return fast
+    if isyms is None and osyms is None:
+        fast = _parse_fast(text, allow_negative_weights)
+        if fast is not None:
+            return fast
     arcs: list[Arc] = []
     finals: dict[int, float] = {}
     start = None
     max_state = -1
+
+    def state(tok, line_no):
+        try:
+            x = int(tok)
+        except ValueError:
+            raise ParseError(f"bad state id {tok!r}", line_no) from None
+        if x < 0:
+            raise ParseError(f"negative state id {x}", line_no)
+        return x
+
+    def weight(tok, line_no):
+        try:
+            x = float(tok)
+        except ValueError:
+            raise ParseError(f"bad weight {tok!r}", line_no) from None
+        if math.isnan(x):
+            raise ParseError("weight is NaN", line_no)
+        if x < 0 and not allow_negative_weights:
+            raise ParseError(f"negative weight {x} (pass allow_negative_weights to accept)",
+                             line_no)
+        return x
+
     for line_no, raw in enumerate(text.splitlines(), start=1):
         line = raw.strip()
         if not line or line.startswith("#"):
             continue
         f = line.split()
-        try:
-            if len(f) in (1, 2):
-                s = int(f[0])
-                x = float(f[1]) if len(f) == 2 else 0.0
-                if s < 0:
-                    raise ParseError(f"negative state id {s}", line_no)
-                if math.isnan(x) or (x < 0 and not allow_negative_weights):
-                    raise ParseError(f"bad weight {f[1]!r}", line_no)
-                finals[s] = x
-                start = s if start is None else start
-                max_state = max(max_state, s)
-            elif len(f) in (4, 5):
-                a, b, i, o = (int(t) for t in f[:4])
-                x = float(f[4]) if len(f) == 5 else 0.0
-                if min(a, b) < 0 or min(i, o) < 0:
-                    raise ParseError("negative id", line_no)
-                if math.isnan(x) or (x < 0 and not allow_negative_weights):
-                    raise ParseError(f"bad weight {f[4]!r}", line_no)
-                arcs.append(Arc(a, b, i, o, x))
-                start = a if start is None else start
-                max_state = max(max_state, a, b)
-            else:
-                raise ParseError(f"expected 1-2 (final) or 4-5 (arc) fields, got {len(f)}", line_no)
-        except ValueError as exc:
-            if isinstance(exc, ParseError):
-                raise
-            raise ParseError(str(exc), line_no) from None
+        if len(f) in (1, 2):
+            s = state(f[0], line_no)
+            finals[s] = weight(f[1], line_no) if len(f) == 2 else 0.0
+            start = s if start is None else start
+            max_state = max(max_state, s)
+        elif len(f) in (4, 5):
+            a, b = state(f[0], line_no), state(f[1], line_no)
+            i, o = _label(f[2], isyms, line_no), _label(f[3], osyms, line_no)
+            x = weight(f[4], line_no) if len(f) == 5 else 0.0
+            arcs.append(Arc(a, b, i, o, x))
+            start = a if start is None else start
+            max_state = max(max_state, a, b)
+        else:
+            raise ParseError(f"expected 1-2 (final) or 4-5 (arc) fields, got {len(f)}", line_no)
     if start is None:
         raise ParseError("no states found in transducer text")
     return Wfst(max_state + 1, start, arcs, finals)
+
+
+def format_wfst_text(w: Wfst) -> str:
+    """AT&T text that ``parse_wfst_text`` reads back to the same graph: the start state is
+    mentioned first, weights are written with ``repr`` so they round-trip exactly.  Raises
+    ``WfstError`` for graphs text cannot express (a start state with neither arcs nor a final
+    weight while other states have arcs; trailing states no line mentions)."""
+    src = w.src
+    fin = w.final_weights
+    order = np.argsort(src != w.start, kind="stable")  # the start state's arcs first
+    lines = [f"{int(src[k])} {int(w.dst[k])} {int(w.ilabel[k])} {int(w.olabel[k])} "
+             f"{float(w.weight[k])!r}" for k in order.tolist()]
+    finals = [f"{s} {x!r}" for s, x in sorted(fin.items())]
+    if w.start in fin and (not lines or int(src[order[0]]) != w.start):
+        finals.remove(f"{w.start} {fin[w.start]!r}")
+        lines.insert(0, f"{w.start} {fin[w.start]!r}")
+    elif lines and int(src[order[0]]) != w.start:
+        raise WfstError("the start state has no arcs and no final weight; text cannot name it")
+    mentioned = [w.start, *fin] + ([int(src.max()), int(w.dst.max())] if len(src) else [])
+    if max(mentioned) != w.num_states - 1:
+        raise WfstError("trailing states with no arcs and no final weight cannot be written")
+    return "\n".join(lines + finals) + "\n"
+
+
+# ------------------------------------------------- binary CSR cache (SURVEY 8f row 2)
+_CSR_MAGIC = "wfst-b200-csr-v1"
+
+
+def save_wfst_binary(w: Wfst, path) -> None:
+    """Write the canonical CSR arrays (plus the cached epsilon-cycle verdict) so later runs
+    skip text parsing, sorting and ``validate_epsilon_acyclic``.  ``.npz``, uncompressed."""
+    cyc = w.epsilon_cycle()
+    np.savez(path, magic=np.array(_CSR_MAGIC), num_states=np.int64(w.num_states),
+             start=np.int64(w.start), row_ptr=w.row_ptr, eps_end=w.eps_end, dst=w.dst,
+             ilabel=w.ilabel, olabel=w.olabel, weight=w.weight, final_w=w.final_w,
+             eps_cycle_states=np.array(cyc.states if cyc else [], np.int64),
+             eps_cycle_weight=np.float64(cyc.total_weight if cyc else np.nan),
+             has_eps_cycle=np.bool_(cyc is not None))
+
+
+def load_wfst_binary(path) -> Wfst:
+    """Inverse of ``save_wfst_binary``; the arrays are checked for CSR consistency (and
+    re-sorted if a foreign writer left them unsorted) but not re-parsed."""
+    with np.load(path, allow_pickle=False) as z:
+        if "magic" not in z.files or str(z["magic"]) != _CSR_MAGIC:
+            raise WfstError(f"{path}: not a {_CSR_MAGIC} file")
+        S = int(z["num_states"])
+        row_ptr = z["row_ptr"].astype(np.int64)
+        if row_ptr.shape != (S + 1,) or row_ptr[0] != 0 or (np.diff(row_ptr) < 0).any():
+            raise WfstError(f"{path}: corrupt row_ptr")
+        A = int(row_ptr[-1])
+        arrs = [z[k] for k in ("dst", "ilabel", "olabel", "weight")]
+        if any(a.shape != (A,) for a in arrs):
+            raise WfstError(f"{path}: arc arrays disagree with row_ptr")
+        src = np.repeat(np.arange(S, dtype=np.int64), np.diff(row_ptr))
+        w = Wfst.from_arrays(S, int(z["start"]), src, *arrs, z["final_w"])
+        if not np.array_equal(w.eps_end, z["eps_end"]):
+            raise WfstError(f"{path}: corrupt eps_end")
+        w._eps_cycle_checked = True
+        w._eps_cycle = (EpsilonCycle(tuple(int(x) for x in z["eps_cycle_states"]),
+                                     float(z["eps_cycle_weight"]))
+                        if bool(z["has_eps_cycle"]) else None)
+    return w
 
 
 def graph_nbytes(w: Wfst) -> int:
@@ -410,5 +588,6 @@ def graph_nbytes(w: Wfst) -> int:
     return int(w.num_states * (4 + 4 + 8) + 4 + w.num_arcs * (16 + 4))
 
 
-__all__ = ["Arc", "EpsilonCycle", "ParseError", "Wfst", "WfstError", "parse_wfst_text",
+__all__ = ["Arc", "EpsilonCycle", "ParseError", "SymbolError", "SymbolTable", "Wfst", "WfstError",
+           "format_wfst_text", "load_wfst_binary", "parse_wfst_text", "save_wfst_binary",
            "validate_epsilon_acyclic", "EPSILON", "ZERO", "ONE"]

@@ -209,11 +209,11 @@ def test_native_wfst_parser_matches_python_parser():
 def test_native_wfst_parser_falls_back_exactly():
     """Malformed / unusual text goes to the Python parser, which raises like the reference."""
     from paper_1808_00687_b200 import wfst as W
-    from paper_1808_00687_b200.wfst import ParseError
+    from paper_1808_00687_b200.wfst import ParseError, SymbolError
     for bad in ("0 1 2\n", "0 1 a b\n", "0 1 2 3 nan\n", "0 1 2 3 -1\n", "", "# only\n",
                 "0 1 2 3 0x1p3\n", "-1 2 3 4\n"):
         assert W._parse_fast(bad, False) is None
-        with pytest.raises((ParseError, ValueError)):
+        with pytest.raises((ParseError, SymbolError, ValueError)):   # "a": SymbolError
             parse_wfst_text(bad)
     assert W._parse_fast("0 1 2 3 1_0\n", False) is None        # Python's float accepts it
     assert parse_wfst_text("0 1 2 3 1_0\n").weight.tolist() == [10.0]
