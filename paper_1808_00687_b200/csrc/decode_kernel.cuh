@@ -84,6 +84,9 @@ struct WorkDev {
     int stage_off;        // dyn-smem byte offset of the per-lane arc prefetch buffers (0 = off)
     int beam_skip;        // expand skips relaxations provably outside the beam
     int exact_min;        // token-filtered exact emitting-minimum pass (needs a non-negative row)
+    int xchg_gather;      // gather reads and resets each slot with one 128-bit atomic exchange
+                          // (2: with an L2 evict-first policy -- the line is dead until the
+                          // state's next touch; 0: load + store)
     // ---- lattice recording (LatticeRecorder / build_lattice, lattice.py:96-249)
     int *tok_eps;         // [slots][2][cap] epsilon-range start of each token's state
     u32 *sbits;           // [slots][ceil(S/32)] survivor bitmap of the current node step (L2-resident)
@@ -141,6 +144,7 @@ struct Smem {
     int n_log;          // relaxations logged this step (lattice mode)
     u64 run_min;        // smallest emitting relaxation key seen so far this step
     int best_tok;       // a live token of minimal cost (its arcs seed run_min); -1 = unknown
+    int next_chunk;     // expand: next unclaimed 32-token chunk (warps claim chunks dynamically)
     int ready_seen;     // streaming: last ready count read for the current utterance
     u64 thr_key;
     u32 thr_state;
@@ -405,12 +409,23 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
                 const u64 rm0 = sh_run_min();
                 const double bound = rm0 == EMPTY_KEY ? INFINITY : key_cost(rm0);
                 u64 m = EMPTY_KEY;
-                for (int ch = w; ch < nchunks; ch += NW) {
-                    const int t = (ch << 5) + l;
+                for (int ch0 = w; ch0 < nchunks; ch0 += 2 * NW) {
+                  // token costs of two chunks in flight; token records only where a token passes
+                  double tcs[2];
+#pragma unroll
+                  for (int q = 0; q < 2; ++q) {
+                    const int t = ((ch0 + q * NW) << 5) + l;
+                    tcs[q] = t < n_live ? tcost[t] : INFINITY;
+                  }
+#pragma unroll
+                  for (int q = 0; q < 2; ++q) {
+                    const int t = ((ch0 + q * NW) << 5) + l;
+                    const double tc = tcs[q];
+                    const bool pass = tc < bound && t != bt;
+                    if (!__any_sync(FULL, pass)) continue;
                     int4 ti = make_int4(0, 0, 0, 0);
-                    double tc = 0.0;
-                    if (t < n_live) { ti = tinfo[t]; tc = tcost[t]; }
-                    const int deg = (t < n_live && tc < bound && t != bt) ? ti.w - ti.z : 0;
+                    if (pass) ti = tinfo[t];
+                    const int deg = pass ? ti.w - ti.z : 0;
                     const int incl = warp_incl_scan(deg);
                     const int total = __shfl_sync(FULL, incl, 31);
                     const int excl = incl - deg;
@@ -428,6 +443,7 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
                             }
                         }
                     }
+                  }
                 }
                 m = warp_min_u64(m);
                 if (l == 0 && m < sh_run_min()) atomicMin(reinterpret_cast<unsigned long long *>(&SH<BLOCK>().run_min), m);
@@ -441,7 +457,11 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
             if (rm != EMPTY_KEY) exact_thr = cost_key(__dadd_rn(key_cost(rm), beam));
         }
         const u32 s0 = (u32)__cvta_generic_to_shared(stage);
-        for (int ch = w; ch < nchunks; ch += NW) {
+        // warps claim 32-token chunks dynamically (first chunk = warp id), so no warp idles at
+        // the closing barrier while another still has two chunks to go
+        for (int ch = w; ch < nchunks;) {
+            int ch_claim = 0;
+            if (l == 0) ch_claim = atomicAdd(&SH<BLOCK>().next_chunk, 1);  // used after this chunk
             const int t = (ch << 5) + l;
             int4 ti = make_int4(0, 0, 0, 0);
             double tc = 0.0;
@@ -523,6 +543,7 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
                 warp_append<BLOCK>(first, (u32)rec.x, r1, true, g, ws, front0);
             }
             asm volatile("cp.async.wait_all;" ::: "memory");
+            ch = __shfl_sync(FULL, ch_claim, 0);
         }
         return ExpandCounts{a_emit, a_fin};
     }
@@ -859,7 +880,10 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
 #pragma unroll
         for (int q = 0; q < Tune<BLOCK>::GATHER; ++q) {
             int i = i0 + q * BLOCK;
-            if (i < n_cand) v[q] = ld_slot(&c.slot()[st[q]]);
+            if (i < n_cand) {
+                if (ws.xchg_gather) v[q] = xchg_slot_empty(&c.slot()[st[q]], ws.xchg_gather > 1);
+                else v[q] = ld_slot(&c.slot()[st[q]]);
+            }
         }
 #pragma unroll
         for (int q = 0; q < Tune<BLOCK>::GATHER; ++q) {
@@ -869,7 +893,7 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
                 c.cand_arc()[i] = v[q].arcp1;
                 c.cand_pay()[i] = v[q].pay;
                 ca[i] = 0u;
-                st_slot_empty(&c.slot()[st[q]]);
+                if (!ws.xchg_gather) st_slot_empty(&c.slot()[st[q]]);
                 mn = v[q].key < mn ? v[q].key : mn;
                 mx = v[q].key > mx ? v[q].key : mx;
             }
@@ -1600,6 +1624,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             }
             if (threadIdx.x == 0) {
                 sh.n_cand = 0; sh.n_front = 0; sh.overflow = 0; sh.n_log = 0; sh.run_min = EMPTY_KEY;
+                sh.next_chunk = BLOCK / 32;
             }
             const bool row_nonneg = !__syncthreads_or(neg);
             tick<BLOCK>(0);

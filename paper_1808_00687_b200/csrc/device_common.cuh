@@ -47,6 +47,38 @@ __device__ __forceinline__ void st_slot_empty(Slot *p) {
     __stcg(reinterpret_cast<ulonglong2 *>(p), make_ulonglong2(EMPTY_KEY, EMPTY_KEY));
 }
 
+// Read a slot and reset it to EMPTY in one 128-bit atomic exchange (one L2 round trip instead
+// of a load plus a store).
+__device__ __forceinline__ Slot xchg_slot_empty(Slot *p, bool evict_first) {
+    const u64 e = EMPTY_KEY;
+    u64 olo, ohi;
+    if (evict_first) {  // the reset line is dead until the state's next (random) touch
+        asm volatile(
+            "{\n\t.reg .b128 d, o;\n\t.reg .b64 pol;\n\t"
+            "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+            "mov.b128 d, {%2, %3};\n\t"
+            "atom.relaxed.gpu.global.exch.L2::cache_hint.b128 o, [%4], d, pol;\n\t"
+            "mov.b128 {%0, %1}, o;\n\t}"
+            : "=l"(olo), "=l"(ohi)
+            : "l"(e), "l"(e), "l"(p)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .b128 d, o;\n\t"
+            "mov.b128 d, {%2, %3};\n\t"
+            "atom.relaxed.gpu.global.exch.b128 o, [%4], d;\n\t"
+            "mov.b128 {%0, %1}, o;\n\t}"
+            : "=l"(olo), "=l"(ohi)
+            : "l"(e), "l"(e), "l"(p)
+            : "memory");
+    }
+    Slot o;
+    o.key = olo;
+    o.arcp1 = (u32)ohi;
+    o.pay = (u32)(ohi >> 32);
+    return o;
+}
+
 // 128-bit compare-and-swap (ATOMG.E.CAS.128).  Returns the previous value.
 __device__ __forceinline__ Slot cas_slot(Slot *p, const Slot &expect, const Slot &desired) {
     u64 elo = expect.key, ehi = ((u64)expect.pay << 32) | expect.arcp1;

@@ -316,6 +316,8 @@ static cudaError_t launch_decode(int max_grid, int num_sms, int num_cols, cudaSt
     wd.beam_skip = (bs && bs[0] == '0') ? 0 : 1;
     const char *em = std::getenv("WB_EXACT_MIN");
     wd.exact_min = (em && em[0] == '0') ? 0 : 1;
+    const char *xg = std::getenv("WB_XCHG_GATHER");
+    wd.xchg_gather = xg ? std::atoi(xg) : 2;
     size_t smem = hdr + std::max(wd.stage_off ? row_r + stage : row,
                                  (size_t)wd.smem_cands * (sizeof(u64) + sizeof(u32)));
     smem = (smem + 15) & ~(size_t)15;
