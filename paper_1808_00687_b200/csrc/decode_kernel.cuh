@@ -72,6 +72,8 @@ struct WorkDev {
     u64 *cand_key;        // [slots][cap] (used when a step overflows shared memory)
     u32 *cand_ca;         // [slots][cap]
     u32 *front;           // [slots][2][cap] frontier states / pending record list
+    int4 *frng;           // [slots][2][cap] frontier entry {candidate index | CA_NONE, eps_lo, eps_hi, 0}
+    int eps_dedup;        // epsilon frontier: drop repeated pushes of a state within a round
     int4 *tok_info;       // [slots][2][cap] {state, trace, emit_lo, emit_hi}
     double *tok_cost;     // [slots][2][cap]
     int *frames;          // [slots][T_cap]
@@ -269,6 +271,7 @@ struct Lane {
     __device__ __forceinline__ u64 *cand_key() const { return ws.cand_key + co(); }
     __device__ __forceinline__ u32 *cand_ca() const { return ws.cand_ca + co(); }
     __device__ __forceinline__ u32 *front(int k) const { return ws.front + 2 * co() + (size_t)k * ws.cap; }
+    __device__ __forceinline__ int4 *frng(int k) const { return ws.frng + 2 * co() + (size_t)k * ws.cap; }
     __device__ __forceinline__ int4 *tok_info(int k) const {
         return ws.tok_info + 2 * co() + (size_t)k * ws.cap;
     }
@@ -287,13 +290,13 @@ struct Lane {
 // {eps_lo, emit_lo, emit_hi} from the arc record.  Epsilon graphs: states with epsilon arcs
 // record their candidate index (frontier lookups) and, if `push`, join the frontier.
 template <int BLOCK>
-__device__ __forceinline__ void warp_append(bool first, u32 d, int4 rng, bool push,
-                                            const GraphDev &g, const WorkDev &ws,
-                                            u32 *front_out) {
+__device__ __forceinline__ int warp_append(bool first, u32 d, int4 rng, bool push,
+                                           const GraphDev &g, const WorkDev &ws,
+                                           u32 *front_out, int4 *frng_out) {
     Smem<BLOCK> &sh = SH<BLOCK>();
     const Lane c{ws};
     const u32 m = __ballot_sync(FULL, first);
-    if (!m) return;
+    if (!m) return -1;
     const int l = threadIdx.x & 31;
     const int leader = __ffs(m) - 1;
     int base = 0;
@@ -320,9 +323,14 @@ __device__ __forceinline__ void warp_append(bool first, u32 d, int4 rng, bool pu
             int fb = 0;
             if (l == lf) fb = atomicAdd(&sh.n_front, __popc(mf));
             fb = __shfl_sync(FULL, fb, lf);
-            if (pf) front_out[fb + __popc(mf & lanemask_lt())] = d;
+            if (pf) {
+                const int f = fb + __popc(mf & lanemask_lt());
+                front_out[f] = d;
+                frng_out[f] = make_int4(idx, rng.x, rng.y, 0);
+            }
         }
     }
+    return (first && idx < ws.cap) ? idx : -1;
 }
 
 // Install `want` in *p under the (cost, arc) total order, optimistic first attempt already
@@ -370,6 +378,7 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
     const double *__restrict__ tcost = c.tok_cost(cur);
     Slot *slot = c.slot();
     u32 *front0 = c.front(0);
+    int4 *frng0 = c.frng(0);
     const int nchunks = (n_live + 31) >> 5;
     const Slot empty = {EMPTY_KEY, 0xFFFFFFFFu, 0xFFFFFFFFu};
     if (ws.stage_off) {
@@ -540,7 +549,7 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
                 }
                 int4 r1 = make_int4(0, 0, 0, 0);
                 if (first) r1 = __ldg(&g.arcs[2 * arc + 1]);
-                warp_append<BLOCK>(first, (u32)rec.x, r1, true, g, ws, front0);
+                warp_append<BLOCK>(first, (u32)rec.x, r1, true, g, ws, front0, frng0);
             }
             asm volatile("cp.async.wait_all;" ::: "memory");
             ch = __shfl_sync(FULL, ch_claim, 0);
@@ -616,7 +625,7 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
                 }
                 int4 r1 = make_int4(0, 0, 0, 0);
                 if (first) r1 = __ldg(&g.arcs[2 * (want[u].arcp1 - 1u) + 1]);
-                warp_append<BLOCK>(first, (u32)rec[u].x, r1, true, g, ws, front0);
+                warp_append<BLOCK>(first, (u32)rec[u].x, r1, true, g, ws, front0, frng0);
             }
         }
     }
@@ -668,6 +677,8 @@ __noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev 
         tag_cur = tag;
         const u32 *fin = c.front(which);
         u32 *fout = c.front(which ^ 1);
+        const int4 *frin = c.frng(which);
+        int4 *frout = c.frng(which ^ 1);
         const int nchunks = (n_front + 31) >> 5;
         for (int ch = w; ch < nchunks; ch += NW) {
             int i = (ch << 5) + l;
@@ -675,12 +686,14 @@ __noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev 
             int lo = 0, deg = 0;
             double ucost = 0.0;
             if (i < n_front) {
+                // the entry carries the state's epsilon range (and its candidate index when the
+                // pusher knew it), so the arcs load alongside the slot
                 uu = fin[i];
+                const int4 fe = frin[i];
                 Slot us = ld_slot(&slot[uu]);
-                ui = min(c.cand_of()[uu], (u32)ws.cap - 1u);
-                int4 rg = c.cand_rng()[ui];
-                lo = rg.x;
-                deg = rg.y - rg.x;
+                ui = fe.x >= 0 ? (u32)fe.x : min(c.cand_of()[uu], (u32)ws.cap - 1u);
+                lo = fe.y;
+                deg = fe.z - fe.y;
                 ucost = key_cost(us.key);
             }
             int incl = warp_incl_scan(deg);
@@ -715,9 +728,10 @@ __noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev 
                 }
                 int4 r1 = make_int4(0, 0, 0, 0);
                 if (dec) r1 = __ldg(&g.arcs[2 * a + 1]);
-                warp_append<BLOCK>(first, (u32)rec.x, r1, false, g, ws, fout);
+                const int nidx = warp_append<BLOCK>(first, (u32)rec.x, r1, false, g, ws, fout, frout);
                 // states whose cost dropped (or that are new) re-relax their epsilon arcs
-                bool push = dec && r1.x < r1.y && atomicExch(&c.qtag()[rec.x], tag) != tag;
+                bool push = dec && r1.x < r1.y &&
+                            (!ws.eps_dedup || atomicExch(&c.qtag()[rec.x], tag) != tag);
                 const u32 mp = __ballot_sync(FULL, push);
                 if (mp) {
                     const int lp = __ffs(mp) - 1;
@@ -726,8 +740,12 @@ __noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev 
                     fb = __shfl_sync(FULL, fb, lp);
                     int f = fb + __popc(mp & lanemask_lt());
                     if (push) {
-                        if (f < ws.cap) fout[f] = (u32)rec.x;
-                        else sh.overflow = 1;
+                        if (f < ws.cap) {
+                            fout[f] = (u32)rec.x;
+                            frout[f] = make_int4(nidx, r1.x, r1.y, 0);  // nidx -1: look it up
+                        } else {
+                            sh.overflow = 1;
+                        }
                     }
                 }
             }
@@ -1565,6 +1583,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             sh.n_front = 0;
             if (g.has_eps && g.start_rng.x < g.start_rng.y) {
                 c.front(0)[0] = (u32)g.start;
+                c.frng(0)[0] = make_int4(0, g.start_rng.x, g.start_rng.y, 0);
                 sh.n_front = 1;
             }
         }

@@ -52,6 +52,7 @@ struct wb_decoder_s {
     int4 *cand_rng = nullptr;
     u64 *cand_key = nullptr;
     u32 *front = nullptr;
+    int4 *frng = nullptr;
     int4 *tok_info = nullptr;
     double *tok_cost = nullptr;
     int *frames = nullptr;
@@ -199,7 +200,7 @@ int wb_graph_device_bytes(wb_graph_t g, int64_t *bytes) {
 
 static void free_decoder(wb_decoder_s *d) {
     void *ptrs[] = {d->slot, d->cand_of, d->qtag, d->tag_ctr, d->cand_state, d->cand_rng,
-                    d->cand_arc, d->cand_pay, d->cand_key, d->cand_ca, d->front, d->tok_info,
+                    d->cand_arc, d->cand_pay, d->cand_key, d->cand_ca, d->front, d->frng, d->tok_info,
                     d->tok_cost, d->frames, d->arena, d->counters, d->h_costs, d->h_blank,
                     d->h_off, d->h_crow, d->h_T, d->h_res, d->h_lab, d->tok_eps, d->sbits, d->snode,
                     d->ln_state, d->ln_out, d->ln_flag, d->la_src, d->la_dst, d->la_arc,
@@ -318,6 +319,8 @@ static cudaError_t launch_decode(int max_grid, int num_sms, int num_cols, cudaSt
     wd.exact_min = (em && em[0] == '0') ? 0 : 1;
     const char *xg = std::getenv("WB_XCHG_GATHER");
     wd.xchg_gather = xg ? std::atoi(xg) : 2;
+    const char *ed = std::getenv("WB_EPS_DEDUP");
+    wd.eps_dedup = ed ? std::atoi(ed) : 1;
     size_t smem = hdr + std::max(wd.stage_off ? row_r + stage : row,
                                  (size_t)wd.smem_cands * (sizeof(u64) + sizeof(u32)));
     smem = (smem + 15) & ~(size_t)15;
@@ -380,6 +383,7 @@ int wb_decoder_create(wb_graph_t g, const wb_decoder_opts *o, wb_decoder_t *out)
     DA(cand_key, slots * cap);
     DA(cand_ca, slots * cap);
     DA(front, slots * 2 * cap);
+    DA(frng, g->has_eps ? slots * 2 * cap : 1);
     DA(tok_info, slots * 2 * cap);
     DA(tok_cost, slots * 2 * cap);
     DA(counters, 4);
@@ -531,7 +535,7 @@ static int decode_impl(wb_decoder_t d, int32_t n, const double *costs, const int
     wd.slot = d->slot; wd.cand_of = d->cand_of; wd.qtag = d->qtag; wd.tag_ctr = d->tag_ctr;
     wd.cand_state = d->cand_state; wd.cand_rng = d->cand_rng; wd.cand_arc = d->cand_arc;
     wd.cand_pay = d->cand_pay; wd.cand_key = d->cand_key; wd.cand_ca = d->cand_ca;
-    wd.front = d->front; wd.tok_info = d->tok_info; wd.tok_cost = d->tok_cost;
+    wd.front = d->front; wd.frng = d->frng; wd.tok_info = d->tok_info; wd.tok_cost = d->tok_cost;
     wd.frames = d->frames;
     wd.arena = d->arena; wd.arena_cap = d->arena_cap;
     wd.utt_ctr = reinterpret_cast<u32 *>(d->counters + 1);
