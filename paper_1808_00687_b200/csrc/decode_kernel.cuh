@@ -45,12 +45,16 @@ __host__ __device__ constexpr int wb_cap(int cause) { return WB_ERR_CAPACITY | (
 #ifndef WB_UNROLL_1024
 #define WB_UNROLL_1024 1
 #endif
+#ifndef WB_GATHER_P1_1024
+#define WB_GATHER_P1_1024 2
+#endif
 #ifndef WB_GATHER_1024
 #define WB_GATHER_1024 2
 #endif
 template <int BLOCK> struct Tune {
     static constexpr int UNROLL = BLOCK >= 1024 ? WB_UNROLL_1024 : 4;
     static constexpr int GATHER = BLOCK >= 1024 ? WB_GATHER_1024 : 4;
+    static constexpr int GATHER_P1 = BLOCK >= 1024 ? WB_GATHER_P1_1024 : 4;  // slot exchange pass
 };
 
 struct GraphDev {
@@ -887,16 +891,17 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
     // P1: gather slot contents (batched loads), reset slots, min / max
     if (threadIdx.x == 0) sh.best_tok = -1;
     u64 mn = EMPTY_KEY, mx = 0;
-    for (int i0 = threadIdx.x; i0 < n_cand; i0 += BLOCK * Tune<BLOCK>::GATHER) {
-        u32 st[Tune<BLOCK>::GATHER];
-        Slot v[Tune<BLOCK>::GATHER];
+    constexpr int G1 = Tune<BLOCK>::GATHER_P1;
+    for (int i0 = threadIdx.x; i0 < n_cand; i0 += BLOCK * G1) {
+        u32 st[G1];
+        Slot v[G1];
 #pragma unroll
-        for (int q = 0; q < Tune<BLOCK>::GATHER; ++q) {
+        for (int q = 0; q < G1; ++q) {
             int i = i0 + q * BLOCK;
             if (i < n_cand) st[q] = c.cand_state()[i];
         }
 #pragma unroll
-        for (int q = 0; q < Tune<BLOCK>::GATHER; ++q) {
+        for (int q = 0; q < G1; ++q) {
             int i = i0 + q * BLOCK;
             if (i < n_cand) {
                 if (ws.xchg_gather) v[q] = xchg_slot_empty(&c.slot()[st[q]], ws.xchg_gather > 1);
@@ -904,7 +909,7 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
             }
         }
 #pragma unroll
-        for (int q = 0; q < Tune<BLOCK>::GATHER; ++q) {
+        for (int q = 0; q < G1; ++q) {
             int i = i0 + q * BLOCK;
             if (i < n_cand) {
                 ckey[i] = v[q].key;
