@@ -10,7 +10,7 @@ __version__ = "0.1.0"
 from .decoder import (BatchDecoder, BatchOutput, DecodeConfig, DecodeResult, DeviceGraph,
                       SearchDied, as_wfst, decode, decode_batch, decode_fsd, decode_lsd,
                       parallel_decode)
-from .lattice import LatticeError, LatticeRecorder
+from .lattice import LatticeError, LatticeRecorder, PipelinedLatticeBuilder
 from .posteriors import (BlankMask, PosteriorFormatError, PosteriorMatrix, acoustic_cost,
                          classify_blank_frames, cost_table, frame_costs, load_posteriors,
                          save_posteriors)
@@ -30,5 +30,5 @@ __all__ = [
     "parse_wfst_text", "validate_epsilon_acyclic", "load_posteriors", "save_posteriors",
     "EMPTY_LATTICE", "Lattice", "build_lattice", "lattice_best_path", "prune_lattice",
     "LatticePipeline", "decode_multi_device", "decode_sharded", "shard_utterances",
-    "SymbolError", "SymbolTable", "format_wfst_text", "load_wfst_binary", "save_wfst_binary",
+    "PipelinedLatticeBuilder", "SymbolError", "SymbolTable", "format_wfst_text", "load_wfst_binary", "save_wfst_binary",
 ]

@@ -297,6 +297,47 @@ class LatticeRecorder:
         self.final_step = final_step
         self.final_state = final_state
         self.reached_final = reached
+        if isinstance(self._consumer, PipelinedLatticeBuilder):
+            self._consumer._deliver(lat)
+
+
+class PipelinedLatticeBuilder:
+    """The reference's ``PipelinedLatticeBuilder`` (lattice.py:252-292), same use::
+
+        builder = PipelinedLatticeBuilder(wfst)
+        rec = LatticeRecorder(consumer=builder)
+        decode(wfst, posts, cfg, recorder=rec)      # or parallel_decode
+        lat = builder.result_from(rec)
+
+    The reference integrates step k on a consumer thread while the decoder works on step k+1
+    (the paper's second stream).  Here the decode kernel records and trims the lattice itself,
+    so nothing per step is left for a host thread; the builder receives the finished lattice
+    when the decode returns.  Overlap across whole batches is ``LatticePipeline``."""
+
+    def __init__(self, wfst=None):
+        self._wfst = wfst
+        self._lat = None
+        self._closed = False
+
+    def _deliver(self, lat: Lattice) -> None:
+        self._lat = lat
+
+    def feed(self, k: int, rec) -> None:
+        """Accepted for protocol compatibility; the device records every step itself."""
+
+    def close(self) -> None:
+        self._closed = True
+
+    def result(self, final_step: int, final_state: int, reached_final: bool) -> Lattice:
+        if self._lat is None:
+            raise LatticeError("no decode has delivered a lattice to this builder")
+        _check(self._lat)
+        return self._lat
+
+    def result_from(self, recorder: LatticeRecorder) -> Lattice:
+        if recorder.final_step is None:
+            raise LatticeError("decode trace is incomplete (finish was never recorded)")
+        return self.result(recorder.final_step, recorder.final_state, recorder.reached_final)
 
 
 def _check(lat: Lattice) -> None:
@@ -467,7 +508,7 @@ def load_lattice(path: str) -> Lattice:
 
 
 __all__ = ["COST_EPS", "EMPTY_LATTICE", "Lattice", "LatticeArc", "LatticeError", "LatticeNode",
-           "LatticeRecorder", "build_lattice", "canonical_batch", "canonical_from_device", "format_lattice_text",
+           "LatticeRecorder", "PipelinedLatticeBuilder", "build_lattice", "canonical_batch", "canonical_from_device", "format_lattice_text",
            "lattice_best_path", "load_lattice", "parse_lattice_text", "prune_lattice", "prune_lattices",
            "split_lattice",
            "save_lattice"]

@@ -259,3 +259,13 @@ def test_bench_report_json(cuda, tmp_path, capsys):
     assert cli.main(["bench", "--graph", g, "--posts", posts[0], "--repeats", "1",
                      "--modes", "lsd-gpu"]) == 0
     assert "lsd-gpu" in capsys.readouterr().out
+
+
+def test_pipelined_builder_without_decode_raises():
+    # lattice.py:289-292: result_from before the decode finished
+    from paper_1808_00687_b200 import LatticeError, LatticeRecorder, PipelinedLatticeBuilder
+    b = PipelinedLatticeBuilder(None)
+    with pytest.raises(LatticeError):
+        b.result_from(LatticeRecorder(consumer=b))
+    b.feed(0, None)
+    b.close()

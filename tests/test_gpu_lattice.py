@@ -105,6 +105,21 @@ def test_gpu_lattice_recorder_api(cuda):
         assert cost == r.total_cost and ol == r.olabels and il == r.ilabels
 
 
+def test_gpu_pipelined_builder_api(cuda):
+    """The reference's PipelinedLatticeBuilder use (cli.py:104-121): recorder(consumer=builder),
+    then builder.result_from(recorder) == build_lattice(recorder)."""
+    import paper_1808_00687_b200 as P
+    g = synth.random_wfst(4, 200, 800, 12, eps_fraction=0.05, final_fraction=0.2)
+    p = synth.random_posteriors(6, 30, 12)
+    builder = P.PipelinedLatticeBuilder(g)
+    rec = L.LatticeRecorder(consumer=builder)
+    P.parallel_decode(g, p, P.DecodeConfig(beam=8.0, mode="lsd"), workers=4, recorder=rec)
+    lat = builder.result_from(rec)
+    assert _key(lat) == _key(L.build_lattice(rec, g))
+    with pytest.raises(L.LatticeError):
+        P.PipelinedLatticeBuilder(g).result_from(L.LatticeRecorder())
+
+
 def test_gpu_lattice_capacity_retry(cuda):
     """Tiny raw-lattice / output pools overflow and are grown transparently."""
     g = synth.random_wfst(11, 300, 1200, 16, eps_fraction=0.05, final_fraction=0.1)
