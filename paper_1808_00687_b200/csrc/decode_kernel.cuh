@@ -361,6 +361,29 @@ __device__ __forceinline__ bool finish_relax(Slot *p, const Slot &want, Slot pre
     return false;
 }
 
+// Beam-skip pilot (one warp): the cheapest relaxation of live token `bt` against `row` lowers
+// the step's running minimum, an upper bound of its best cost.
+template <int BLOCK>
+__device__ __forceinline__ void pilot_min(int bt, int cur, const double *row, const GraphDev &g,
+                                          const WorkDev &ws) {
+    const Lane c{ws};
+    const int l = threadIdx.x & 31;
+    const int4 ti = c.tok_info(cur)[bt];
+    const double tc = c.tok_cost(cur)[bt];
+    u64 m = EMPTY_KEY;
+    for (int a = ti.z + l; a < ti.w; a += 32) {
+        const int4 r = ld_arc(&g.arcs[2 * a]);
+        const double ac = row[r.y];
+        if (ac != INFINITY) {
+            const u64 k = cost_key(__dadd_rn(__dadd_rn(tc, __hiloint2double(r.w, r.z)), ac));
+            m = k < m ? k : m;
+        }
+    }
+    m = warp_min_u64(m);
+    if (l == 0 && m < *(volatile u64 *)&SH<BLOCK>().run_min)
+        atomicMin(reinterpret_cast<unsigned long long *>(&SH<BLOCK>().run_min), m);
+}
+
 // Emitting expansion of all live tokens (viterbi_step's emitting loop, decoder.py:212-225;
 // parallel form parallel.py:257-283).  Per lane, UNROLL relaxations are in flight: their arc
 // loads, then their CAS attempts (optimistically expecting an empty slot -- most relaxations
@@ -372,7 +395,7 @@ struct ExpandCounts {
 template <int BLOCK>
 __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const double *row,
                                                      const GraphDev &g, const WorkDev &ws,
-                                                     double beam, bool row_nonneg) {
+                                                     double beam, bool row_nonneg, bool piloted) {
     const Lane c{ws};
     u32 a_emit = 0, a_fin = 0;
     constexpr int NW = BLOCK / 32;
@@ -397,22 +420,10 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
             // (1) pilot: evaluate (no CAS) the arcs of a cheapest live token, so the running
             // minimum -- an upper bound of the step's best cost -- is tight from the start
             const int bt = SH<BLOCK>().best_tok;
-            if (w == 0 && bt >= 0 && bt < n_live) {
-                const int4 ti = tinfo[bt];
-                const double tc = tcost[bt];
-                u64 m = EMPTY_KEY;
-                for (int a = ti.z + l; a < ti.w; a += 32) {
-                    const int4 r = ld_arc(&g.arcs[2 * a]);
-                    const double ac = row[r.y];
-                    if (ac != INFINITY) {
-                        const u64 k = cost_key(__dadd_rn(__dadd_rn(tc, __hiloint2double(r.w, r.z)), ac));
-                        m = k < m ? k : m;
-                    }
-                }
-                m = warp_min_u64(m);
-                if (l == 0 && m < sh_run_min()) atomicMin(reinterpret_cast<unsigned long long *>(&SH<BLOCK>().run_min), m);
+            if (!piloted) {  // (done by warp 0 during row staging when the row is staged)
+                if (w == 0 && bt >= 0 && bt < n_live) pilot_min<BLOCK>(bt, cur, row, g, ws);
+                __syncthreads();
             }
-            __syncthreads();
             // (2) exact minimum: with non-negative weights and acoustic costs a relaxation of
             // token t costs at least c_t, so only tokens cheaper than the pilot's minimum can
             // lower it -- usually a handful -- and the skip below then uses the step's final
@@ -1549,6 +1560,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
     const int slot_id = blockIdx.x;
     u32 tag = ws.tag_ctr[slot_id];
     const bool row_in_smem = ws.row_in_smem != 0;
+    const bool pilot_on = g.nonneg && cfg.beam < INFINITY && ws.beam_skip && ws.stage_off;
     double *srow = s_row<BLOCK>();
 
     for (;;) {
@@ -1638,23 +1650,32 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
                 }
             }
             int neg = !row_in_smem;  // acoustic costs of this row all >= 0? (checked while staging)
+            // Pilot of the beam skip (expand_emitting): warp 0 evaluates the arcs of a cheapest
+            // live token against the row in global memory while the other warps stage it.
+            const bool pilot = row_in_smem && pilot_on && sh.best_tok >= 0 && sh.best_tok < n_live;
+            if (threadIdx.x == 0) {
+                sh.n_cand = 0; sh.n_front = 0; sh.overflow = 0; sh.n_log = 0; sh.run_min = EMPTY_KEY;
+                sh.next_chunk = BLOCK / 32;
+            }
+            if (pilot && threadIdx.x < 32) {
+                __syncwarp();
+                pilot_min<BLOCK>(sh.best_tok, cur, grow, g, ws);
+            }
             if (row_in_smem) {
-                for (int q = threadIdx.x; q < b.L1; q += BLOCK) {
+                const int t0 = pilot ? (int)threadIdx.x - 32 : (int)threadIdx.x;
+                const int nt = pilot ? BLOCK - 32 : BLOCK;
+                for (int q = t0; q >= 0 && q < b.L1; q += nt) {
                     const double v = __ldg(&grow[q]);
                     neg |= v < 0.0;
                     srow[q] = v;
                 }
                 row = srow;
             }
-            if (threadIdx.x == 0) {
-                sh.n_cand = 0; sh.n_front = 0; sh.overflow = 0; sh.n_log = 0; sh.run_min = EMPTY_KEY;
-                sh.next_chunk = BLOCK / 32;
-            }
             const bool row_nonneg = !__syncthreads_or(neg);
             tick<BLOCK>(0);
             expanded += n_live;
             n_tok += n_live;
-            ExpandCounts ec = expand_emitting<BLOCK>(n_live, cur, row, g, ws, cfg.beam, row_nonneg);
+            ExpandCounts ec = expand_emitting<BLOCK>(n_live, cur, row, g, ws, cfg.beam, row_nonneg, pilot);
             a_emit += ec.a_emit;
             a_fin += ec.a_fin;
             __syncthreads();
