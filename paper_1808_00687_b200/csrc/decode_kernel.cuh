@@ -947,20 +947,21 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
         double top = cutoff < hi ? cutoff : hi;
         double range = __dsub_rn(top, best);
         if (range > 0.0 && range < INFINITY) scale = __ddiv_rn((double)NB, range);
-        for (int b = threadIdx.x; b < NB; b += BLOCK) sh.u.hist[b] = 0;
-        __syncthreads();
+        // count the beam survivors first (no atomics); the histogram only if max-active binds
         long long kept = 0;
-        for (int i = threadIdx.x; i < n_cand; i += BLOCK) {
-            double cst = key_cost(ckey[i]);
-            if (cst <= cutoff) {
-                ++kept;
-                atomicAdd(&sh.u.hist[bucket_of(cst, best, scale)], 1u);
-            }
-        }
+        for (int i = threadIdx.x; i < n_cand; i += BLOCK) kept += key_cost(ckey[i]) <= cutoff;
         kept = block_sum<BLOCK>(kept);
         need_select = kept > cfg.max_active;
-        if (need_select)
+        if (need_select) {
+            for (int b = threadIdx.x; b < NB; b += BLOCK) sh.u.hist[b] = 0;
+            __syncthreads();
+            for (int i = threadIdx.x; i < n_cand; i += BLOCK) {
+                const double cst = key_cost(ckey[i]);
+                if (cst <= cutoff) atomicAdd(&sh.u.hist[bucket_of(cst, best, scale)], 1u);
+            }
+            __syncthreads();
             select_threshold<BLOCK>(n_cand, cfg.max_active, best, cutoff, scale, ckey, ws);
+        }
     }
     tick<BLOCK>(4);
     const int bstar = need_select ? sh.thr_bucket : 0;
