@@ -183,3 +183,36 @@ def test_edge_cases_vs_oracle(cuda):
                          np.array([np.inf, 0.0, np.inf]))
     p = synth.random_posteriors(4, 5, 2)
     _check_batch(w, [p], P.DecodeConfig(beam=INF, mode="fsd"))
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_negative_weights_disable_the_skip_exactly(cuda, seed):
+    """Graphs with negative arc weights (parse_wfst_text(allow_negative_weights=True)): the
+    exact beam skip needs weights >= 0 and is off for them (GraphDev.nonneg); results still
+    equal the oracle's.  Epsilon arcs stay forward-only, so no epsilon cycle exists."""
+    from paper_1808_00687_b200.wfst import Wfst
+    g0 = synth.random_wfst(40 + seed, 400, 1800, 14, eps_fraction=0.05, selfloops=seed % 2 == 1,
+                           final_fraction=0.2)
+    rng = np.random.default_rng(seed)
+    w = g0.weight.copy()
+    flip = rng.random(len(w)) < 0.3
+    w[flip] = -np.round(rng.uniform(0.0, 0.5, int(flip.sum())), 6)
+    g = Wfst.from_arrays(g0.num_states, g0.start, g0.src, g0.dst, g0.ilabel, g0.olabel, w,
+                         g0.final_w)
+    assert g.epsilon_cycle() is None and (g.weight < 0).any()
+    posts = [synth.random_posteriors(300 * seed + k, 30 + 7 * k, 14, blank_fraction=0.3)
+             for k in range(6)]
+    for mode in ("fsd", "lsd"):
+        for beam, ma in ((6.0, 30), (INF, None), (3.0, None)):
+            _check_batch(g, posts, P.DecodeConfig(beam=beam, max_active=ma, mode=mode))
+
+
+def test_acoustic_scale_and_wide_beam_vs_oracle(cuda):
+    """Non-unit acoustic scales (costs = -scale * log p) with beams wide enough that the skip
+    rarely fires, and narrow ones where it fires on most relaxations."""
+    g = synth.random_wfst(77, 1500, 6000, 25, eps_fraction=0.03, final_fraction=0.1)
+    posts = [synth.random_posteriors(900 + k, 60, 25, blank_fraction=0.2) for k in range(5)]
+    for scale in (0.3, 1.7):
+        for beam in (1.5, 40.0):
+            _check_batch(g, posts, P.DecodeConfig(beam=beam, max_active=200, mode="fsd",
+                                                  acoustic_scale=scale))
