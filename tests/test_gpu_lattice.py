@@ -222,3 +222,49 @@ def test_gpu_device_prune_batch_matches_host_prune(cuda):
                     except L.LatticeError:
                         want = "error"
                     assert ("error" if isinstance(b, L.LatticeError) else _key(b)) == want, (seed, mode, lb)
+
+
+def test_gpu_lattices_with_negative_weights(cuda):
+    """Negative arc weights (beam skip off): device lattices equal the oracle's build_lattice
+    and device-pruned lattices equal the host prune_lattice of them."""
+    from paper_1808_00687_b200.posteriors import cost_table
+    from paper_1808_00687_b200.wfst import Wfst
+    for seed in range(2):
+        g0 = synth.random_wfst(60 + seed, 300, 1200, 16, eps_fraction=0.06, selfloops=True,
+                               final_fraction=0.1)
+        rng = np.random.default_rng(seed)
+        w = g0.weight.copy()
+        flip = rng.random(len(w)) < 0.3
+        w[flip] = -np.round(rng.uniform(0.0, 0.5, int(flip.sum())), 6)
+        g = Wfst.from_arrays(g0.num_states, g0.start, g0.src, g0.dst, g0.ilabel, g0.olabel, w,
+                             g0.final_w)
+        posts = [synth.random_posteriors(700 * seed + i, 12 + 5 * i, 16, blank_fraction=0.3)
+                 for i in range(8)]
+        costs = [cost_table(p) for p in posts]
+        blanks = [np.ascontiguousarray(p.rows[:, 0]) for p in posts]
+        cfg = DecodeConfig(beam=7.0, max_active=40, mode="lsd")
+        out, lats = _decode_lattices(g, costs, blanks, cfg)
+        for i, (c, b) in enumerate(zip(costs, blanks)):
+            try:
+                _, olat = O.decode(g, c, b, beam=7.0, max_active=40, mode="lsd",
+                                   return_lattice=True)
+                exp = olat.key() if not olat.empty else ("EMPTY",)
+            except O.OracleLatticeError:
+                with pytest.raises(L.LatticeError):
+                    L._check(lats[i])
+                continue
+            assert lats[i].key() == exp, (seed, i)
+        T = np.asarray([len(x) for x in costs], np.int32)
+        off = np.zeros(len(T), np.int64)
+        np.cumsum(T[:-1], out=off[1:])
+        dec = BatchDecoder(g, 0, max_utts_in_flight=4)
+        for lb in (1.0, 6.0):
+            dec.decode_host(np.concatenate(costs), off, T, np.concatenate(blanks), cfg, "lsd",
+                            lattice=True, lattice_beam=lb)
+            got = dec.fetch_pruned_lattices(g, lb)
+            for a, b in zip(lats, got):
+                try:
+                    want = _key(L.prune_lattice(a, lb))
+                except L.LatticeError:
+                    want = "error"
+                assert ("error" if isinstance(b, L.LatticeError) else _key(b)) == want, (seed, lb)
