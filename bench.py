@@ -259,6 +259,7 @@ def main():
     ap.add_argument("--utts", type=int, default=0, help="utterances per GPU (default: config)")
     ap.add_argument("--frames", type=int, default=0, help="frames per utterance (default: config)")
     ap.add_argument("--block", type=int, default=0, help="threads per CTA (0 = library default)")
+    ap.add_argument("--lanes", type=int, default=0, help="utterances decoded concurrently per GPU (0 = min(utts, 148))")
     ap.add_argument("--max-active", type=int, default=0, help="override the config's max-active (tuning)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -316,7 +317,7 @@ def main():
     dcfg = DecodeConfig(beam=cfg["beam"], max_active=cfg["max_active"], mode=cfg["mode"])
 
     block = args.block or 1024
-    dec = BatchDecoder(g, local, max_utts_in_flight=min(utts, 148), block_threads=args.block)
+    dec = BatchDecoder(g, local, max_utts_in_flight=args.lanes or min(utts, 148), block_threads=args.block)
     lat_on = cfg.get("lattice_beam") is not None
     dec.reserve(int(T.sum()) + utts, cfg["max_active"], int(T.max()), lattice=lat_on)
     cap = frames + 64

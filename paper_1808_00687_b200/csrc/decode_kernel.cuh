@@ -51,10 +51,19 @@ __host__ __device__ constexpr int wb_cap(int cause) { return WB_ERR_CAPACITY | (
 #ifndef WB_GATHER_1024
 #define WB_GATHER_1024 2
 #endif
+// CTAs per SM the 512-thread variant is compiled for (2: two lanes per SM at 64 registers)
+#ifndef WB_MINB_512
+#define WB_MINB_512 1
+#endif
+#ifndef WB_MINB_256
+#define WB_MINB_256 1
+#endif
 template <int BLOCK> struct Tune {
-    static constexpr int UNROLL = BLOCK >= 1024 ? WB_UNROLL_1024 : 4;
-    static constexpr int GATHER = BLOCK >= 1024 ? WB_GATHER_1024 : 4;
-    static constexpr int GATHER_P1 = BLOCK >= 1024 ? WB_GATHER_P1_1024 : 4;  // slot exchange pass
+    static constexpr int MINB = BLOCK == 512 ? WB_MINB_512 : BLOCK == 256 ? WB_MINB_256 : 1;
+    static constexpr bool R64 = BLOCK * MINB >= 1024;  // 64-register budget
+    static constexpr int UNROLL = R64 ? WB_UNROLL_1024 : 4;
+    static constexpr int GATHER = R64 ? WB_GATHER_1024 : 4;
+    static constexpr int GATHER_P1 = R64 ? WB_GATHER_P1_1024 : 4;  // slot exchange pass
 };
 
 struct GraphDev {
@@ -1552,7 +1561,7 @@ __device__ __noinline__ void backtrace(const GraphDev &g, const u64 *arena, long
 }
 
 template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK, 1)
+__global__ void __launch_bounds__(BLOCK, Tune<BLOCK>::MINB)
 decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDev ws,
               const __grid_constant__ BatchDev b, const __grid_constant__ CfgDev cfg,
               wb_utt_result *res) {
