@@ -87,6 +87,7 @@ struct WorkDev {
     u32 *front;           // [slots][2][cap] frontier states / pending record list
     int4 *frng;           // [slots][2][cap] frontier entry {candidate index | CA_NONE, eps_lo, eps_hi, 0}
     int eps_dedup;        // epsilon frontier: drop repeated pushes of a state within a round
+    int ma_early;         // expand: max-active early cutoff (cheaper tokens first, see expand)
     int4 *tok_info;       // [slots][2][cap] {state, trace, emit_lo, emit_hi}
     double *tok_cost;     // [slots][2][cap]
     int *frames;          // [slots][T_cap]
@@ -161,6 +162,9 @@ struct Smem {
     int best_tok;       // a live token of minimal cost (its arcs seed run_min); -1 = unknown
     int next_chunk;     // expand: next unclaimed 32-token chunk (warps claim chunks dynamically)
     int ready_seen;     // streaming: last ready count read for the current utterance
+    double tok_lo, tok_hi;  // cost range of the current live tokens (from the last prune)
+    float ma_frac;          // max-active early cutoff: split point in [tok_lo, tok_hi]
+    u64 ma_thr;             // its bound key for the step
     u64 thr_key;
     u32 thr_state;
     u64 arena_base;
@@ -401,10 +405,81 @@ struct ExpandCounts {
     u32 a_emit, a_fin;
 };
 
+__device__ __forceinline__ int bucket_of(double cst, double best, double scale);
+
+// Max-active early cutoff (exact).  Candidate costs only fall and the candidate set only grows
+// during a step, so once >= max_active candidates are registered, the largest first-install key
+// among the max_active cheapest of them bounds the step's final max-active cutoff from above
+// (decoder.py:188-191 keeps the first max_active by (cost, state)): a relaxation costing more
+// cannot survive, and with non-negative weights nothing reached from it by epsilon arcs can.
+// Called between the two token passes of expand_emitting; returns the bound key (EMPTY_KEY =
+// fewer than max_active candidates).  cand_key holds each candidate's first-install key.
+template <int BLOCK>
+__device__ __noinline__ u64 ma_bound(int max_active, const WorkDev &ws) {
+    Smem<BLOCK> &sh = SH<BLOCK>();
+    const Lane c{ws};
+    const int n = min(sh.n_cand, ws.cap);
+    if (n < max_active) return EMPTY_KEY;
+    const u64 *ck = c.cand_key();
+    u64 mn = EMPTY_KEY, mx = 0;
+    for (int i = threadIdx.x; i < n; i += BLOCK) {
+        const u64 k = ck[i];
+        mn = k < mn ? k : mn;
+        mx = k > mx ? k : mx;
+    }
+    block_minmax<BLOCK>(mn, mx);
+    const double lo = key_cost(mn), hi = key_cost(mx);
+    const double range = __dsub_rn(hi, lo);
+    if (!(range > 0.0 && range < INFINITY)) return EMPTY_KEY;
+    const double scale = __ddiv_rn((double)NB, range);
+    for (int b = threadIdx.x; b < NB; b += BLOCK) sh.u.hist[b] = 0;
+    if (threadIdx.x == 0) { sh.ma_thr = 0; sh.thr_bucket = NB - 1; }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += BLOCK) atomicAdd(&sh.u.hist[bucket_of(key_cost(ck[i]), lo, scale)], 1u);
+    __syncthreads();
+    constexpr int PER = NB / BLOCK;
+    constexpr int NW = BLOCK / 32;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    u32 loc[PER], tot = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) { loc[q] = sh.u.hist[threadIdx.x * PER + q]; tot += loc[q]; }
+    const int incl = warp_incl_scan((int)tot);
+    if (l == 31) sh.wa[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        const int v = l < NW ? sh.wa[l] : 0;
+        const int iv = warp_incl_scan(v);
+        if (l < NW) sh.wa[l] = iv - v;
+    }
+    __syncthreads();
+    u32 run = sh.wa[w] + incl - tot;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        if (run < (u32)max_active && run + loc[q] >= (u32)max_active) sh.thr_bucket = threadIdx.x * PER + q;
+        run += loc[q];
+    }
+    __syncthreads();
+    const int bstar = sh.thr_bucket;
+    u64 m = 0;
+    for (int i = threadIdx.x; i < n; i += BLOCK) {
+        const u64 k = ck[i];
+        if (bucket_of(key_cost(k), lo, scale) <= bstar && k > m) m = k;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const u64 x = __shfl_xor_sync(FULL, m, o);
+        m = x > m ? x : m;
+    }
+    if (l == 0 && m) atomicMax(reinterpret_cast<unsigned long long *>(&sh.ma_thr), (unsigned long long)m);
+    __syncthreads();
+    return sh.ma_thr ? sh.ma_thr : EMPTY_KEY;
+}
+
 template <int BLOCK>
 __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const double *row,
                                                      const GraphDev &g, const WorkDev &ws,
-                                                     double beam, bool row_nonneg, bool piloted) {
+                                                     double beam, bool row_nonneg, bool piloted,
+                                                     int max_active) {
     const Lane c{ws};
     u32 a_emit = 0, a_fin = 0;
     constexpr int NW = BLOCK / 32;
@@ -490,6 +565,28 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
             if (rm != EMPTY_KEY) exact_thr = cost_key(__dadd_rn(key_cost(rm), beam));
         }
         const u32 s0 = (u32)__cvta_generic_to_shared(stage);
+        // max-active early cutoff: pass 0 expands the tokens up to a split cost, ma_bound
+        // turns the candidates it registered into a bound, pass 1 expands the rest against it
+        const bool ma_on = ws.ma_early > 0 && n_live >= ws.ma_early && max_active > 0 && !ws.rlog &&
+                           g.nonneg && ws.beam_skip;
+        u64 ma_thr = EMPTY_KEY;
+        double split = INFINITY;
+        if (ma_on) {
+            const Smem<BLOCK> &sh = SH<BLOCK>();
+            split = __dadd_rn(sh.tok_lo, (double)sh.ma_frac * __dsub_rn(sh.tok_hi, sh.tok_lo));
+        }
+        for (int pass = 0; pass < (ma_on ? 2 : 1); ++pass) {
+        if (pass == 1) {
+            __syncthreads();  // pass 0's registrations and first-install keys are visible
+            const u64 mb = ma_bound<BLOCK>(max_active, ws);
+            if (threadIdx.x == 0) {
+                Smem<BLOCK> &sh = SH<BLOCK>();
+                sh.ma_frac = mb != EMPTY_KEY ? fmaxf(0.05f, sh.ma_frac - 0.02f) : fminf(1.0f, sh.ma_frac + 0.1f);
+                sh.next_chunk = NW;
+            }
+            ma_thr = mb;
+            __syncthreads();
+        }
         // warps claim 32-token chunks dynamically (first chunk = warp id), so no warp idles at
         // the closing barrier while another still has two chunks to go
         for (int ch = w; ch < nchunks;) {
@@ -499,7 +596,8 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
             int4 ti = make_int4(0, 0, 0, 0);
             double tc = 0.0;
             if (t < n_live) { ti = tinfo[t]; tc = tcost[t]; }
-            const int deg = t < n_live ? ti.w - ti.z : 0;
+            const bool in_pass = !ma_on || ((tc <= split) == (pass == 0));
+            const int deg = (t < n_live && in_pass) ? ti.w - ti.z : 0;
             a_emit += deg;
             const int incl = warp_incl_scan(deg);
             const int total = __shfl_sync(FULL, incl, 31);
@@ -566,6 +664,7 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
                     if (relax && rm != EMPTY_KEY && want.key > cost_key(__dadd_rn(key_cost(rm), beam)))
                         relax = false;
                 }
+                if (want.key > ma_thr) relax = false;  // max-active early cutoff (ma_bound)
                 if (act) a_fin++;
                 if (relax) {
                     const Slot prev = cas_slot(&slot[rec.x], empty, want);
@@ -573,10 +672,12 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
                 }
                 int4 r1 = make_int4(0, 0, 0, 0);
                 if (first) r1 = __ldg(&g.arcs[2 * arc + 1]);
-                warp_append<BLOCK>(first, (u32)rec.x, r1, true, g, ws, front0, frng0);
+                const int ci = warp_append<BLOCK>(first, (u32)rec.x, r1, true, g, ws, front0, frng0);
+                if (ma_on && pass == 0 && ci >= 0) c.cand_key()[ci] = want.key;
             }
             asm volatile("cp.async.wait_all;" ::: "memory");
             ch = __shfl_sync(FULL, ch_claim, 0);
+        }
         }
         return ExpandCounts{a_emit, a_fin};
     }
@@ -973,6 +1074,11 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
         }
     }
     tick<BLOCK>(4);
+    if (threadIdx.x == 0) {  // cost range of the next live tokens (the early cutoff's split)
+        const double top = key_cost(mx) < cutoff ? key_cost(mx) : cutoff;
+        sh.tok_lo = best;
+        sh.tok_hi = need_select ? key_cost(sh.thr_key) : top;
+    }
     const int bstar = need_select ? sh.thr_bucket : 0;
     const u64 tkey = need_select ? sh.thr_key : 0;
     const u32 tst = need_select ? sh.thr_state : 0;
@@ -1581,6 +1687,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
         if (threadIdx.x < 8) sh.pc[threadIdx.x] = 0;
         if (threadIdx.x == 0) {
             sh.t_mark = clock64(); sh.arena_used = 0; sh.ready_seen = 0; sh.run_min = EMPTY_KEY;
+            sh.tok_lo = 0.0; sh.tok_hi = 0.0; sh.ma_frac = 0.5f;
         }
         const int T = b.T[u];
         const long long row0 = b.row_off[u];
@@ -1685,7 +1792,8 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             tick<BLOCK>(0);
             expanded += n_live;
             n_tok += n_live;
-            ExpandCounts ec = expand_emitting<BLOCK>(n_live, cur, row, g, ws, cfg.beam, row_nonneg, pilot);
+            ExpandCounts ec = expand_emitting<BLOCK>(n_live, cur, row, g, ws, cfg.beam, row_nonneg, pilot,
+                                                    cfg.max_active);
             a_emit += ec.a_emit;
             a_fin += ec.a_fin;
             __syncthreads();

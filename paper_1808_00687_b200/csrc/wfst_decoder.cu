@@ -321,6 +321,8 @@ static cudaError_t launch_decode(int max_grid, int num_sms, int num_cols, cudaSt
     wd.xchg_gather = xg ? std::atoi(xg) : 2;
     const char *ed = std::getenv("WB_EPS_DEDUP");
     wd.eps_dedup = ed ? std::atoi(ed) : 1;
+    const char *ma = std::getenv("WB_MA_EARLY");
+    wd.ma_early = ma ? std::atoi(ma) : 0;
     size_t smem = hdr + std::max(wd.stage_off ? row_r + stage : row,
                                  (size_t)wd.smem_cands * (sizeof(u64) + sizeof(u32)));
     smem = (smem + 15) & ~(size_t)15;

@@ -216,3 +216,15 @@ def test_acoustic_scale_and_wide_beam_vs_oracle(cuda):
         for beam in (1.5, 40.0):
             _check_batch(g, posts, P.DecodeConfig(beam=beam, max_active=200, mode="fsd",
                                                   acoustic_scale=scale))
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_max_active_early_cutoff_is_exact(cuda, seed, monkeypatch):
+    """WB_MA_EARLY (expand's max-active early cutoff, off by default) on every step: same
+    results as the oracle, with max-active binding hard and with beam = inf."""
+    monkeypatch.setenv("WB_MA_EARLY", "1")
+    g = synth.random_wfst(100 + seed, 5000, 16000, 50, eps_fraction=0.05, selfloops=True,
+                          final_fraction=0.05)
+    posts = [synth.random_posteriors(seed * 11 + k, 100, 50, blank_fraction=0.2) for k in range(6)]
+    for beam, ma in ((10.0, 40), (10.0, 300), (INF, 100)):
+        _check_batch(g, posts, P.DecodeConfig(beam=beam, max_active=ma, mode="fsd"))
