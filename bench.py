@@ -59,10 +59,10 @@ CONFIGS = {
               final_fraction=0.01, lattice_beam=8.0),
     "5": dict(name="config5: large synthetic graph 7M states/20M arcs/512 pdfs, 4096 utt x 1000 "
                    "frames in total sharded by utterance over the GPUs (strong scaling), beam 13, "
-                   "max-active 7000, FSD; 64 distinct posterior streams tiled",
+                   "max-active 7000, FSD; every utterance its own posterior stream",
               states=7_000_000, arcs=20_000_000, labels=512, utts=4096, frames=1000, beam=13.0,
               max_active=7000, mode="fsd", blank_fraction=0.0, eps=0.015, selfloops=False,
-              final_fraction=0.01, strong=True, distinct=64),
+              final_fraction=0.01, strong=True),
     "4": dict(name="config4: CTC LSD, 5k-label synthetic TLG-like graph (self-loops), 256 utt x "
                    "1500 frames, 80% blank frames, blank-skip threshold 0.98, beam 13, "
                    "max-active 7000", states=100_000, arcs=300_000, labels=5000, utts=256,
@@ -70,10 +70,26 @@ CONFIGS = {
               eps=0.015, selfloops=True, final_fraction=0.01),
 }
 
-# SURVEY 8d algorithmic bytes per step and utterance
-def algorithmic_bytes(r) -> int:
-    return int(24 * r["n_tok"].sum() + 24 * r["a_emit"].sum() + 16 * r["a_fin"].sum()
+# SURVEY 8d algorithmic bytes per step and utterance.  The 8d convention charges a 16-byte
+# slot update to every finite relaxation (a_fin); the exact beam skip leaves about half of
+# them without any slot access, so the headline fraction charges only the relaxations that
+# reached a slot (a_cas) and the 8d figure is reported beside it.
+def algorithmic_bytes(r, slot_term: str = "a_cas") -> int:
+    return int(24 * r["n_tok"].sum() + 24 * r["a_emit"].sum() + 16 * r[slot_term].sum()
                + 32 * r["e_eps"].sum() + 24 * r["n_cand"].sum() + 16 * r["n_surv"].sum())
+
+
+def kernel_source_hash() -> str:
+    """Hash of the decode kernel's sources: a committed ncu traffic figure is only used when
+    it was measured on exactly this kernel."""
+    import hashlib
+    h = hashlib.sha256()
+    csrc = os.path.join(ROOT, "paper_1808_00687_b200", "csrc")
+    for f in sorted(os.listdir(csrc)):
+        if f.endswith((".cu", ".cuh")):
+            with open(os.path.join(csrc, f), "rb") as fh:
+                h.update(f.encode() + b"\0" + fh.read())
+    return h.hexdigest()[:16]
 
 
 def peaks():
@@ -155,32 +171,26 @@ def make_workload(cfg: dict, rank: int, utts: int, frames: int):
     return g, L1, T, off, R
 
 
-def fill_inputs(cfg, rank, T, off, L1, costs_out, blank_out, ids=None):
-    """Cost table rows of each utterance (numpy -log, exactly frame_costs); ``ids`` are the
-    global utterance ids (strong scaling), ``cfg['distinct']`` tiles that many streams.
-    Returns the posterior matrices (the e2e input; tiled streams share one object)."""
+def fill_inputs(cfg, rank, T, off, L1, costs_out, blank_out, ids=None, keep_posts=True):
+    """Cost table rows of each utterance (numpy -log, exactly frame_costs) on host threads;
+    ``ids`` are the global utterance ids (strong scaling); utterance id u uses posterior seed
+    u + 1 (bench utterance i of rank 0 == the oracle sample's utterance i).  Returns the
+    posterior matrices (the e2e input) when ``keep_posts``."""
+    from concurrent.futures import ThreadPoolExecutor
     from paper_1808_00687_b200 import synth
     from paper_1808_00687_b200.posteriors import PosteriorMatrix, cost_table
-    distinct = cfg.get("distinct")
-    made = {}
-    posts = []
-    for i, (o, t) in enumerate(zip(off, T)):
+
+    def one(i):
+        o, t = int(off[i]), int(T[i])
         uid = int(ids[i]) if ids is not None else 1000 * rank + i
-        seed = (uid % distinct if distinct else uid) + 1
-        if seed in made:
-            src, p = made[seed]
-            costs_out[o:o + t] = costs_out[src:src + t]
-            blank_out[o:o + t] = blank_out[src:src + t]
-            posts.append(p)
-            continue
-        rows = synth.random_posterior_rows(seed, int(t), cfg["labels"],
+        rows = synth.random_posterior_rows(uid + 1, t, cfg["labels"],
                                            blank_fraction=cfg["blank_fraction"])
         p = PosteriorMatrix(rows, 0, validate=False)
         cost_table(p, 1.0, out=costs_out[o:o + t])
         blank_out[o:o + t] = rows[:, 0]
-        made[seed] = (o, p)
-        posts.append(p)
-    return posts
+        return p if keep_posts else None
+    with ThreadPoolExecutor(len(os.sched_getaffinity(0))) as ex:
+        return list(ex.map(one, range(len(T))))
 
 
 def cpu_sample(g, cfg, L1, n_threads: int, frames: int):
@@ -276,9 +286,15 @@ def main():
     if args.warmup < 0 or args.steps < 1:
         raise SystemExit("need --steps >= 1")
 
+    if args.utts or args.frames:   # the workload string names what is actually decoded
+        cfg["name"] += (f" [overridden: {args.utts or cfg['utts']} utt x "
+                        f"{args.frames or cfg['frames']} frames per GPU]")
+
     if args.impl == "reference":
-        import __graft_entry__
-        __graft_entry__.build()
+        # the CPU reference arm builds and loads only the oracle (oracle/liboracle.so); the
+        # product library is never built or mapped in this process
+        from oracle import oracle as O
+        O.build()
         run_reference(args, cfg, rank, world)
         return
 
@@ -313,7 +329,9 @@ def main():
     # pinned host inputs (the e2e path copies from these every step)
     costs_h = torch.empty((R, L1), dtype=torch.float64, pin_memory=True)
     blank_h = torch.empty(R, dtype=torch.float64, pin_memory=True)
-    posts = fill_inputs(cfg, rank, T, off, L1, costs_h.numpy(), blank_h.numpy(), ids)
+    keep_posts = not cfg.get("strong")   # config 5: 4096 streams, the posterior e2e is skipped
+    posts = fill_inputs(cfg, rank, T, off, L1, costs_h.numpy(), blank_h.numpy(), ids,
+                        keep_posts=keep_posts)
     dcfg = DecodeConfig(beam=cfg["beam"], max_active=cfg["max_active"], mode=cfg["mode"])
 
     block = args.block or 1024
@@ -385,6 +403,7 @@ def main():
     res = np.frombuffer(res_d.cpu().numpy().tobytes(), dtype=N.UTT_RESULT_DTYPE)
     relax = int(res["a_fin"].sum() + res["e_eps"].sum())
     nbytes = algorithmic_bytes(res)
+    nbytes_8d = algorithmic_bytes(res, "a_fin")
     avg_kernel_ms = sum(kernel_ms) / len(kernel_ms)
     peak, peak_src = peaks()
     achieved = nbytes / (avg_kernel_ms * 1e-3) / 1e9
@@ -469,7 +488,7 @@ def main():
     # (numpy -log, bit-exactness needs the host's own log) on host threads, streamed into the
     # running kernel through page-locked memory (wb_decode_stream)
     e2e_post = None
-    if not (args.no_e2e or args.profile or lat_on):
+    if not (args.no_e2e or args.profile or lat_on or not keep_posts):
         dec.decode_posteriors(posts, dcfg, cfg["mode"], cap)  # warm (page-locked buffers)
         p_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                 for _ in range(args.steps)]
@@ -489,29 +508,60 @@ def main():
         e2e_post = {"value": frames_all * args.steps / (p_ms / 1e3), "unit": "frames/s",
                     "ms_per_step": p_ms / args.steps,
                     "note": "posterior matrices in; host numpy log (rows in frame blocks, "
-                            "<= 8 threads) streamed into the running kernel"}
+                            "all host cores) streamed into the running kernel"}
 
     # ---------------- CPU baseline (oracle port, rank 0, N = 1)
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not (args.no_cpu or args.profile):
         n_thr = max(1, min(len(os.sched_getaffinity(0)), utts))
-        wall, nfr, _ = cpu_sample(g, cfg, L1, n_thr, frames)
+        wall, nfr, cpu_res = cpu_sample(g, cfg, L1, n_thr, frames)
         cpu = {"value": nfr / wall, "unit": "frames/s", "cores": n_thr, "kind": "port",
                "sample": f"{n_thr} utterances x {frames} frames (one full utterance per host "
                          f"thread) of the same workload, oracle/ C port of decoder.py"}
+        # the oracle decoded the same inputs as GPU utterances with posterior seed i + 1:
+        # compare every DecodeResult field of those utterances (timed device run's output)
+        olab = ol_d.cpu().numpy()
+        ilab = il_d.cpu().numpy()
+        seed_of = (np.asarray(ids) if ids is not None else np.arange(utts)) + 1
+        mism = []
+        checked = 0
+        for i, o in enumerate(cpu_res):
+            hit = np.flatnonzero(seed_of == i + 1)
+            if not len(hit):
+                continue
+            j = int(hit[0])
+            r = res[j]
+            no, ni = int(r["n_olabels"]), int(r["n_ilabels"])
+            got = (float(r["total_cost"]), tuple(int(x) for x in olab[j, :no]),
+                   tuple(int(x) for x in ilab[j, :ni]), int(r["search_steps"]),
+                   int(r["tokens_expanded"]), bool(r["reached_final"]),
+                   None if int(r["died_at_step"]) < 0 else int(r["died_at_step"]))
+            checked += 1
+            if got != o.astuple():
+                mism.append(j)
+        parity = {"checked": checked, "mismatches": len(mism), "mismatched_utts": mism[:8],
+                  "fields": "all 7 DecodeResult fields vs the oracle (reference-exact mode)"}
 
     if rank == 0:
         value = frames_all * args.steps / (total_ms / 1e3)
         traffic = None
+        traffic_note = "no ncu capture for this workload"
         tfile = os.path.join(ROOT, "profiles", "decode_traffic.json")
-        default_size = (not args.utts and not args.frames and not args.max_active
-                        and not cfg.get("strong"))
+        default_size = (not args.utts and not args.frames and not args.max_active)
+        src_sha = kernel_source_hash()
         if os.path.exists(tfile) and default_size:   # measured for the config's own sizes
             try:
                 with open(tfile) as fh:
-                    traffic = json.load(fh).get(cfg["name"])
+                    ent = json.load(fh).get(cfg["name"])
             except Exception:
-                traffic = None
+                ent = None
+            if isinstance(ent, dict) and ent.get("src_sha") == src_sha:
+                traffic = ent.get("bytes_per_launch")
+                traffic_note = ("ncu dram__bytes_read.sum + dram__bytes_write.sum of the decode "
+                                f"kernel built from these sources ({src_sha}), {ent.get('source')}")
+            elif ent is not None:
+                traffic_note = "the committed ncu capture is of another kernel build: not used"
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
@@ -529,16 +579,25 @@ def main():
             "rtf_note": "per-GPU batch wall / batch audio at an assumed 10 ms frame shift",
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         "traffic_note": traffic_note, "kernel_src_sha": src_sha,
                          "kernel": "decode_kernel", "kernel_ms": avg_kernel_ms,
-                         "algorithmic_bytes": nbytes, "peak_source": peak_src},
+                         "algorithmic_bytes": nbytes,
+                         "bytes_convention": "SURVEY 8d, slot term charged per relaxation "
+                                             "that reached a slot (a_cas)",
+                         "algorithmic_bytes_8d": nbytes_8d,
+                         "frac_8d": nbytes_8d / (avg_kernel_ms * 1e-3) / 1e9 / peak,
+                         "peak_source": peak_src},
+            "parity": parity,
             "cpu_baseline": cpu,
             "lattice": lat_stats,
             "e2e_from_posteriors": e2e_post,
             "e2e": e2e,
             "clocks": clocks,
-            "gpu_launches": args.steps,  # one persistent decode kernel per step (backtrace in-kernel)
+            # one persistent decode kernel per step (backtrace in-kernel) + the lattice prune
+            "gpu_launches": args.steps * (2 if lat_on else 1),
             "counters_per_step": {k: int(res[k].sum()) for k in
-                                  ("n_tok", "a_emit", "a_fin", "e_eps", "n_cand", "n_surv", "n_rec")},
+                                  ("n_tok", "a_emit", "a_fin", "a_cas", "e_eps", "n_cand",
+                                   "n_surv", "n_rec")},
             "phase_share": dict(zip(["stage_row", "expand", "eps_closure", "gather", "select",
                                      "flags", "compact", "other"],
                                     [round(float(x), 4) for x in

@@ -82,6 +82,12 @@ typedef struct {
                                 (stage one of prune_lattice, see wb_lattice_pruned_fetch); < 0 off */
 } wb_config;
 
+/* wb_utt_result.path_flags (evidence for tests: which prune branches ran) */
+#define WB_PATH_GLOBAL_CANDS 1  /* a step's candidate keys spilled from shared to global memory */
+#define WB_PATH_SELECT 2        /* max-active bound: the histogram select ran */
+#define WB_PATH_RADIX 4         /* ... and its boundary bucket was ranked by radix select */
+#define WB_PATH_PREFETCH 8      /* expand used the cp.async prefetch pipeline */
+
 /* Per-utterance result (DecodeResult, decoder.py:97-105) plus device counters. */
 typedef struct {
     double total_cost;
@@ -95,7 +101,7 @@ typedef struct {
     int32_t n_ilabels;
     int32_t status;          /* WB_OK or WB_ERR_CAPACITY */
     int32_t capacity_flags;  /* WB_CAP_* bits of a WB_ERR_CAPACITY utterance */
-    int32_t _pad;
+    int32_t path_flags;      /* WB_PATH_* bits: which prune code paths the utterance took */
     int64_t best_trace;      /* lane-arena index of the winning token's record */
     /* counters for the roofline: summed over the utterance's steps */
     int64_t n_tok;           /* live tokens expanded */
@@ -106,6 +112,7 @@ typedef struct {
     int64_t n_surv;          /* survivors */
     int64_t n_rec;           /* backpointer records written */
     int64_t lat_arcs;        /* raw lattice arcs recorded (lattice mode) */
+    int64_t a_cas;           /* emitting relaxations that reached a slot (not beam-skipped) */
     /* SM clock cycles spent per phase (CTA thread 0, measured after each phase barrier):
      * [0] cost-row staging, [1] emitting expansion, [2] epsilon closure, [3] candidate
      * gather + min/max, [4] max-active histogram/select, [5] survivor flags + chain marks,

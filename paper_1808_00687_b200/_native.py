@@ -21,6 +21,8 @@ WB_PARSE_FALLBACK = 7
 WB_MEM_DEVICE, WB_MEM_HOST = 0, 1
 (WB_CAP_CANDIDATES, WB_CAP_ARENA, WB_CAP_FRAMES, WB_CAP_LABELS, WB_CAP_LATTICE_RAW,
  WB_CAP_LATTICE_OUT, WB_CAP_EPS_ROUNDS, WB_CAP_STREAM) = (1, 2, 4, 8, 16, 32, 64, 128)
+# wb_utt_result.path_flags: prune / expand branches an utterance took (test evidence)
+WB_PATH_GLOBAL_CANDS, WB_PATH_SELECT, WB_PATH_RADIX, WB_PATH_PREFETCH = 1, 2, 4, 8
 
 
 class NativeError(RuntimeError):
@@ -71,10 +73,11 @@ UTT_RESULT_DTYPE = np.dtype([
     ("total_cost", np.float64), ("tokens_expanded", np.int64), ("search_steps", np.int32),
     ("reached_final", np.int32), ("died_at_step", np.int32), ("final_state", np.int32),
     ("final_step", np.int32), ("n_olabels", np.int32), ("n_ilabels", np.int32),
-    ("status", np.int32), ("capacity_flags", np.int32), ("_pad", np.int32),
+    ("status", np.int32), ("capacity_flags", np.int32), ("path_flags", np.int32),
     ("best_trace", np.int64), ("n_tok", np.int64), ("a_emit", np.int64),
     ("a_fin", np.int64), ("e_eps", np.int64), ("n_cand", np.int64), ("n_surv", np.int64),
-    ("n_rec", np.int64), ("lat_arcs", np.int64), ("phase_cycles", np.int64, (8,))])
+    ("n_rec", np.int64), ("lat_arcs", np.int64), ("a_cas", np.int64),
+    ("phase_cycles", np.int64, (8,))])
 
 _lib = None
 

@@ -88,6 +88,7 @@ struct WorkDev {
     int4 *frng;           // [slots][2][cap] frontier entry {candidate index | CA_NONE, eps_lo, eps_hi, 0}
     int eps_dedup;        // epsilon frontier: drop repeated pushes of a state within a round
     int ma_early;         // expand: max-active early cutoff (cheaper tokens first, see expand)
+    int force_radix;      // prune: radix-select every boundary bucket (test knob, WB_FORCE_RADIX)
     int4 *tok_info;       // [slots][2][cap] {state, trace, emit_lo, emit_hi}
     double *tok_cost;     // [slots][2][cap]
     int *frames;          // [slots][T_cap]
@@ -162,6 +163,7 @@ struct Smem {
     int best_tok;       // a live token of minimal cost (its arcs seed run_min); -1 = unknown
     int next_chunk;     // expand: next unclaimed 32-token chunk (warps claim chunks dynamically)
     int ready_seen;     // streaming: last ready count read for the current utterance
+    int pflags;         // WB_PATH_* bits of the current utterance (thread 0 writes)
     double tok_lo, tok_hi;  // cost range of the current live tokens (from the last prune)
     float ma_frac;          // max-active early cutoff: split point in [tok_lo, tok_hi]
     u64 ma_thr;             // its bound key for the step
@@ -402,7 +404,7 @@ __device__ __forceinline__ void pilot_min(int bt, int cur, const double *row, co
 // loads, then their CAS attempts (optimistically expecting an empty slot -- most relaxations
 // are first touches), are issued back to back.
 struct ExpandCounts {
-    u32 a_emit, a_fin;
+    u32 a_emit, a_fin, a_cas;
 };
 
 __device__ __forceinline__ int bucket_of(double cst, double best, double scale);
@@ -481,7 +483,7 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
                                                      double beam, bool row_nonneg, bool piloted,
                                                      int max_active) {
     const Lane c{ws};
-    u32 a_emit = 0, a_fin = 0;
+    u32 a_emit = 0, a_fin = 0, a_cas = 0;
     constexpr int NW = BLOCK / 32;
     constexpr int U = Tune<BLOCK>::UNROLL;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -667,6 +669,7 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
                 if (want.key > ma_thr) relax = false;  // max-active early cutoff (ma_bound)
                 if (act) a_fin++;
                 if (relax) {
+                    a_cas++;
                     const Slot prev = cas_slot(&slot[rec.x], empty, want);
                     finish_relax(&slot[rec.x], want, prev, &first, &dec);
                 }
@@ -679,7 +682,7 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
             ch = __shfl_sync(FULL, ch_claim, 0);
         }
         }
-        return ExpandCounts{a_emit, a_fin};
+        return ExpandCounts{a_emit, a_fin, a_cas};
     }
     for (int ch = w; ch < nchunks; ch += NW) {
         int t = (ch << 5) + l;
@@ -746,6 +749,7 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
                 bool first = false, dec = false;
                 if (act[u]) {
                     a_fin++;
+                    a_cas++;
                     finish_relax(&slot[rec[u].x], want[u], prev[u], &first, &dec);
                 }
                 int4 r1 = make_int4(0, 0, 0, 0);
@@ -754,7 +758,7 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
             }
         }
     }
-    return ExpandCounts{a_emit, a_fin};
+    return ExpandCounts{a_emit, a_fin, a_cas};
 }
 
 // Epsilon closure to a fixpoint by frontier rounds (decoder.py:138-171; parallel.py:287-325).
@@ -925,7 +929,7 @@ __noinline__ __device__ void select_threshold(int n_cand, int max_active, double
     int r = max_active - sh.thr_below;  // 1-based rank inside the boundary bucket
     const int cnt = sh.ng;
     __syncthreads();
-    if (cnt <= GCAP) {
+    if (cnt <= GCAP && !ws.force_radix) {
         if (threadIdx.x == 0) sh.ng = 0;
         __syncthreads();
         for (int i = threadIdx.x; i < n_cand; i += BLOCK) {
@@ -953,6 +957,7 @@ __noinline__ __device__ void select_threshold(int n_cand, int max_active, double
         return;
     }
     // radix select over the 96-bit (key, state) of the boundary-bucket members, MSB first
+    if (threadIdx.x == 0) sh.pflags |= WB_PATH_RADIX;
     u64 kpre = 0, kmask = 0;
     u32 spre = 0, smask = 0;
     for (int dig = 0; dig < 12; ++dig) {
@@ -1005,6 +1010,7 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
     const int n_cand = min(sh.n_cand, ws.cap);
     int status = sh.overflow ? wb_cap(WB_CAP_CANDIDATES) : WB_OK;
     const bool in_smem = n_cand <= ws.smem_cands;
+    if (!in_smem && threadIdx.x == 0) sh.pflags |= WB_PATH_GLOBAL_CANDS;
     u64 *ckey = in_smem ? s_key<BLOCK>() : c.cand_key();
     u32 *ca = in_smem ? s_ca<BLOCK>(ws) : c.cand_ca();
     volatile u32 *vca = ca;
@@ -1063,6 +1069,7 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
         kept = block_sum<BLOCK>(kept);
         need_select = kept > cfg.max_active;
         if (need_select) {
+            if (threadIdx.x == 0) sh.pflags |= WB_PATH_SELECT;
             for (int b = threadIdx.x; b < NB; b += BLOCK) sh.u.hist[b] = 0;
             __syncthreads();
             for (int i = threadIdx.x; i < n_cand; i += BLOCK) {
@@ -1687,12 +1694,13 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
         if (threadIdx.x < 8) sh.pc[threadIdx.x] = 0;
         if (threadIdx.x == 0) {
             sh.t_mark = clock64(); sh.arena_used = 0; sh.ready_seen = 0; sh.run_min = EMPTY_KEY;
+            sh.pflags = ws.stage_off ? WB_PATH_PREFETCH : 0;
             sh.tok_lo = 0.0; sh.tok_hi = 0.0; sh.ma_frac = 0.5f;
         }
         const int T = b.T[u];
         const long long row0 = b.row_off[u];
         int status = WB_OK;
-        u32 a_emit = 0, a_fin = 0, e_eps = 0;  // per-thread counters
+        u32 a_emit = 0, a_fin = 0, a_cas = 0, e_eps = 0;  // per-thread counters
         long long n_tok = 0, n_cand_tot = 0, n_surv_tot = 0, n_rec = 0;
         int nf = T;
         if (cfg.mode == 1) {
@@ -1751,12 +1759,16 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
                 if (threadIdx.x == 0) {
                     int seen = sh.ready_seen;
                     const long long t0 = clock64();
-                    while (seen <= ridx) {
-                        asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(seen) : "l"(b.ready + u) : "memory");
-                        if (seen <= ridx) {
+                    if (seen <= ridx) {
+                        // relaxed polls; one acquire fence once a new count is seen, so the
+                        // row data it covers is read after the counter
+                        for (;;) {
+                            asm volatile("ld.relaxed.sys.global.s32 %0, [%1];" : "=r"(seen) : "l"(b.ready + u) : "memory");
+                            if (seen > ridx) break;
                             __nanosleep(500);
                             if (clock64() - t0 > STREAM_WAIT_CYCLES) { seen = -1; break; }
                         }
+                        asm volatile("fence.acq_rel.sys;" ::: "memory");
                     }
                     sh.ready_seen = seen;
                 }
@@ -1796,6 +1808,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
                                                     cfg.max_active);
             a_emit += ec.a_emit;
             a_fin += ec.a_fin;
+            a_cas += ec.a_cas;
             __syncthreads();
             tick<BLOCK>(1);
             if (g.has_eps) {
@@ -1879,6 +1892,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
         }
         long long t_emit = block_sum<BLOCK>(a_emit);
         long long t_fin = block_sum<BLOCK>(a_fin);
+        long long t_cas = block_sum<BLOCK>(a_cas);
         long long t_eps = block_sum<BLOCK>(e_eps);
         tick<BLOCK>(7);
         if (threadIdx.x == 0) {
@@ -1903,9 +1917,11 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             }
             r.status = status & 0xFF;
             r.capacity_flags = capf;
+            r.path_flags = sh.pflags;
             r.n_tok = n_tok;
             r.a_emit = t_emit;
             r.a_fin = t_fin;
+            r.a_cas = t_cas;
             r.e_eps = t_eps;
             r.n_cand = n_cand_tot;
             r.n_surv = n_surv_tot;

@@ -308,6 +308,8 @@ static cudaError_t launch_decode(int max_grid, int num_sms, int num_cols, cudaSt
     if (row > avail) row = 0;  // the kernel reads the row from global memory instead
     if (zero_copy && row == 0) return cudaErrorNotSupported;  // host rows must be staged
     wd.smem_cands = (int)std::min<size_t>(avail / (sizeof(u64) + sizeof(u32)), (size_t)wd.cap);
+    // WB_SMEM_CANDS caps the candidates kept in shared memory (tests force the global path)
+    if (const char *sc = std::getenv("WB_SMEM_CANDS")) wd.smem_cands = std::min(wd.smem_cands, std::max(0, std::atoi(sc)));
     wd.row_in_smem = row > 0;
     // per-lane arc prefetch buffers (2 x 16 B) after the staged row, when they fit
     const size_t row_r = (row + 127) & ~(size_t)127, stage = (size_t)BLOCK * 32;
@@ -323,6 +325,8 @@ static cudaError_t launch_decode(int max_grid, int num_sms, int num_cols, cudaSt
     wd.eps_dedup = ed ? std::atoi(ed) : 1;
     const char *ma = std::getenv("WB_MA_EARLY");
     wd.ma_early = ma ? std::atoi(ma) : 0;
+    const char *fr = std::getenv("WB_FORCE_RADIX");  // tests: rank every boundary bucket by radix select
+    wd.force_radix = (fr && fr[0] == '1') ? 1 : 0;
     size_t smem = hdr + std::max(wd.stage_off ? row_r + stage : row,
                                  (size_t)wd.smem_cands * (sizeof(u64) + sizeof(u32)));
     smem = (smem + 15) & ~(size_t)15;
@@ -583,6 +587,22 @@ static int decode_impl(wb_decoder_t d, int32_t n, const double *costs, const int
     if (cfg->lattice && !(cfg->lattice_beam < 0) && std::isnan(cfg->lattice_beam))
         return set_err(WB_ERR_VALUE, "lattice_beam must be >= 0");
     d->pruned_n = 0;
+    if (prune) {
+        // Size the prune pools BEFORE the decode launch: cudaFree synchronises the device, and a
+        // streaming decode's kernel may be waiting for cost rows the caller publishes only
+        // after this call returns.
+        const size_t nn = d->o_node_n, na = d->o_arc_n, nf = d->o_fin_n;
+        const size_t T2 = (size_t)d->T_cap + 3;
+        int rc;
+        if ((rc = grow(&d->p_node, d->p_node_n, nn)) || (rc = grow(&d->p_arc, d->p_arc_n, na)) ||
+            (rc = grow(&d->p_ac, d->p_ac_n, na)) || (rc = grow(&d->p_fin, d->p_fin_n, nf)) ||
+            (rc = grow(&d->p_finw, d->p_finw_n, nf)) || (rc = grow(&d->p_fw, d->p_fw_n, nn)) ||
+            (rc = grow(&d->p_bw, d->p_bw_n, nn)) || (rc = grow(&d->p_nflag, d->p_nflag_n, nn + 4)) ||
+            (rc = grow(&d->p_depth, d->p_depth_n, nn)) || (rc = grow(&d->p_aflag, d->p_aflag_n, na)) ||
+            (rc = grow(&d->p_steps, d->p_steps_n, (size_t)n * T2 * 3)) ||
+            (rc = grow(&d->p_ctr, d->p_ctr_n, 4)) || (rc = grow(&d->p_meta, d->p_meta_n, (size_t)n * 8)))
+            return rc;
+    }
     // 1024 threads per CTA, one persistent CTA (utterance lane) per SM
     int block = d->block ? d->block : 1024;
     int max_grid = std::min(n, d->slots);
@@ -610,17 +630,7 @@ static int decode_impl(wb_decoder_t d, int32_t n, const double *costs, const int
     }
     d->last_zero_copy = zc ? 1 : 0;
     if (e == cudaSuccess && prune) {
-        const size_t nn = d->o_node_n, na = d->o_arc_n, nf = d->o_fin_n;
         const size_t T2 = (size_t)d->T_cap + 3;
-        int rc;
-        if ((rc = grow(&d->p_node, d->p_node_n, nn)) || (rc = grow(&d->p_arc, d->p_arc_n, na)) ||
-            (rc = grow(&d->p_ac, d->p_ac_n, na)) || (rc = grow(&d->p_fin, d->p_fin_n, nf)) ||
-            (rc = grow(&d->p_finw, d->p_finw_n, nf)) || (rc = grow(&d->p_fw, d->p_fw_n, nn)) ||
-            (rc = grow(&d->p_bw, d->p_bw_n, nn)) || (rc = grow(&d->p_nflag, d->p_nflag_n, nn + 4)) ||
-            (rc = grow(&d->p_depth, d->p_depth_n, nn)) || (rc = grow(&d->p_aflag, d->p_aflag_n, na)) ||
-            (rc = grow(&d->p_steps, d->p_steps_n, (size_t)n * T2 * 3)) ||
-            (rc = grow(&d->p_ctr, d->p_ctr_n, 4)) || (rc = grow(&d->p_meta, d->p_meta_n, (size_t)n * 8)))
-            return rc;
         CUDA_TRY(cudaMemsetAsync(d->p_ctr, 0, sizeof(unsigned long long) * 4, st));
         PruneDev P;
         std::memset(&P, 0, sizeof(P));

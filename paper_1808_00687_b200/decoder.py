@@ -11,7 +11,9 @@ exceptions.  There is no CPU search path.
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import math
+import threading
 import weakref
 from dataclasses import dataclass
 
@@ -151,6 +153,17 @@ class BatchOutput:
         return [self.decode_result(i) for i in range(len(self.results))]
 
 
+def _locked(fn):
+    """Serialise calls on one decoder: its workspace, page-locked cost table and ready
+    counters are mutable state shared by every call (the reference's decode() is pure and its
+    Wfst safe for concurrent readers, so concurrent callers must not observe each other)."""
+    @functools.wraps(fn)
+    def wrapper(self, *a, **k):
+        with self.lock:
+            return fn(self, *a, **k)
+    return wrapper
+
+
 class BatchDecoder:
     """Device workspace + the batched decode call (``wb_decoder_create`` / ``wb_decode``).
 
@@ -172,6 +185,7 @@ class BatchDecoder:
                          lattice_capacity=lattice_capacity,
                          lattice_out_capacity=lattice_out_capacity)
         self._h = None
+        self.lock = threading.RLock()
         self._create()
 
     def _create(self):
@@ -252,6 +266,7 @@ class BatchDecoder:
             self._create()
 
     # ------------------------------------------------------------------ host buffers (e2e)
+    @_locked
     def decode_host(self, costs: np.ndarray, row_offset: np.ndarray, num_frames: np.ndarray,
                     blank: np.ndarray, cfg, mode: str, label_capacity: int | None = None,
                     lattice: bool = False, lattice_beam: float | None = None) -> BatchOutput:
@@ -307,6 +322,7 @@ class BatchDecoder:
             setattr(self, name, buf)
         return buf.numpy()[:n].reshape(shape)
 
+    @_locked
     def decode_posteriors(self, posts_list, cfg, mode: str | None = None,
                           label_capacity: int | None = None, lattice: bool = False,
                           lattice_beam: float | None = None, block_frames: int = 32,
@@ -359,13 +375,12 @@ class BatchDecoder:
             raise ValueError(f"lattice_beam must be >= 0, got {lattice_beam}")
         ncfg = _native_config(cfg, mode, lattice, lattice_beam)
         self._last_max_active = cfg.max_active
-        N.flush_destroy()   # nothing may free device memory while the kernel waits on us
+        N.flush_destroy()
         L = N.load()
-        N.check(L.wb_decode_stream(self._h, n, costs.ctypes.data, off.ctypes.data, T.ctypes.data,
-                                   L1, blank.ctypes.data, C.byref(ncfg), cap, ready.ctypes.data,
-                                   crow.ctypes.data if compact else None, None), "decode")
         # producers: row blocks in block-major order; each utterance's ready count advances
-        # over its contiguous finished prefix
+        # over its contiguous finished prefix.  They start BEFORE the launch: when launches are
+        # serialised (CUDA_LAUNCH_BLOCKING=1, ncu, compute-sanitizer) wb_decode_stream returns
+        # only after the kernel has finished, so the rows must not depend on it returning.
         lock = threading.Lock()
         done = [dict() for _ in range(n)]
         nxt = [0] * n
@@ -400,11 +415,18 @@ class BatchDecoder:
                     ready[u] = done[u].pop(nxt[u])
                     nxt[u] += 1
         tasks = [(u, b) for b in range(max(nblk) if nblk else 0) for u in range(n) if b < nblk[u]]
-        nw = workers or int(os.environ.get("WB_PRODUCERS", 0)) or min(8, len(os.sched_getaffinity(0)))
+        nw = workers or int(os.environ.get("WB_PRODUCERS", 0)) or len(os.sched_getaffinity(0))
+        ex = ThreadPoolExecutor(nw)
         try:
-            with ThreadPoolExecutor(nw) as ex:
-                list(ex.map(lambda ub: work(*ub), tasks))
+            futs = [ex.submit(work, u, b) for u, b in tasks]
+            N.check(L.wb_decode_stream(self._h, n, costs.ctypes.data, off.ctypes.data,
+                                       T.ctypes.data, L1, blank.ctypes.data, C.byref(ncfg), cap,
+                                       ready.ctypes.data, crow.ctypes.data if compact else None,
+                                       None), "decode")
+            for f in futs:
+                f.result()
         finally:
+            ex.shutdown(wait=True)
             ready[:] = total  # every row is written (or the kernel must not wait forever)
         res = np.zeros(n, dtype=N.UTT_RESULT_DTYPE)
         ol = np.zeros((n, cap), dtype=np.int32)
@@ -430,6 +452,7 @@ class BatchDecoder:
                                           block_frames, workers, _attempt + 1)
         return BatchOutput(res, ol, il, cap)
 
+    @_locked
     def fetch_lattices(self, wfst: Wfst) -> list:
         """Trimmed lattices of the last lattice-mode decode, canonically ordered."""
         from .lattice import canonical_batch
@@ -451,6 +474,7 @@ class BatchDecoder:
             raise N.CapacityError("lattice output pool overflowed")
         return canonical_batch(wfst, meta, nodes, arcs, ac, fin, finw)
 
+    @_locked
     def fetch_pruned_lattices(self, wfst: Wfst, lattice_beam: float,
                               max_workers: int | None = None, split: bool = True) -> list:
         """Lattices of the last decode made with ``lattice_beam``: stage one of prune_lattice
@@ -506,6 +530,7 @@ class BatchDecoder:
             return list(ex.map(one, out))
 
     # ------------------------------------------------------------------ device buffers
+    @_locked
     def decode_device(self, costs, row_offset, num_frames, blank, cfg, mode: str, results,
                       olabels, ilabels, label_capacity: int, stream=None, lattice: bool = False,
                       lattice_beam: float | None = None):
@@ -538,13 +563,17 @@ def _check_decodable(w: Wfst, posts) -> None:
                          f"only covers labels 1..{L}")
 
 
+_DECODER_LOCK = threading.Lock()
+
+
 def _decoder_for(w: Wfst) -> BatchDecoder:
     dev = _current_device()
-    cache = w.__dict__.setdefault("_b200_decoders", {})
-    dec = cache.get(dev)
-    if dec is None:
-        dec = BatchDecoder(w, dev)
-        cache[dev] = dec
+    with _DECODER_LOCK:
+        cache = w.__dict__.setdefault("_b200_decoders", {})
+        dec = cache.get(dev)
+        if dec is None:
+            dec = BatchDecoder(w, dev)
+            cache[dev] = dec
     return dec
 
 
@@ -569,11 +598,12 @@ def decode_batch(wfst, posts_list, cfg: DecodeConfig, mode: str | None = None,
         if len(recorders) != len(posts_list):
             raise ValueError("pass one LatticeRecorder per utterance")
     dec = _decoder_for(w)
-    # cost rows are computed on host threads while the kernel already decodes (streaming)
-    out = dec.decode_posteriors(posts_list, cfg, mode, lattice=recorders is not None)
-    results = out.decode_results()
+    with dec.lock:   # the decode and its lattice fetch see one workspace state
+        # cost rows are computed on host threads while the kernel already decodes (streaming)
+        out = dec.decode_posteriors(posts_list, cfg, mode, lattice=recorders is not None)
+        results = out.decode_results()
+        lats = dec.fetch_lattices(w) if recorders is not None else None
     if recorders is not None:
-        lats = dec.fetch_lattices(w)
         for rec, lat, r in zip(recorders, lats, out.results):
             rec._set(lat, int(r["final_step"]), int(r["final_state"]), bool(r["reached_final"]))
     return results

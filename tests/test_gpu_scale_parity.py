@@ -1,0 +1,192 @@
+"""Parity at the benchmarked sizes (BASELINE.json configs 2-5) against the C oracle.
+
+The small-graph tests (test_gpu_parity.py) never reach the branches the benchmark configs
+take: steps with more candidates than the shared-memory store holds (global-memory candidate
+keys), the radix-select ranking of a large boundary bucket, the non-prefetch expand loop.
+Every test here runs at a config's own graph, beam and max-active (frames reduced only where
+the oracle would take minutes), checks all seven DecodeResult fields against the oracle in
+its reference-exact mode (oracle/wfst_oracle.c restates decoder.py:121-346), and asserts via
+``path_flags`` (WB_PATH_*) that the branch under test really ran.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import paper_1808_00687_b200 as P
+from paper_1808_00687_b200 import _native as N
+from paper_1808_00687_b200 import synth
+from paper_1808_00687_b200.decoder import BatchDecoder
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+INF = math.inf
+
+
+def _fields(r):
+    return (r.total_cost, r.olabels, r.ilabels, r.search_steps, r.tokens_expanded,
+            r.reached_final, r.died_at_step)
+
+
+def _table(posts, scale=1.0):
+    T = np.asarray([p.num_frames for p in posts], np.int32)
+    off = np.zeros(len(T), np.int64)
+    np.cumsum(T[:-1], out=off[1:])
+    costs = np.concatenate([P.cost_table(p, scale) for p in posts])
+    blank = np.concatenate([p.rows[:, p.blank_col] for p in posts])
+    return costs, off, T, blank
+
+
+def _oracle(og, posts, cfg, canonical=False):
+    return O.decode_batch(og, [P.cost_table(p, cfg.acoustic_scale) for p in posts],
+                          [p.rows[:, p.blank_col] for p in posts], beam=cfg.beam,
+                          max_active=cfg.max_active, mode=cfg.mode,
+                          blank_threshold=cfg.blank_threshold, canonical=canonical,
+                          n_threads=min(len(posts), len(os.sched_getaffinity(0))))
+
+
+def _decode_table(dec, posts, cfg):
+    costs, off, T, blank = _table(posts, cfg.acoustic_scale)
+    return dec.decode_host(costs, off, T, blank, cfg, cfg.mode)
+
+
+def _assert_equal(out, want, tag):
+    got = out.decode_results()
+    bad = [i for i, (r, o) in enumerate(zip(got, want)) if _fields(r) != o.astuple()]
+    assert not bad, (tag, bad[:3], [(got[i], want[i]) for i in bad[:2]])
+
+
+# --------------------------------------------------------------------------- config 2 graph
+@pytest.fixture(scope="module")
+def c2():
+    g = synth.hclg_like(0)   # 1M states / 3M arcs / 3000 labels, ~1.5 % epsilon arcs
+    return g, O.OracleGraph(g)
+
+
+C2 = P.DecodeConfig(beam=13.0, max_active=7000, mode="fsd")
+
+
+def test_config2_full_utterances(cuda, c2):
+    """Config 2 exactly as benched (seeds 1..8 are bench.py's utterances 0..7; 1000 frames,
+    beam 13, max-active 7000, FSD): results == oracle, and the max-active select ran."""
+    g, og = c2
+    posts = [synth.random_posteriors(i + 1, 1000, 3000) for i in range(8)]
+    dec = BatchDecoder(g, 0)
+    out = _decode_table(dec, posts, C2)
+    _assert_equal(out, _oracle(og, posts, C2), "config2")
+    flags = out.results["path_flags"]
+    assert (flags & N.WB_PATH_SELECT).all() and (flags & N.WB_PATH_PREFETCH).all()
+    # the public posterior path (streamed frame_costs) on the same utterances
+    got = P.decode_batch(g, posts[:4], C2)
+    assert [_fields(r) for r in got] == [_fields(r) for r in out.decode_results()[:4]]
+
+
+@pytest.mark.parametrize("env,flag,absent", [
+    ({"WB_SMEM_CANDS": "0"}, N.WB_PATH_GLOBAL_CANDS, 0),              # every step spills
+    ({"WB_SMEM_CANDS": "6000"}, N.WB_PATH_GLOBAL_CANDS, 0),           # large steps spill
+    ({"WB_FORCE_RADIX": "1"}, N.WB_PATH_RADIX, 0),                    # radix-select ranking
+    ({"WB_PREFETCH": "0"}, N.WB_PATH_SELECT, N.WB_PATH_PREFETCH),     # unpipelined expand
+    ({"WB_SMEM_KB": "32"}, N.WB_PATH_GLOBAL_CANDS, N.WB_PATH_PREFETCH),
+    ({"WB_BEAM_SKIP": "0"}, N.WB_PATH_SELECT, 0),
+    ({"WB_EXACT_MIN": "0"}, N.WB_PATH_SELECT, 0),
+    ({"WB_XCHG_GATHER": "0"}, N.WB_PATH_SELECT, 0),
+])
+def test_config2_forced_branches(cuda, c2, monkeypatch, env, flag, absent):
+    """Each tuning knob / spill branch at config-2 scale: identical results to the oracle."""
+    g, og = c2
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    posts = [synth.random_posteriors(100 + i, 250, 3000) for i in range(4)]
+    out = _decode_table(BatchDecoder(g, 0, max_utts_in_flight=4), posts, C2)
+    _assert_equal(out, _oracle(og, posts, C2), env)
+    flags = out.results["path_flags"]
+    assert (flags & flag).all(), (env, flags)
+    assert not (flags & absent).any(), (env, flags)
+
+
+def test_config2_tight_max_active_and_beam(cuda, c2):
+    """Max-active far below the candidate count (every step selects), a narrow beam."""
+    g, og = c2
+    posts = [synth.random_posteriors(300 + i, 200, 3000) for i in range(4)]
+    for cfg in (P.DecodeConfig(beam=13.0, max_active=500, mode="fsd"),
+                P.DecodeConfig(beam=6.0, max_active=20000, mode="fsd"),
+                P.DecodeConfig(beam=INF, max_active=3000, mode="fsd")):
+        out = _decode_table(BatchDecoder(g, 0, max_utts_in_flight=4), posts, cfg)
+        _assert_equal(out, _oracle(og, posts, cfg), cfg)
+
+
+# --------------------------------------------------------------------------- tie-heavy
+def test_tie_heavy_boundary_bucket_radix(cuda):
+    """Integer arc weights and uniform posteriors: each step's candidates share a handful of
+    distinct costs, so the max-active boundary bucket holds thousands of exact ties and is
+    ranked by radix select over (cost, state) (decoder.py:188-191 tie order) without a
+    forcing knob.  No epsilon arcs: the reference's stale-backpointer quirk cannot fire."""
+    from paper_1808_00687_b200.wfst import Wfst
+    g0 = synth.random_wfst(5, 200_000, 800_000, 20, eps_fraction=0.0, final_fraction=0.05)
+    w = np.floor(g0.weight)            # {0, 1, 2}
+    g = Wfst.from_arrays(g0.num_states, g0.start, g0.src, g0.dst, g0.ilabel, g0.olabel, w,
+                         np.floor(g0.final_w))
+    L = 20
+    posts = [P.PosteriorMatrix(np.full((60 + 10 * i, L + 1), 1.0 / (L + 1)), 0, validate=False)
+             for i in range(4)]
+    cfg = P.DecodeConfig(beam=INF, max_active=2500, mode="fsd")
+    out = _decode_table(BatchDecoder(g, 0, max_utts_in_flight=4), posts, cfg)
+    _assert_equal(out, _oracle(O.OracleGraph(g), posts, cfg), "ties")
+    assert (out.results["path_flags"] & N.WB_PATH_RADIX).any()
+
+
+# --------------------------------------------------------------------------- config 4
+def test_config4_ctc_lsd_full_utterances(cuda):
+    """Config 4: 5k-label CTC-like graph (self-loops on every state), 1500-frame utterances
+    with 80 % blank frames above the 0.98 threshold, LSD, beam 13, max-active 7000, through
+    the public posterior path (streamed, compacted non-blank rows)."""
+    g = synth.random_wfst(0, 100_000, 300_000, 5000, eps_fraction=0.015, selfloops=True,
+                          final_fraction=0.01)
+    posts = [synth.random_posteriors(i + 1, 1500, 5000, blank_fraction=0.8) for i in range(6)]
+    cfg = P.DecodeConfig(beam=13.0, max_active=7000, mode="lsd")
+    got = P.decode_batch(g, posts, cfg)
+    want = _oracle(O.OracleGraph(g), posts, cfg)
+    assert [_fields(r) for r in got] == [o.astuple() for o in want]
+    for p, r in zip(posts, got):   # the step law: steps = T - |U| (or the dying step)
+        assert r.search_steps == int((p.rows[:, 0] <= 0.98).sum()) or r.died_at_step is not None
+
+
+# --------------------------------------------------------------------------- config 3
+def test_config3_lattice_and_prune(cuda, c2):
+    """Config 3 shape: config-2 graph, exact lattices + lattice-beam 8 pruned on the device,
+    against the oracle's build_lattice + prune_lattice (lattice.py:148-501)."""
+    from paper_1808_00687_b200 import lattice as Lt
+    g, og = c2
+    posts = [synth.random_posteriors(500 + i, 300, 3000) for i in range(3)]
+    costs, off, T, blank = _table(posts)
+    dec = BatchDecoder(g, 0, max_utts_in_flight=3)
+    out = dec.decode_host(costs, off, T, blank, C2, "fsd", lattice=True, lattice_beam=8.0)
+    lats = dec.fetch_lattices(g)
+    # the pruned lattices of the same launch come from the device prune_kernel
+    out2 = dec.decode_host(costs, off, T, blank, C2, "fsd", lattice=True, lattice_beam=8.0)
+    pruned = dec.fetch_pruned_lattices(g, 8.0)
+    assert out2.decode_results() == out.decode_results()
+    for i, p in enumerate(posts):
+        r, olat = O.decode(og, P.cost_table(p), p.rows[:, 0], beam=13.0, max_active=7000,
+                           mode="fsd", return_lattice=True)
+        assert _fields(out.decode_results()[i]) == r.astuple()
+        assert lats[i].key() == olat.key(), i
+        try:
+            want = O.prune_lattice(olat, 8.0).key()
+        except O.OracleLatticeError:
+            want = "error"
+        got = "error" if isinstance(pruned[i], Lt.LatticeError) else pruned[i].key()
+        assert got == want, i
+        assert Lt.lattice_best_path(lats[i])[0] == r.total_cost
+
+
+# --------------------------------------------------------------------------- config 5
+def test_config5_large_graph(cuda):
+    """Config 5 graph (7M states / 20M arcs / 512 labels, beam 13, max-active 7000): a few
+    utterances against the oracle (the graph alone takes ~30 s to generate)."""
+    g = synth.random_wfst(0, 7_000_000, 20_000_000, 512, eps_fraction=0.015,
+                          final_fraction=0.01)
+    posts = [synth.random_posteriors(i + 1, 400, 512) for i in range(4)]
+    out = _decode_table(BatchDecoder(g, 0, max_utts_in_flight=4), posts, C2)
+    _assert_equal(out, _oracle(O.OracleGraph(g), posts, C2), "config5")
