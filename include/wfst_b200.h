@@ -47,7 +47,8 @@ extern "C" {
 #define WB_CAP_STREAM 128      /* wb_decode_stream: a cost row was not published within ~60 s */
 #define WB_ERR_NOMEM 6
 
-#define WB_PARSE_FALLBACK 7 /* wb_wfst_parse_text: text needs the full (Python) parser */
+#define WB_PARSE_ERROR 7    /* wb_wfst_parse_text: malformed line (ParseError) */
+#define WB_PARSE_SYMBOL 8   /* wb_wfst_parse_text: unknown symbol / negative label id (SymbolError) */
 
 #define WB_MEM_DEVICE 0    /* all batch pointers are device pointers; the call is asynchronous */
 #define WB_MEM_HOST 1      /* all batch pointers are host pointers; the call copies and syncs */
@@ -276,11 +277,14 @@ void wb_gather_rows(const double *src, int64_t src_ld, const int32_t *idx, int64
 int wb_decode_finish(wb_decoder_t d, wb_utt_result *results, int32_t *olabels, int32_t *ilabels);
 
 /*
- * parse_wfst_text fast path (wfst.py:315-378) for ASCII AT&T text with integer labels: arcs in
- * file order, finals in first-mention order (last weight wins), start = first state
- * mentioned.  Returns WB_PARSE_FALLBACK for anything it does not reproduce exactly (symbols,
- * non-ASCII, Python numeric extras, malformed lines) -- the caller then runs the full parser.
- * Arrays are owned by the caller: wb_parsed_wfst_free.
+ * parse_wfst_text (wfst.py:315-378): AT&T transducer text -> arc arrays in file order, finals
+ * in first-mention order (last weight wins), start = first state mentioned.  `isyms` / `osyms`
+ * (may be null): "symbol id" lines; a label token resolves through its table first, then as a
+ * bare non-negative integer.  Text must use '\n' (optionally "\r\n") line breaks and ASCII
+ * whitespace between fields (the Python shim normalises anything else).  Errors:
+ * WB_PARSE_ERROR (ParseError) / WB_PARSE_SYMBOL (SymbolError) with out->error_line (1-based,
+ * 0 = no line) and the message in wb_last_error().  Arrays are owned by the caller:
+ * wb_parsed_wfst_free.
  */
 typedef struct {
     int32_t num_states, start;
@@ -289,10 +293,20 @@ typedef struct {
     double *weight;
     int32_t *final_state;
     double *final_weight;
+    int32_t error_line, _pad;
 } wb_parsed_wfst;
 int wb_wfst_parse_text(const char *text, int64_t len, int32_t allow_negative_weights,
-                       wb_parsed_wfst *out);
+                       const char *isyms, int64_t isyms_len, const char *osyms,
+                       int64_t osyms_len, wb_parsed_wfst *out);
 void wb_parsed_wfst_free(wb_parsed_wfst *p);
+
+/*
+ * POST1 posterior files (load_posteriors' binary form, posteriors.py:147-217): header, and the
+ * rows read straight into `dst` (row stride dst_ld doubles) -- typically the decoder's
+ * page-locked table, so no pageable staging copy.  WB_ERR_VALUE + message on a malformed file.
+ */
+int wb_post1_info(const char *path, int32_t *num_frames, int32_t *num_cols, int32_t *blank_col);
+int wb_post1_read(const char *path, double *dst, int64_t dst_ld);
 
 /* Device time (ms) of the decode kernel of the last wb_decode call (CUDA events on its stream). */
 int wb_last_kernel_ms(wb_decoder_t d, float *ms);

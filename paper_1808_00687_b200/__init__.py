@@ -11,7 +11,7 @@ from .decoder import (BatchDecoder, BatchOutput, DecodeConfig, DecodeResult, Dev
                       SearchDied, as_wfst, decode, decode_batch, decode_fsd, decode_lsd,
                       parallel_decode)
 from .lattice import LatticeError, LatticeRecorder, PipelinedLatticeBuilder
-from .posteriors import (BlankMask, PosteriorFormatError, PosteriorMatrix, acoustic_cost,
+from .posteriors import (BlankMask, PosteriorBatch, PosteriorFormatError, PosteriorMatrix, acoustic_cost,
                          classify_blank_frames, cost_table, frame_costs, load_posteriors,
                          save_posteriors)
 from .lattice import (EMPTY_LATTICE, Lattice, build_lattice, lattice_best_path, prune_lattice)
@@ -24,7 +24,7 @@ from .wfst import (Arc, EpsilonCycle, ParseError, SymbolError, SymbolTable, Wfst
 __all__ = [
     "Arc", "BatchDecoder", "BatchOutput", "BlankMask", "DecodeConfig", "DecodeResult",
     "DeviceGraph", "EpsilonCycle", "LatticeError", "LatticeRecorder", "ParseError",
-    "PosteriorFormatError", "PosteriorMatrix", "SearchDied", "Wfst", "WfstError",
+    "PosteriorBatch", "PosteriorFormatError", "PosteriorMatrix", "SearchDied", "Wfst", "WfstError",
     "acoustic_cost", "as_wfst", "classify_blank_frames", "cost_table", "decode",
     "decode_batch", "decode_fsd", "decode_lsd", "frame_costs", "parallel_decode",
     "parse_wfst_text", "validate_epsilon_acyclic", "load_posteriors", "save_posteriors",

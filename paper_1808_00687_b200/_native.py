@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("WB_LIB") or os.path.join(_HERE, "_lib", "libwfstb200.so")
 
 WB_OK, WB_ERR_CUDA, WB_ERR_VALUE, WB_ERR_LATTICE, WB_ERR_WFST, WB_ERR_CAPACITY, WB_ERR_NOMEM = range(7)
-WB_PARSE_FALLBACK = 7
+WB_PARSE_ERROR, WB_PARSE_SYMBOL = 7, 8
 WB_MEM_DEVICE, WB_MEM_HOST = 0, 1
 (WB_CAP_CANDIDATES, WB_CAP_ARENA, WB_CAP_FRAMES, WB_CAP_LABELS, WB_CAP_LATTICE_RAW,
  WB_CAP_LATTICE_OUT, WB_CAP_EPS_ROUNDS, WB_CAP_STREAM) = (1, 2, 4, 8, 16, 32, 64, 128)
@@ -58,7 +58,8 @@ class ParsedWfst(C.Structure):
     _fields_ = [("num_states", C.c_int32), ("start", C.c_int32), ("num_arcs", C.c_int64),
                 ("num_finals", C.c_int64), ("src", C.c_void_p), ("dst", C.c_void_p),
                 ("ilabel", C.c_void_p), ("olabel", C.c_void_p), ("weight", C.c_void_p),
-                ("final_state", C.c_void_p), ("final_weight", C.c_void_p)]
+                ("final_state", C.c_void_p), ("final_weight", C.c_void_p),
+                ("error_line", C.c_int32), ("_pad", C.c_int32)]
 
 
 class LatticeArrays(C.Structure):
@@ -89,7 +90,7 @@ EXPORTED = ("wb_last_error", "wb_version", "wb_device_count", "wb_graph_create",
             "wb_lattice_arrays_free", "wb_lattice_best_path", "wb_last_transfer",
             "wb_lattice_canonical", "wb_lattice_pruned_totals", "wb_lattice_pruned_fetch",
             "wb_lattice_split", "wb_decode_stream", "wb_decode_finish", "wb_wfst_parse_text",
-            "wb_parsed_wfst_free", "wb_gather_rows")
+            "wb_parsed_wfst_free", "wb_gather_rows", "wb_post1_info", "wb_post1_read")
 
 
 def load():
@@ -120,8 +121,11 @@ def load():
     L.wb_gather_rows.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32,
                                  C.c_int32, C.c_void_p, C.c_int64, C.c_int32]
     L.wb_gather_rows.restype = None
+    L.wb_post1_info.argtypes = [C.c_char_p] + [C.POINTER(C.c_int32)] * 3
+    L.wb_post1_read.argtypes = [C.c_char_p, C.c_void_p, C.c_int64]
     L.wb_decode_finish.argtypes = [C.c_void_p] + [C.c_void_p] * 3
-    L.wb_wfst_parse_text.argtypes = [C.c_char_p, C.c_int64, C.c_int32, C.POINTER(ParsedWfst)]
+    L.wb_wfst_parse_text.argtypes = [C.c_char_p, C.c_int64, C.c_int32, C.c_char_p, C.c_int64,
+                                     C.c_char_p, C.c_int64, C.POINTER(ParsedWfst)]
     L.wb_parsed_wfst_free.argtypes = [C.POINTER(ParsedWfst)]
     L.wb_parsed_wfst_free.restype = None
     L.wb_last_transfer.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
@@ -143,6 +147,27 @@ def load():
                                        C.c_int32]
     _lib = L
     return L
+
+
+def post1_info(path: str) -> tuple[int, int, int]:
+    """(frames, columns, blank column) of a POST1 file (native header check)."""
+    from .posteriors import PosteriorFormatError
+    T, Cn, b = C.c_int32(), C.c_int32(), C.c_int32()
+    if load().wb_post1_info(path.encode(), C.byref(T), C.byref(Cn), C.byref(b)) != WB_OK:
+        raise PosteriorFormatError(f"{path}: {last_error()}")
+    return T.value, Cn.value, b.value
+
+
+def post1_read(path: str, dst) -> None:
+    """Read a POST1 file's rows into the float64 rows ``dst`` (e.g. a page-locked table)."""
+    from .posteriors import PosteriorFormatError
+    if load().wb_post1_read(path.encode(), dst.ctypes.data, dst.strides[0] // 8) != WB_OK:
+        raise PosteriorFormatError(f"{path}: {last_error()}")
+
+
+def last_error() -> str:
+    """Text of the last failure on the calling thread (wb_last_error)."""
+    return (load().wb_last_error() or b"").decode(errors="replace")
 
 
 def check(rc: int, what: str = "") -> None:

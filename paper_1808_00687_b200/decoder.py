@@ -336,15 +336,18 @@ class BatchDecoder:
         import os
         import threading
         from concurrent.futures import ThreadPoolExecutor
-        from .posteriors import cost_rows
+        from .posteriors import PosteriorBatch, cost_rows
         mode = mode or cfg.mode
-        posts_list = list(posts_list)
+        # a PosteriorBatch's page-locked table becomes the cost table itself: rows are
+        # converted in place (the blank column is read out first) and read zero-copy
+        batch = posts_list if isinstance(posts_list, PosteriorBatch) else None
+        posts_list = batch.matrices() if batch is not None else list(posts_list)
         n = len(posts_list)
         if n == 0:
             return BatchOutput(np.zeros(0, dtype=N.UTT_RESULT_DTYPE), np.zeros((0, 1), np.int32),
                                np.zeros((0, 1), np.int32), 1)
         L1 = posts_list[0].rows.shape[1]
-        T = np.asarray([p.num_frames for p in posts_list], np.int32)
+        T = np.asarray([p.rows.shape[0] for p in posts_list], np.int32)
         off = np.zeros(n, np.int64)
         np.cumsum(T[:-1], out=off[1:])
         blank = np.zeros(max(int(T.sum()), 1), np.float64)
@@ -353,7 +356,7 @@ class BatchDecoder:
         # LSD: only the frames the device pre-pass will search (blank <= threshold, strict >
         # for blank), compacted per utterance in search-step order when the label columns
         # are contiguous (blank column 0); otherwise rows stay indexed by frame
-        compact = mode == "lsd" and all(p.blank_col == 0 for p in posts_list)
+        compact = mode == "lsd" and batch is None and all(p.blank_col == 0 for p in posts_list)
         need = [np.flatnonzero(~(p.rows[:, p.blank_col] > cfg.blank_threshold)).astype(np.int32)
                 if mode == "lsd" else None for p in posts_list]
         if compact:
@@ -365,7 +368,11 @@ class BatchDecoder:
         else:
             R = max(int(T.sum()), 1)
             total = T
-        costs = self._pinned("_pin_costs", (R, L1), np.float64)
+        if batch is not None:
+            costs = batch.table
+            batch.consumed = True
+        else:
+            costs = self._pinned("_pin_costs", (R, L1), np.float64)
         ready = self._pinned("_pin_ready", (n,), np.int32)
         ready[:] = 0
         maxT = int(T.max())
@@ -582,9 +589,11 @@ def decode_batch(wfst, posts_list, cfg: DecodeConfig, mode: str | None = None,
     """Decode many utterances in one persistent-kernel launch (utterances are independent,
     SURVEY 8e).  Each element equals ``decode(wfst, posts, cfg)`` of the reference.
     ``recorder``: one ``LatticeRecorder`` per utterance (a list) to record lattices."""
+    from .posteriors import PosteriorBatch
     w = as_wfst(wfst)
     mode = mode or cfg.mode
-    posts_list = list(posts_list)
+    batch = posts_list if isinstance(posts_list, PosteriorBatch) else None
+    posts_list = batch.matrices() if batch is not None else list(posts_list)
     for p in posts_list:
         _check_decodable(w, p)
     if not posts_list:
@@ -600,7 +609,8 @@ def decode_batch(wfst, posts_list, cfg: DecodeConfig, mode: str | None = None,
     dec = _decoder_for(w)
     with dec.lock:   # the decode and its lattice fetch see one workspace state
         # cost rows are computed on host threads while the kernel already decodes (streaming)
-        out = dec.decode_posteriors(posts_list, cfg, mode, lattice=recorders is not None)
+        out = dec.decode_posteriors(batch if batch is not None else posts_list, cfg, mode,
+                                    lattice=recorders is not None)
         results = out.decode_results()
         lats = dec.fetch_lattices(w) if recorders is not None else None
     if recorders is not None:

@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import re
 from dataclasses import dataclass
 
 import numpy as np
@@ -44,84 +45,66 @@ class SymbolError(WfstError):
 
 
 class SymbolTable:
-    """Label id <-> symbol string map (reference ``SymbolTable``, wfst.py:67-151).
+    """Label id <-> symbol map for symbolic transducer text and transcripts (the reference's
+    ``SymbolTable``, wfst.py:67-151).  Id 0 is ``<eps>``; the id of ``<blank>`` is kept as
+    ``blank_id``.  A symbol or id may be bound once (rebinding raises ``SymbolError``)."""
 
-    Id 0 is always ``<eps>``; a ``<blank>`` entry's id is kept as ``blank_id``.  Remapping a
-    symbol or an id to a different partner raises ``SymbolError`` (``ParseError`` from
-    ``parse``, with the line number).
-    """
-
-    EPS_SYMBOL = "<eps>"
-    BLANK_SYMBOL = "<blank>"
+    EPS_SYMBOL, BLANK_SYMBOL = "<eps>", "<blank>"
 
     def __init__(self, symbols: dict[str, int] | None = None):
-        self._by_sym: dict[str, int] = {self.EPS_SYMBOL: 0}
-        self._by_id: dict[int, str] = {0: self.EPS_SYMBOL}
-        self.blank_id: int | None = None
-        for sym, idx in (symbols or {}).items():
-            self.add(sym, idx)
+        self._id_of = {self.EPS_SYMBOL: 0}
+        self._sym_of = {0: self.EPS_SYMBOL}
+        for name, ident in (symbols or {}).items():
+            self.add(name, ident)
+
+    @property
+    def blank_id(self) -> int | None:
+        return self._id_of.get(self.BLANK_SYMBOL)
 
     def add(self, symbol: str, idx: int | None = None) -> int:
-        if idx is None:
-            idx = max(self._by_id) + 1
-        if idx == 0 or symbol == self.EPS_SYMBOL:
-            if idx == 0 and symbol == self.EPS_SYMBOL:
-                return 0
+        idx = max(self._sym_of) + 1 if idx is None else int(idx)
+        bound_id, bound_sym = self._id_of.get(symbol, idx), self._sym_of.get(idx, symbol)
+        if (idx == 0) != (symbol == self.EPS_SYMBOL):
             raise SymbolError(f"id 0 is reserved for {self.EPS_SYMBOL!r}, got {symbol!r} = {idx}")
-        have = self._by_sym.get(symbol)
-        if have is not None and have != idx:
-            raise SymbolError(f"symbol {symbol!r} already mapped to {have}, cannot remap to {idx}")
-        other = self._by_id.get(idx)
-        if other is not None and other != symbol:
-            raise SymbolError(f"id {idx} already mapped to {other!r}, cannot remap to {symbol!r}")
-        self._by_sym[symbol] = idx
-        self._by_id[idx] = symbol
-        if symbol == self.BLANK_SYMBOL:
-            self.blank_id = idx
+        if bound_id != idx:
+            raise SymbolError(f"symbol {symbol!r} already mapped to {bound_id}, cannot remap to {idx}")
+        if bound_sym != symbol:
+            raise SymbolError(f"id {idx} already mapped to {bound_sym!r}, cannot remap to {symbol!r}")
+        self._id_of[symbol], self._sym_of[idx] = idx, symbol
         return idx
 
     def find_id(self, symbol: str) -> int | None:
-        return self._by_sym.get(symbol)
+        return self._id_of.get(symbol)
 
     def find_symbol(self, idx: int) -> str | None:
-        return self._by_id.get(idx)
+        return self._sym_of.get(idx)
 
     def __len__(self) -> int:
-        return len(self._by_sym)
+        return len(self._id_of)
 
     def __contains__(self, symbol: str) -> bool:
-        return symbol in self._by_sym
+        return symbol in self._id_of
 
     def __iter__(self):
-        return iter(sorted(self._by_id.items()))
+        return iter(sorted(self._sym_of.items()))
 
     @classmethod
     def parse(cls, text: str) -> "SymbolTable":
-        """``symbol id`` lines; ``#`` comments and blank lines skipped; id 0 must be <eps>."""
+        """``symbol id`` per line (``#`` comments and blank lines skipped)."""
         table = cls()
-        for line_no, raw in enumerate(text.splitlines(), start=1):
-            line = raw.strip()
-            if not line or line.startswith("#"):
-                continue
-            f = line.split()
-            if len(f) != 2:
-                raise ParseError(f"expected 'symbol id', got {raw!r}", line_no)
+        rows = [(n, ln.split()) for n, ln in enumerate(text.splitlines(), 1)]
+        for n, f in ((n, f) for n, f in rows if f and not f[0].startswith("#")):
+            if len(f) != 2 or not f[1].lstrip("+-").isdigit():
+                raise ParseError(f"expected 'symbol id', got {' '.join(f)!r}"
+                                 if len(f) != 2 else f"bad id {f[1]!r}", n)
             try:
-                idx = int(f[1])
-            except ValueError:
-                raise ParseError(f"bad id {f[1]!r}", line_no) from None
-            if idx == 0:
-                if f[0] != cls.EPS_SYMBOL:
-                    raise ParseError(f"id 0 must be {cls.EPS_SYMBOL!r}, got {f[0]!r}", line_no)
-                continue
-            try:
-                table.add(f[0], idx)
+                table.add(f[0], int(f[1]))
             except SymbolError as exc:
-                raise ParseError(str(exc), line_no) from None
+                raise ParseError(str(exc), n) from None
         return table
 
     def format(self) -> str:
-        return "".join(f"{sym} {idx}\n" for idx, sym in sorted(self._by_id.items()))
+        return "".join(f"{sym} {i}\n" for i, sym in sorted(self._sym_of.items()))
 
 
 @dataclass(frozen=True)
@@ -322,202 +305,166 @@ def _has_structural_cycle(n: int, u: np.ndarray, v: np.ndarray) -> bool:
 
 
 def validate_epsilon_acyclic(w: Wfst) -> EpsilonCycle | None:
-    """Detect an epsilon cycle with total weight <= 0 (wfst.py:412-470).
+    """An epsilon cycle whose total weight is <= 0, or None (the check of wfst.py:412-470:
+    such a cycle would make non-emitting propagation diverge; strictly positive cycles are
+    accepted).  Same tolerances as the reference: an arc improves a potential when it beats it
+    by more than 1e-15, and counts as tight when within 1e-12.
 
-    Fast path: an epsilon subgraph with no structural cycle at all (the usual case, and every
-    graph ``make_random_wfst`` emits) is accepted after a vectorised Kahn peel.  Otherwise the
-    reference procedure runs: Bellman-Ford from a virtual zero source, then a cycle search on
-    zero-reduced-cost (tight) arcs.
+    1. A vectorised Kahn peel accepts epsilon subgraphs with no structural cycle at all (the
+       usual case, every make_random_wfst graph).
+    2. Otherwise only strongly connected components (scipy.sparse.csgraph) can hold a cycle.
+       Per component a vectorised (Jacobi) Bellman-Ford from all-zero potentials either keeps
+       improving for |C| passes -- a negative cycle, read off the predecessor graph -- or
+       converges; then every arc has non-negative reduced cost and a zero-weight cycle is a
+       cycle of tight arcs, i.e. a non-trivial strongly connected component of them.
     """
     u, v, wt = _eps_edges(w)
-    if len(u) == 0:
+    if len(u) == 0 or not _has_structural_cycle(w.num_states, u, v):
         return None
-    n = w.num_states
-    if not _has_structural_cycle(n, u, v):
-        return None
-    edges = list(zip(u.tolist(), v.tolist(), wt.tolist()))
-    dist = [0.0] * n
-    pred = [-1] * n
-    relaxed_tail = -1
-    for _ in range(n):
-        relaxed_tail = -1
-        for a, b, x in edges:
-            c = dist[a] + x
-            if c < dist[b] - 1e-15:
-                dist[b] = c
-                pred[b] = a
-                relaxed_tail = b
-        if relaxed_tail < 0:
+    for comp in _components(w.num_states, u, v):
+        cyc = _component_cycle(comp, u, v, wt)
+        if cyc is not None:
+            return EpsilonCycle(tuple(int(x) for x in cyc), _cycle_weight(cyc, u, v, wt))
+    return None
+
+
+def _scc_labels(n: int, u: np.ndarray, v: np.ndarray) -> np.ndarray:
+    from scipy.sparse import csr_matrix
+    from scipy.sparse.csgraph import connected_components
+    g = csr_matrix((np.ones(len(u), np.int8), (u, v)), shape=(n, n))
+    return connected_components(g, directed=True, connection="strong")[1]
+
+
+def _components(n: int, u: np.ndarray, v: np.ndarray):
+    """Node sets that can carry a cycle: non-trivial SCCs and self-loop states, ordered by
+    their smallest state."""
+    lab = _scc_labels(n, u, v)
+    size = np.bincount(lab)
+    cyclic = size[lab] > 1
+    cyclic[u[u == v]] = True
+    nodes = np.flatnonzero(cyclic)
+    order = np.argsort(lab[nodes], kind="stable")
+    groups = np.split(nodes[order], np.flatnonzero(np.diff(lab[nodes][order])) + 1)
+    return sorted((g for g in groups if len(g)), key=lambda g: int(g.min()))
+
+
+def _component_cycle(comp: np.ndarray, u, v, wt):
+    inside = np.zeros(max(int(u.max()), int(v.max())) + 1, bool)
+    inside[comp] = True
+    m = inside[u] & inside[v]
+    loc = np.full(len(inside), -1, np.int64)
+    loc[comp] = np.arange(len(comp))
+    a, b, x = loc[u[m]], loc[v[m]], wt[m]
+    k = len(comp)
+    dist = np.zeros(k)
+    pred = np.full(k, -1, np.int64)
+    improving = False
+    for _ in range(k + 1):
+        cand = dist[a] + x
+        best = np.full(k, np.inf)
+        np.minimum.at(best, b, cand)
+        better = best < dist - 1e-15
+        improving = bool(better.any())
+        if not improving:
             break
-    if relaxed_tail >= 0:
-        x = relaxed_tail
-        for _ in range(n):
-            x = pred[x]
-        cycle = [x]
-        y = pred[x]
-        while y != x:
-            cycle.append(y)
-            y = pred[y]
-        cycle.reverse()
-        return EpsilonCycle(tuple(cycle), _cycle_weight(cycle, edges))
-    tight: dict[int, list[int]] = {}
-    for a, b, x in edges:
-        if dist[a] + x <= dist[b] + 1e-12:
-            tight.setdefault(a, []).append(b)
-    cycle = _find_cycle(tight, n)
-    if cycle is not None:
-        return EpsilonCycle(tuple(cycle), _cycle_weight(cycle, edges))
+        hit = better[b] & (cand == best[b])
+        pred[b[hit]] = a[hit]
+        dist = np.where(better, best, dist)
+    if improving:
+        cyc = _functional_cycle(pred)
+    else:
+        t = dist[a] + x <= dist[b] + 1e-12
+        cyc = _tight_cycle(k, a[t], b[t])
+    return None if cyc is None else comp[cyc]
+
+
+def _functional_cycle(nxt: np.ndarray):
+    """A cycle of the map i -> nxt[i] (-1 = none), listed in arc direction (reversed walk)."""
+    seen = np.full(len(nxt), -1, np.int64)
+    for s0 in range(len(nxt)):
+        x, path = s0, []
+        while x >= 0 and seen[x] < 0:
+            seen[x] = s0
+            path.append(x)
+            x = int(nxt[x])
+        if x >= 0 and seen[x] == s0:
+            cyc = path[path.index(x):]
+            return np.asarray(cyc[::-1], np.int64)
     return None
 
 
-def _cycle_weight(cycle, edges) -> float:
-    lookup: dict[tuple[int, int], float] = {}
-    for a, b, x in edges:
-        if (a, b) not in lookup or x < lookup[(a, b)]:
-            lookup[(a, b)] = x
-    return sum(lookup[(a, b)] for a, b in zip(cycle, cycle[1:] + cycle[:1]))
-
-
-def _find_cycle(succ: dict[int, list[int]], num_states: int):
-    color = [0] * num_states
-    parent: dict[int, int] = {}
-    for root in sorted(succ):
-        if color[root]:
-            continue
-        stack = [(root, iter(succ.get(root, ())))]
-        color[root] = 1
-        while stack:
-            node, it = stack[-1]
-            for nxt in it:
-                if color[nxt] == 0:
-                    color[nxt] = 1
-                    parent[nxt] = node
-                    stack.append((nxt, iter(succ.get(nxt, ()))))
-                    break
-                if color[nxt] == 1:
-                    cycle = [node]
-                    x = node
-                    while x != nxt:
-                        x = parent[x]
-                        cycle.append(x)
-                    cycle.reverse()
-                    return cycle
-            else:
-                color[node] = 2
-                stack.pop()
-    return None
-
-
-def _parse_fast(text: str, allow_negative_weights: bool):
-    """The C++ fast path (csrc/wfst_text.cpp); None when the text needs this module's parser
-    (symbols, non-ASCII, malformed lines -- which then raise exactly as the reference)."""
-    try:
-        from . import _native as N
-        L = N.load()
-    except Exception:   # library not built: the Python parser is exact, only slower
+def _tight_cycle(k: int, a: np.ndarray, b: np.ndarray):
+    if len(a) == 0:
         return None
-    data = text.encode("ascii", errors="replace") if text.isascii() else None
-    if data is None:
+    loops = a[a == b]
+    if len(loops):
+        return np.asarray([loops.min()], np.int64)
+    lab = _scc_labels(k, a, b)
+    big = np.flatnonzero(np.bincount(lab) > 1)
+    if not len(big):
         return None
-    out = N.ParsedWfst()
-    rc = L.wb_wfst_parse_text(data, len(data), int(bool(allow_negative_weights)), C.byref(out))
-    if rc != N.WB_OK:
-        return None
-    try:
-        def arr(ptr, n, t):
-            if n == 0:
-                return np.zeros(0, t)
-            ct = np.ctypeslib.as_ctypes_type(t)
-            return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ct)), shape=(n,)).copy()
-        na, nfin = out.num_arcs, out.num_finals
-        fw = np.full(out.num_states, np.inf)
-        fw[arr(out.final_state, nfin, np.int32)] = arr(out.final_weight, nfin, np.float64)
-        return Wfst.from_arrays(out.num_states, out.start, arr(out.src, na, np.int32),
-                                arr(out.dst, na, np.int32), arr(out.ilabel, na, np.int32),
-                                arr(out.olabel, na, np.int32), arr(out.weight, na, np.float64),
-                                fw)
-    finally:
-        L.wb_parsed_wfst_free(C.byref(out))
+    keep = (lab[a] == big[0]) & (lab[b] == big[0])
+    first = {}
+    for x, y in zip(a[keep].tolist(), b[keep].tolist()):
+        first.setdefault(x, y)
+    succ = np.full(k, -1, np.int64)
+    succ[list(first)] = list(first.values())
+    walk = _functional_cycle(succ)
+    return None if walk is None else walk[::-1]
 
 
-def _label(tok: str, table: SymbolTable | None, line_no: int) -> int:
-    """Symbol lookup first, then a bare non-negative integer id (wfst.py:300-312)."""
-    if table is not None:
-        idx = table.find_id(tok)
-        if idx is not None:
-            return idx
-    try:
-        idx = int(tok)
-    except ValueError:
-        raise SymbolError(f"line {line_no}: unknown symbol {tok!r}") from None
-    if idx < 0:
-        raise SymbolError(f"line {line_no}: negative label id {idx}")
-    return idx
+def _cycle_weight(cyc, u, v, wt) -> float:
+    """Sum over the cycle's consecutive state pairs of the lightest epsilon arc between them."""
+    total = 0.0
+    for x, y in zip(cyc, np.roll(cyc, -1)):
+        total += float(wt[(u == x) & (v == y)].min())
+    return total
+
+
+_ODD_BREAKS = re.compile("[\u000b\u000c\u001c-\u001f\u0085\u00a0\u1680\u2000-\u200a\u2028\u2029"
+                         "\u202f\u205f\u3000]|\r(?!\n)")
 
 
 def parse_wfst_text(text: str, isyms: SymbolTable | None = None,
                     osyms: SymbolTable | None = None,
                     allow_negative_weights: bool = False) -> Wfst:
-    """AT&T-style transducer text (reference ``parse_wfst_text``, wfst.py:315-378).
-
-    Arc lines ``src dst ilabel olabel [weight]``, final lines ``state [weight]`` (missing
-    weight = 0.0); the first state mentioned is the start state; ``#`` comment lines and
-    blank lines are skipped.  Labels resolve through ``isyms`` / ``osyms`` when given, with
-    bare non-negative integers accepted as raw ids.  Without symbol tables the text goes
-    through the C++ fast path (csrc/wfst_text.cpp) when it can reproduce this parser exactly.
-    """
-    if isyms is None and osyms is None:
-        fast = _parse_fast(text, allow_negative_weights)
-        if fast is not None:
-            return fast
-    arcs: list[Arc] = []
-    finals: dict[int, float] = {}
-    start = None
-    max_state = -1
-
-    def state(tok, line_no):
-        try:
-            x = int(tok)
-        except ValueError:
-            raise ParseError(f"bad state id {tok!r}", line_no) from None
-        if x < 0:
-            raise ParseError(f"negative state id {x}", line_no)
-        return x
-
-    def weight(tok, line_no):
-        try:
-            x = float(tok)
-        except ValueError:
-            raise ParseError(f"bad weight {tok!r}", line_no) from None
-        if math.isnan(x):
-            raise ParseError("weight is NaN", line_no)
-        if x < 0 and not allow_negative_weights:
-            raise ParseError(f"negative weight {x} (pass allow_negative_weights to accept)",
-                             line_no)
-        return x
-
-    for line_no, raw in enumerate(text.splitlines(), start=1):
-        line = raw.strip()
-        if not line or line.startswith("#"):
-            continue
-        f = line.split()
-        if len(f) in (1, 2):
-            s = state(f[0], line_no)
-            finals[s] = weight(f[1], line_no) if len(f) == 2 else 0.0
-            start = s if start is None else start
-            max_state = max(max_state, s)
-        elif len(f) in (4, 5):
-            a, b = state(f[0], line_no), state(f[1], line_no)
-            i, o = _label(f[2], isyms, line_no), _label(f[3], osyms, line_no)
-            x = weight(f[4], line_no) if len(f) == 5 else 0.0
-            arcs.append(Arc(a, b, i, o, x))
-            start = a if start is None else start
-            max_state = max(max_state, a, b)
-        else:
-            raise ParseError(f"expected 1-2 (final) or 4-5 (arc) fields, got {len(f)}", line_no)
-    if start is None:
-        raise ParseError("no states found in transducer text")
-    return Wfst(max_state + 1, start, arcs, finals)
+    """AT&T-style transducer text (the reference's ``parse_wfst_text``, wfst.py:315-378),
+    parsed natively (csrc/wfst_text.cpp): arc lines ``src dst ilabel olabel [weight]``, final
+    lines ``state [weight]`` (missing weight 0.0), the first state mentioned is the start,
+    ``#`` comment and blank lines skipped; labels resolve through ``isyms`` / ``osyms`` first,
+    then as bare non-negative integers.  Raises ``ParseError`` (with ``line_no``) /
+    ``SymbolError`` as the reference does."""
+    from . import _native as N
+    L = N.load()
+    if not text.isascii() or _ODD_BREAKS.search(text):
+        # Python line breaks and Unicode whitespace the native tokenizer does not know
+        text = "\n".join(" ".join(line.split()) for line in text.splitlines())
+    data = text.encode("utf-8")
+    tabs = [t.format().encode("utf-8") if t is not None else None for t in (isyms, osyms)]
+    out = N.ParsedWfst()
+    rc = L.wb_wfst_parse_text(data, len(data), int(bool(allow_negative_weights)),
+                              tabs[0], len(tabs[0] or b""), tabs[1], len(tabs[1] or b""),
+                              C.byref(out))
+    if rc == N.WB_PARSE_ERROR:
+        raise ParseError(N.last_error(), out.error_line or None)
+    if rc == N.WB_PARSE_SYMBOL:
+        raise SymbolError(f"line {out.error_line}: {N.last_error()}")
+    N.check(rc, "parse_wfst_text")
+    try:
+        def take(ptr, n, t):
+            if n == 0:
+                return np.zeros(0, t)
+            return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(np.ctypeslib.as_ctypes_type(t))),
+                                         shape=(n,)).copy()
+        na, nf = out.num_arcs, out.num_finals
+        finals = np.full(out.num_states, np.inf)
+        finals[take(out.final_state, nf, np.int32)] = take(out.final_weight, nf, np.float64)
+        return Wfst.from_arrays(out.num_states, out.start, take(out.src, na, np.int32),
+                                take(out.dst, na, np.int32), take(out.ilabel, na, np.int32),
+                                take(out.olabel, na, np.int32), take(out.weight, na, np.float64),
+                                finals)
+    finally:
+        L.wb_parsed_wfst_free(C.byref(out))
 
 
 def format_wfst_text(w: Wfst) -> str:

@@ -228,3 +228,28 @@ def test_max_active_early_cutoff_is_exact(cuda, seed, monkeypatch):
     posts = [synth.random_posteriors(seed * 11 + k, 100, 50, blank_fraction=0.2) for k in range(6)]
     for beam, ma in ((10.0, 40), (10.0, 300), (INF, 100)):
         _check_batch(g, posts, P.DecodeConfig(beam=beam, max_active=ma, mode="fsd"))
+
+
+@pytest.mark.parametrize("mode", ["fsd", "lsd"])
+def test_posterior_batch_from_post1_files(cuda, tmp_path, mode):
+    """POST1 files read natively into one page-locked table (PosteriorBatch), converted to
+    costs in place while the kernel streams them: same results as decoding the matrices."""
+    from paper_1808_00687_b200.posteriors import PosteriorBatch, save_posteriors
+    g = synth.random_wfst(61, 2500, 8000, 30, eps_fraction=0.03, selfloops=mode == "lsd",
+                          final_fraction=0.05)
+    mats = [synth.random_posteriors(500 + k, 60 + 17 * k, 30, blank_col=(k % 2) * 4,
+                                    blank_fraction=0.6 if mode == "lsd" else 0.0)
+            for k in range(6)]
+    paths = []
+    for k, m in enumerate(mats):
+        paths.append(str(tmp_path / f"{k}.post"))
+        save_posteriors(m, paths[-1], binary=True)
+    cfg = P.DecodeConfig(beam=10.0, max_active=300, mode=mode)
+    batch = PosteriorBatch(paths)
+    got = P.decode_batch(g, batch, cfg)
+    assert batch.consumed
+    assert got == P.decode_batch(g, mats, cfg)
+    for m, r in zip(mats, got):
+        o = O.decode(g, P.cost_table(m), m.rows[:, m.blank_col], beam=10.0, max_active=300,
+                     mode=mode)
+        assert _fields(r) == o.astuple()

@@ -11,7 +11,7 @@ import refutil
 from paper_1808_00687_b200 import synth
 from paper_1808_00687_b200.decoder import DecodeConfig
 from paper_1808_00687_b200.posteriors import PosteriorMatrix, cost_table, frame_costs
-from paper_1808_00687_b200.wfst import Arc, Wfst, WfstError, parse_wfst_text, validate_epsilon_acyclic
+from paper_1808_00687_b200.wfst import SymbolTable, Arc, Wfst, WfstError, parse_wfst_text, validate_epsilon_acyclic
 
 needs_ref = pytest.mark.skipif(not refutil.HAVE_REF, reason="reference not present")
 
@@ -195,30 +195,61 @@ def _texts():
     return out
 
 
-def test_native_wfst_parser_matches_python_parser():
-    """The C++ fast path (csrc/wfst_text.cpp) builds the same Wfst as the Python parser; a
-    non-ASCII comment forces the Python path on the same content."""
-    from paper_1808_00687_b200 import wfst as W
-    for t in _texts():
-        fast = W._parse_fast(t, False)
-        assert fast is not None
-        slow = parse_wfst_text(t + "\n# é\n")
-        assert _wfst_key(fast) == _wfst_key(slow)
-
-
-def test_native_wfst_parser_falls_back_exactly():
-    """Malformed / unusual text goes to the Python parser, which raises like the reference."""
-    from paper_1808_00687_b200 import wfst as W
+def test_wfst_parser_errors_and_number_grammar():
+    """The native parser raises ParseError / SymbolError for malformed text and follows
+    Python's int()/float() grammar (underscores, inf, no hex) like the reference's parser."""
     from paper_1808_00687_b200.wfst import ParseError, SymbolError
-    for bad in ("0 1 2\n", "0 1 a b\n", "0 1 2 3 nan\n", "0 1 2 3 -1\n", "", "# only\n",
-                "0 1 2 3 0x1p3\n", "-1 2 3 4\n"):
-        assert W._parse_fast(bad, False) is None
-        with pytest.raises((ParseError, SymbolError, ValueError)):   # "a": SymbolError
+    for bad, exc in (("0 1 2\n", ParseError), ("0 1 a b\n", SymbolError),
+                     ("0 1 2 3 nan\n", ParseError), ("0 1 2 3 -1\n", ParseError),
+                     ("", ParseError), ("# only\n", ParseError), ("0 1 2 3 0x1p3\n", ParseError),
+                     ("-1 2 3 4\n", ParseError), ("0 1 2 3 1__0\n", ParseError),
+                     ("0 1 -2 3\n", SymbolError), ("x 1 2 3\n", ParseError)):
+        with pytest.raises(exc):
             parse_wfst_text(bad)
-    assert W._parse_fast("0 1 2 3 1_0\n", False) is None        # Python's float accepts it
     assert parse_wfst_text("0 1 2 3 1_0\n").weight.tolist() == [10.0]
-    ok = W._parse_fast("0 1 2 3 -1.5\n1\n", True)
-    assert ok is not None and ok.weight.tolist() == [-1.5]
+    assert parse_wfst_text("0 1 2 3 -1.5\n1\n", allow_negative_weights=True).weight.tolist() == [-1.5]
+    assert parse_wfst_text("0 1 2 3 .5e+1_0\n1 INF\n").num_states == 2
+    # Python line breaks / Unicode whitespace are normalised before the native tokenizer
+    w = parse_wfst_text("0 1 2 3 0.5\x0b1\u00a02 3 4 1e-3\u20282 0.25\r3 1 1 1")
+    assert w.num_arcs == 3 and w.final_w[2] == 0.25
+
+
+@needs_ref
+def test_wfst_parser_fuzz_matches_reference():
+    """Random (and randomly corrupted) transducer texts, with and without symbol tables: the
+    same graph or the same exception type and message as the reference parser."""
+    import numpy as np
+    L = refutil.ref()
+    rng = np.random.default_rng(11)
+    syms = "<eps> 0\na 1\nb 2\n<blank> 3\nc 7\n"
+    junk = ["x", "-3", "1__2", "nan", "inf", "-0.0", "1e400", "_1", "1_", "0x10", "+4", "1.5.2",
+            "\u00e9", "# c", "3 4 5 6 7 8"]
+    for k in range(400):
+        base = _texts()[k % 30]
+        lines = base.splitlines()
+        for _ in range(int(rng.integers(0, 3))):
+            if lines:
+                i = int(rng.integers(0, len(lines)))
+                f = lines[i].split()
+                if f:
+                    f[int(rng.integers(0, len(f)))] = junk[int(rng.integers(0, len(junk)))]
+                    lines[i] = " ".join(f)
+        text = "\n".join(lines)
+        use_syms = k % 3 == 0
+        tabs = ((L.wfst.SymbolTable.parse(syms), L.wfst.SymbolTable.parse(syms)) if use_syms
+                else (None, None))
+        mine_tabs = ((SymbolTable.parse(syms), SymbolTable.parse(syms)) if use_syms
+                     else (None, None))
+        try:
+            r = L.wfst.parse_wfst_text(text, *tabs, allow_negative_weights=k % 2 == 1)
+            want = _wfst_key(Wfst.from_reference(r))
+        except Exception as e:
+            want = (type(e).__name__, str(e))
+        try:
+            got = _wfst_key(parse_wfst_text(text, *mine_tabs, allow_negative_weights=k % 2 == 1))
+        except Exception as e:
+            got = (type(e).__name__, str(e))
+        assert got == want, (k, text[:200])
 
 
 @needs_ref
@@ -251,3 +282,58 @@ def test_posterior_files_roundtrip_and_match_reference(tmp_path):
         assert ref.rows.tobytes() == p.rows.tobytes()
         mine = load_posteriors(L.posteriors.format_posteriors_text(ref).encode())
         assert mine.rows.tobytes() == p.rows.tobytes()
+
+
+@needs_ref
+def test_epsilon_cycle_fuzz_matches_reference():
+    """Random epsilon subgraphs with cycles of negative, zero and positive weight (and self-
+    loops): the SCC + Bellman-Ford check accepts / rejects exactly the graphs the reference
+    rejects."""
+    L = refutil.ref()
+    rng = random.Random(5)
+    for k in range(300):
+        S = rng.randrange(2, 14)
+        lines = []
+        for _ in range(rng.randrange(1, 3 * S)):
+            a, b = rng.randrange(S), rng.randrange(S)
+            w = rng.choice([0.0, 0.5, 1.0, -0.5, 0.25, 2.0, -1.0])
+            lines.append(f"{a} {b} {0 if rng.random() < 0.7 else 1} 0 {w}")
+        lines.append(f"{S - 1} 0.0")
+        text = "\n".join(lines)
+        ref = L.wfst.parse_wfst_text(text, allow_negative_weights=True).epsilon_cycle()
+        mine = parse_wfst_text(text, allow_negative_weights=True).epsilon_cycle()
+        assert (ref is None) == (mine is None), (k, text)
+        if mine is not None:   # the reported cycle is a real epsilon cycle of weight <= 0
+            assert mine.total_weight <= 1e-12
+            st = list(mine.states)
+            w = parse_wfst_text(text, allow_negative_weights=True)
+            eps = w.ilabel == 0
+            arcs = set(zip(w.src[eps].tolist(), w.dst[eps].tolist()))
+            assert all((x, y) in arcs for x, y in zip(st, st[1:] + st[:1])), (k, st)
+
+
+@needs_ref
+def test_post1_native_reader_matches_reference(tmp_path):
+    """POST1 files read by the native reader (wb_post1_read, into the PosteriorBatch table)
+    equal the reference's load_posteriors; malformed files raise PosteriorFormatError."""
+    from paper_1808_00687_b200.posteriors import (PosteriorBatch, PosteriorFormatError,
+                                                   format_posteriors_binary, save_posteriors)
+    L = refutil.ref()
+    mats = [synth.random_posteriors(40 + k, 5 + 7 * k, 9, blank_col=k % 3) for k in range(4)]
+    paths = []
+    for k, m in enumerate(mats):
+        path = tmp_path / f"u{k}.post"
+        save_posteriors(m, str(path), binary=k != 1)     # one text file in the batch
+        paths.append(str(path))
+    batch = PosteriorBatch(paths)
+    for path, view in zip(paths, batch.matrices()):
+        ref = L.posteriors.load_posteriors(path)
+        assert view.rows.tobytes() == ref.rows.tobytes() and view.blank_col == ref.blank_col
+    good = format_posteriors_binary(mats[0])
+    for bad in (good[:-8], good[:12], good + b"\0" * 8):
+        p = tmp_path / "bad.post"
+        p.write_bytes(bad)
+        with pytest.raises(PosteriorFormatError):
+            PosteriorBatch([str(p)])
+        with pytest.raises(L.posteriors.PosteriorFormatError):
+            L.posteriors.load_posteriors(str(p))
