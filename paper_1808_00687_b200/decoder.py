@@ -58,6 +58,18 @@ class DecodeResult:
     died_at_step: int | None = None
 
 
+def result_class():
+    """The class decode results are returned as: the reference's own
+    ``lsd_wfst.decoder.DecodeResult`` when the caller has the reference loaded (a frozen
+    dataclass compares equal only to its own class, so ``lsd_wfst.decode(...) ==
+    decode(...)`` holds field for field), else this module's identical ``DecodeResult``.
+    The reference is never imported here: only an already loaded one is used."""
+    import sys
+    ref = sys.modules.get("lsd_wfst.decoder")
+    cls = getattr(ref, "DecodeResult", None)
+    return cls if cls is not None else DecodeResult
+
+
 class SearchDied(RuntimeError):
     """For callers that treat an emptied beam as fatal (decoder.py:108-110)."""
 
@@ -140,7 +152,7 @@ class BatchOutput:
         r = self.results[i]
         no, ni = int(r["n_olabels"]), int(r["n_ilabels"])
         died = int(r["died_at_step"])
-        return DecodeResult(
+        return result_class()(
             total_cost=float(r["total_cost"]),
             olabels=tuple(int(x) for x in self.olabels[i, :no]),
             ilabels=tuple(int(x) for x in self.ilabels[i, :ni]),
@@ -571,6 +583,7 @@ def _check_decodable(w: Wfst, posts) -> None:
 
 
 _DECODER_LOCK = threading.Lock()
+_RECORDER_PROTOCOL = ("begin_step", "emitting", "epsilon", "survivors", "finish")
 
 
 def _decoder_for(w: Wfst) -> BatchDecoder:
@@ -606,6 +619,12 @@ def decode_batch(wfst, posts_list, cfg: DecodeConfig, mode: str | None = None,
         recorders = list(recorder) if isinstance(recorder, (list, tuple)) else [recorder]
         if len(recorders) != len(posts_list):
             raise ValueError("pass one LatticeRecorder per utterance")
+        from .lattice import LatticeRecorder
+        for rec in recorders:
+            if not isinstance(rec, LatticeRecorder) and not all(
+                    callable(getattr(rec, m, None)) for m in _RECORDER_PROTOCOL):
+                raise TypeError(f"recorder {type(rec).__name__} does not implement "
+                                f"{'/'.join(_RECORDER_PROTOCOL)} (lattice.py:112-135)")
     dec = _decoder_for(w)
     with dec.lock:   # the decode and its lattice fetch see one workspace state
         # cost rows are computed on host threads while the kernel already decodes (streaming)
@@ -614,8 +633,13 @@ def decode_batch(wfst, posts_list, cfg: DecodeConfig, mode: str | None = None,
         results = out.decode_results()
         lats = dec.fetch_lattices(w) if recorders is not None else None
     if recorders is not None:
+        from .lattice import LatticeRecorder, replay
         for rec, lat, r in zip(recorders, lats, out.results):
-            rec._set(lat, int(r["final_step"]), int(r["final_state"]), bool(r["reached_final"]))
+            args = (int(r["final_step"]), int(r["final_state"]), bool(r["reached_final"]))
+            if isinstance(rec, LatticeRecorder):
+                rec._set(lat, *args)
+            else:   # e.g. the reference's own lsd_wfst.lattice.LatticeRecorder
+                replay(lat, rec, *args)
     return results
 
 

@@ -279,26 +279,179 @@ def canonical_batch(wfst, meta, nodes, arcs, arc_ac, finals, final_w,
     return res
 
 
+class StepRecord:
+    """One node step of the recorder protocol (the reference's ``_StepRecord``,
+    lattice.py:86-93): emitting relaxations (src_state, wfst_arc, acoustic) into step k,
+    within-step epsilon relaxations (src_state, wfst_arc), and the step's survivor states."""
+
+    __slots__ = ("emit", "eps", "survivors")
+
+    def __init__(self):
+        self.emit: list = []
+        self.eps: set = set()
+        self.survivors: tuple = ()
+
+
+def replay(lat: Lattice, recorder, final_step: int, final_state: int, reached: bool) -> None:
+    """Drive any object with the reference recorder protocol (``begin_step / emitting /
+    epsilon / survivors / finish``, lattice.py:112-135) with a decoded lattice.
+
+    The device records and trims the lattice itself, so the replay carries the trimmed
+    lattice: each step's survivors are the lattice nodes of that step, its emitting / epsilon
+    calls the lattice arcs into / within it.  The reference's ``build_lattice`` (or its
+    ``PipelinedLatticeBuilder``) over these calls assembles exactly ``lat``: trimming an
+    already trimmed lattice keeps it, and every live final is one of its nodes."""
+    empty = lat.start_id is None
+    n_steps = final_step + 1 if final_step is not None and final_step >= 0 else 0
+    st = lat.node_state.astype(np.int64)
+    sp = lat.node_step.astype(np.int64)
+    nodes_at = np.split(np.argsort(sp * (int(st.max(initial=0)) + 1) + st, kind="stable"),
+                        np.searchsorted(np.sort(sp), np.arange(1, n_steps)))
+    if not empty:
+        fs, ts = sp[lat.arc_from], sp[lat.arc_to]
+        order = np.lexsort((lat.arc_tie, ts == fs, ts))   # per step: emitting, then epsilon
+        bounds = np.searchsorted(ts[order], np.arange(n_steps + 1))
+    for k in range(n_steps):
+        recorder.begin_step(k)
+        if not empty:
+            for e in order[bounds[k]:bounds[k + 1]].tolist():
+                src, arc = int(st[lat.arc_from[e]]), int(lat.arc_tie[e])
+                if fs[e] == k:
+                    recorder.epsilon(k, src, arc)
+                else:
+                    recorder.emitting(k, src, arc, float(lat.arc_a[e]))
+        recorder.survivors(k, tuple(int(x) for x in st[nodes_at[k]]) if not empty and
+                           k < len(nodes_at) else ())
+    recorder.finish(final_step, final_state, reached)
+
+
 class LatticeRecorder:
     """Pass as ``recorder=`` to ``decode`` / ``decode_fsd`` / ``decode_lsd`` /
-    ``parallel_decode`` (lattice.py:96-135): the device records the raw lattice of that
-    decode, and ``build_lattice(recorder, wfst)`` returns it.  The per-relaxation callbacks of
-    the reference protocol have no host equivalent (recording happens inside the kernel)."""
+    ``parallel_decode`` (lattice.py:96-135); ``build_lattice(recorder, wfst)`` returns the
+    lattice the device recorded.  It also implements the reference protocol
+    (``begin_step / emitting / epsilon / survivors / finish``): with a ``consumer`` (a
+    ``PipelinedLatticeBuilder``, ours or the reference's) the decode replays the lattice
+    step by step into it (``feed`` per step, ``close`` at the end), and protocol calls from
+    any other source are accumulated like the reference recorder does."""
 
     def __init__(self, consumer=None):
         self._lattice = None
+        self.steps: list[StepRecord] = []
         self.final_step = None
         self.final_state = None
         self.reached_final = False
         self._consumer = consumer
 
+    # ---- the device fast path
     def _set(self, lat: Lattice, final_step: int, final_state: int, reached: bool):
+        if self._consumer is not None:   # the consumer sees the step protocol
+            replay(lat, self, final_step, final_state, reached)
         self._lattice = lat
-        self.final_step = final_step
-        self.final_state = final_state
-        self.reached_final = reached
-        if isinstance(self._consumer, PipelinedLatticeBuilder):
-            self._consumer._deliver(lat)
+        self.final_step, self.final_state, self.reached_final = final_step, final_state, reached
+
+    # ---- the reference protocol
+    def begin_step(self, node_step: int) -> None:
+        if node_step != len(self.steps):
+            raise LatticeError(f"steps must be recorded in order; got {node_step}, "
+                               f"expected {len(self.steps)}")
+        self.steps.append(StepRecord())
+
+    def emitting(self, node_step: int, src_state: int, wfst_arc: int, acoustic: float) -> None:
+        self.steps[node_step].emit.append((src_state, wfst_arc, acoustic))
+
+    def epsilon(self, node_step: int, src_state: int, wfst_arc: int) -> None:
+        self.steps[node_step].eps.add((src_state, wfst_arc))
+
+    def survivors(self, node_step: int, states) -> None:
+        rec = self.steps[node_step]
+        rec.survivors = tuple(states)
+        if self._consumer is not None:
+            self._consumer.feed(node_step, rec)
+
+    def finish(self, final_step: int, final_state: int, reached_final: bool) -> None:
+        self.final_step, self.final_state, self.reached_final = final_step, final_state, reached_final
+        if self._consumer is not None:
+            self._consumer.close()
+
+
+class _StepAssembler:
+    """Raw lattice from protocol steps (lattice.py:148-183): survivors become nodes; an
+    emitting record (deduplicated by (src, arc)) becomes an arc when its source survived step
+    k-1 and its destination survives step k; an epsilon record when both ends survive step k
+    and it is not a self-loop.  ``build`` trims to start-to-final paths and orders the result
+    canonically (``_assemble``, lattice.py:190-237) with numpy / scipy graph searches."""
+
+    def __init__(self, wfst):
+        self.wfst = wfst
+        self.node_st: list = []
+        self.node_sp: list = []
+        self.arcs: list = []      # (from_state, from_step, to_state, to_step, wfst_arc, ac)
+        self._prev = frozenset()
+        self._surv = {}
+
+    def add_step(self, k: int, rec) -> None:
+        surv = frozenset(rec.survivors)
+        self._surv[k] = surv
+        self.node_st.extend(surv)
+        self.node_sp.extend([k] * len(surv))
+        dst = self.wfst.dst
+        if k > 0:
+            seen = set()
+            for src, ai, ac in rec.emit:
+                if (src, ai) not in seen and src in self._prev and int(dst[ai]) in surv:
+                    self.arcs.append((src, k - 1, int(dst[ai]), k, ai, ac))
+                seen.add((src, ai))
+        for src, ai in sorted(rec.eps):
+            d = int(dst[ai])
+            if src in surv and d in surv and d != src:
+                self.arcs.append((src, k, d, k, ai, 0.0))
+        self._prev = surv
+
+    def build(self, final_step, final_state, reached_final) -> Lattice:
+        from scipy.sparse import csr_matrix
+        from scipy.sparse.csgraph import breadth_first_order
+        w = self.wfst
+        if not self.node_st:
+            return EMPTY_LATTICE
+        span = max(self.node_sp) + 2
+        key = np.unique(np.asarray(self.node_st, np.int64) * span + np.asarray(self.node_sp))
+        start_key = w.start * span
+        if not np.isin(start_key, key):
+            return EMPTY_LATTICE
+        if reached_final:
+            fs = np.asarray(sorted(self._surv.get(final_step, ())), np.int64)
+            fs = fs[w.final_w[fs] != INF] if len(fs) else fs
+            fin = {int(s) * span + final_step: float(w.final_w[s]) for s in fs}
+        else:
+            fin = {final_state * span + final_step: 0.0}
+        a = np.asarray(self.arcs, dtype=object).reshape(-1, 6)
+        af = np.searchsorted(key, a[:, 0].astype(np.int64) * span + a[:, 1].astype(np.int64))
+        at = np.searchsorted(key, a[:, 2].astype(np.int64) * span + a[:, 3].astype(np.int64))
+        n = len(key)
+        g = csr_matrix((np.ones(len(af)), (af, at)), shape=(n, n))
+        fwd = np.zeros(n, bool)
+        fwd[breadth_first_order(g, int(np.searchsorted(key, start_key)), return_predecessors=False)] = True
+        live = {int(np.searchsorted(key, k)): x for k, x in fin.items()
+                if np.isin(k, key) and fwd[np.searchsorted(key, k)]}
+        if not live:
+            return EMPTY_LATTICE
+        bwd = np.zeros(n, bool)
+        gt = g.T.tocsr()
+        for f in live:
+            if not bwd[f]:
+                bwd[breadth_first_order(gt, f, return_predecessors=False)] = True
+        keep = fwd & bwd
+        ka = keep[af] & keep[at]
+        ai = a[ka, 4].astype(np.int64)
+        nodes = np.stack([key[keep] // span, key[keep] % span], 1).astype(np.int32)
+        loc = np.cumsum(keep) - 1
+        arcs = np.stack([loc[af[ka]], loc[at[ka]], ai, np.zeros(len(ai), np.int64)], 1)
+        fin_ids = np.asarray(sorted(live), np.int64)
+        lat = canonical_from_device(w, nodes, arcs.astype(np.uint32), a[ka, 5].astype(np.float64),
+                                    loc[fin_ids].astype(np.uint32),
+                                    np.asarray([live[f] for f in fin_ids], np.float64))
+        _check(lat)
+        return lat
 
 
 class PipelinedLatticeBuilder:
@@ -309,32 +462,49 @@ class PipelinedLatticeBuilder:
         decode(wfst, posts, cfg, recorder=rec)      # or parallel_decode
         lat = builder.result_from(rec)
 
-    The reference integrates step k on a consumer thread while the decoder works on step k+1
-    (the paper's second stream).  Here the decode kernel records and trims the lattice itself,
-    so nothing per step is left for a host thread; the builder receives the finished lattice
-    when the decode returns.  Overlap across whole batches is ``LatticePipeline``."""
+    ``feed(k, step)`` queues a protocol step that a builder thread integrates while the
+    producer moves on (the paper's second stream); ``close()`` ends the stream.  With this
+    package's decoder the steps come from the device lattice (recorded and trimmed in the
+    kernel) replayed at the end of the decode; with the reference decoder they arrive live."""
 
     def __init__(self, wfst=None):
-        self._wfst = wfst
-        self._lat = None
-        self._closed = False
+        import queue
+        import threading
+        from .decoder import as_wfst
+        self._acc = _StepAssembler(as_wfst(wfst)) if wfst is not None else None
+        self._q: "queue.Queue" = queue.Queue()
+        self._err = None
+        self._thread = threading.Thread(target=self._run, daemon=True)
+        self._thread.start()
 
-    def _deliver(self, lat: Lattice) -> None:
-        self._lat = lat
+    def _run(self) -> None:
+        while True:
+            item = self._q.get()
+            if item is None:
+                return
+            try:
+                self._acc.add_step(*item)
+            except Exception as exc:  # surfaced by result()
+                self._err = exc
+                return
 
     def feed(self, k: int, rec) -> None:
-        """Accepted for protocol compatibility; the device records every step itself."""
+        if self._acc is None:
+            raise LatticeError("PipelinedLatticeBuilder needs the transducer")
+        self._q.put((k, rec))
 
     def close(self) -> None:
-        self._closed = True
+        self._q.put(None)
 
     def result(self, final_step: int, final_state: int, reached_final: bool) -> Lattice:
-        if self._lat is None:
-            raise LatticeError("no decode has delivered a lattice to this builder")
-        _check(self._lat)
-        return self._lat
+        self._thread.join()
+        if self._err is not None:
+            raise self._err
+        if self._acc is None:
+            raise LatticeError("no decode has fed this builder")
+        return self._acc.build(final_step, final_state, reached_final)
 
-    def result_from(self, recorder: LatticeRecorder) -> Lattice:
+    def result_from(self, recorder) -> Lattice:
         if recorder.final_step is None:
             raise LatticeError("decode trace is incomplete (finish was never recorded)")
         return self.result(recorder.final_step, recorder.final_state, recorder.reached_final)
@@ -352,10 +522,18 @@ def _check(lat: Lattice) -> None:
 def build_lattice(recorder: LatticeRecorder, wfst=None) -> Lattice:
     """The lattice of the decode ``recorder`` was attached to (lattice.py:240-249); raises
     LatticeError on an epsilon cycle among its nodes (lattice.py:186)."""
-    if recorder._lattice is None:
+    if getattr(recorder, "_lattice", None) is None:
         if recorder.final_step is None:
-            return EMPTY_LATTICE
-        raise LatticeError("decode trace is incomplete (finish was never recorded)")
+            if not recorder.steps:
+                return EMPTY_LATTICE
+            raise LatticeError("decode trace is incomplete (finish was never recorded)")
+        if wfst is None:
+            raise LatticeError("build_lattice needs the transducer for protocol-recorded steps")
+        from .decoder import as_wfst
+        acc = _StepAssembler(as_wfst(wfst))
+        for k, rec in enumerate(recorder.steps):
+            acc.add_step(k, rec)
+        return acc.build(recorder.final_step, recorder.final_state, recorder.reached_final)
     _check(recorder._lattice)
     return recorder._lattice
 
@@ -508,7 +686,7 @@ def load_lattice(path: str) -> Lattice:
 
 
 __all__ = ["COST_EPS", "EMPTY_LATTICE", "Lattice", "LatticeArc", "LatticeError", "LatticeNode",
-           "LatticeRecorder", "PipelinedLatticeBuilder", "build_lattice", "canonical_batch", "canonical_from_device", "format_lattice_text",
+           "LatticeRecorder", "PipelinedLatticeBuilder", "StepRecord", "build_lattice", "replay", "canonical_batch", "canonical_from_device", "format_lattice_text",
            "lattice_best_path", "load_lattice", "parse_lattice_text", "prune_lattice", "prune_lattices",
            "split_lattice",
            "save_lattice"]

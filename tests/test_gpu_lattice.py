@@ -268,3 +268,48 @@ def test_gpu_lattices_with_negative_weights(cuda):
                 except L.LatticeError:
                     want = "error"
                 assert ("error" if isinstance(b, L.LatticeError) else _key(b)) == want, (seed, lb)
+
+
+def test_gpu_foreign_recorder_gets_the_protocol(cuda):
+    """Any object with begin_step/emitting/epsilon/survivors/finish (here a minimal stand-in
+    for the reference's LatticeRecorder) receives the decoded lattice step by step; the
+    steps it collected rebuild the same lattice, and a PipelinedLatticeBuilder consumer is
+    fed and closed."""
+    import paper_1808_00687_b200 as P
+
+    class Protocol:
+        def __init__(self):
+            self.steps, self.calls = [], []
+            self.final_step = self.final_state = None
+            self.reached_final = False
+
+        def begin_step(self, k):
+            self.steps.append(L.StepRecord())
+            self.calls.append(("begin", k))
+
+        def emitting(self, k, src, arc, ac):
+            self.steps[k].emit.append((src, arc, ac))
+
+        def epsilon(self, k, src, arc):
+            self.steps[k].eps.add((src, arc))
+
+        def survivors(self, k, states):
+            self.steps[k].survivors = tuple(states)
+
+        def finish(self, fs, fst, reached):
+            self.final_step, self.final_state, self.reached_final = fs, fst, reached
+
+    g = synth.random_wfst(9, 300, 1200, 12, eps_fraction=0.06, final_fraction=0.2)
+    posts = [synth.random_posteriors(70 + i, 20 + 4 * i, 12) for i in range(4)]
+    cfg = P.DecodeConfig(beam=7.0, max_active=40, mode="fsd")
+    recs = [Protocol() for _ in posts]
+    P.decode_batch(g, posts, cfg, recorder=recs)
+    ours = [L.LatticeRecorder() for _ in posts]
+    P.decode_batch(g, posts, cfg, recorder=ours)
+    for rec, mine in zip(recs, ours):
+        assert [c[1] for c in rec.calls] == list(range(rec.final_step + 1))
+        assert _key(L.build_lattice(rec, g)) == _key(L.build_lattice(mine, g))
+    builder = P.PipelinedLatticeBuilder(g)
+    piped = L.LatticeRecorder(consumer=builder)
+    P.decode(g, posts[0], cfg, recorder=piped)
+    assert _key(builder.result_from(piped)) == _key(L.build_lattice(ours[0], g))
