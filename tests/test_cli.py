@@ -267,5 +267,6 @@ def test_pipelined_builder_without_decode_raises():
     b = PipelinedLatticeBuilder(None)
     with pytest.raises(LatticeError):
         b.result_from(LatticeRecorder(consumer=b))
-    b.feed(0, None)
+    with pytest.raises(LatticeError):   # no transducer to assemble steps against
+        b.feed(0, None)
     b.close()
