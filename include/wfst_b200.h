@@ -129,7 +129,9 @@ typedef struct {
     int32_t max_frames;          /* longest utterance a call may contain */
     int32_t block_threads;       /* 256, 512 or 1024 */
     int64_t lattice_capacity;    /* raw lattice nodes (and arcs) per utterance lane */
-    int64_t hash_entries;        /* reserved (0) */
+    int32_t cluster_ctas;        /* CTAs per utterance lane (thread-block cluster): 1, 2, 4, 8;
+                                    0 = auto (2 or 4 when utterances leave SMs idle) */
+    int32_t _pad;
     int64_t lattice_out_capacity;/* trimmed lattice nodes / arcs / finals per wb_decode call */
 } wb_decoder_opts;
 
@@ -307,6 +309,9 @@ void wb_parsed_wfst_free(wb_parsed_wfst *p);
  */
 int wb_post1_info(const char *path, int32_t *num_frames, int32_t *num_cols, int32_t *blank_col);
 int wb_post1_read(const char *path, double *dst, int64_t dst_ld);
+
+/* CTAs per utterance lane (thread-block cluster size) of the last decode launch. */
+int wb_last_launch(wb_decoder_t d, int32_t *cluster_ctas);
 
 /* Device time (ms) of the decode kernel of the last wb_decode call (CUDA events on its stream). */
 int wb_last_kernel_ms(wb_decoder_t d, float *ms);

@@ -51,7 +51,8 @@ class DecoderOpts(C.Structure):
     _fields_ = [("max_utts_in_flight", C.c_int32), ("cand_capacity", C.c_int32),
                 ("arena_capacity", C.c_int64), ("max_frames", C.c_int32),
                 ("block_threads", C.c_int32), ("lattice_capacity", C.c_int64),
-                ("hash_entries", C.c_int64), ("lattice_out_capacity", C.c_int64)]
+                ("cluster_ctas", C.c_int32), ("_pad", C.c_int32),
+                ("lattice_out_capacity", C.c_int64)]
 
 
 class ParsedWfst(C.Structure):
@@ -90,7 +91,7 @@ EXPORTED = ("wb_last_error", "wb_version", "wb_device_count", "wb_graph_create",
             "wb_lattice_arrays_free", "wb_lattice_best_path", "wb_last_transfer",
             "wb_lattice_canonical", "wb_lattice_pruned_totals", "wb_lattice_pruned_fetch",
             "wb_lattice_split", "wb_decode_stream", "wb_decode_finish", "wb_wfst_parse_text",
-            "wb_parsed_wfst_free", "wb_gather_rows", "wb_post1_info", "wb_post1_read")
+            "wb_parsed_wfst_free", "wb_gather_rows", "wb_post1_info", "wb_post1_read", "wb_last_launch")
 
 
 def load():
@@ -121,6 +122,7 @@ def load():
     L.wb_gather_rows.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32,
                                  C.c_int32, C.c_void_p, C.c_int64, C.c_int32]
     L.wb_gather_rows.restype = None
+    L.wb_last_launch.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
     L.wb_post1_info.argtypes = [C.c_char_p] + [C.POINTER(C.c_int32)] * 3
     L.wb_post1_read.argtypes = [C.c_char_p, C.c_void_p, C.c_int64]
     L.wb_decode_finish.argtypes = [C.c_void_p] + [C.c_void_p] * 3

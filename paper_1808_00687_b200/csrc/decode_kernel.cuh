@@ -25,6 +25,7 @@
 // Arithmetic is float64 in the reference's association order, so costs, survivor sets,
 // tokens_expanded and (tie-free) labels are bit-identical to decoder.py.
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "../../include/wfst_b200.h"
@@ -89,6 +90,9 @@ struct WorkDev {
     int eps_dedup;        // epsilon frontier: drop repeated pushes of a state within a round
     int ma_early;         // expand: max-active early cutoff (cheaper tokens first, see expand)
     int force_radix;      // prune: radix-select every boundary bucket (test knob, WB_FORCE_RADIX)
+    int K, kshift;        // CTAs per utterance lane (a thread-block cluster of K = 1 << kshift);
+                          // CTA rank r owns candidate / frontier indices [r*cap, (r+1)*cap)
+    int lcap;             // K * cap: a lane's candidate / token / frontier capacity
     int4 *tok_info;       // [slots][2][cap] {state, trace, emit_lo, emit_hi}
     double *tok_cost;     // [slots][2][cap]
     int *frames;          // [slots][T_cap]
@@ -164,6 +168,17 @@ struct Smem {
     int next_chunk;     // expand: next unclaimed 32-token chunk (warps claim chunks dynamically)
     int ready_seen;     // streaming: last ready count read for the current utterance
     int pflags;         // WB_PATH_* bits of the current utterance (thread 0 writes)
+    // cluster lanes (K > 1): per-CTA values the other CTAs of the lane read through DSMEM
+    // after a cluster barrier
+    int nfr[2];         // epsilon frontier entries pushed for round parity 0 / 1
+    u64 x_mn, x_mx;     // this CTA's candidate key min / max (prune)
+    long long x_sum;    // this CTA's partial sum of a cluster reduction
+    int x_n, x_flags;   // this CTA's candidates this step; bit 0 overflow, bit 1 keys in global
+    int x_gn;           // rank 0: boundary-bucket members collected from the lane's CTAs
+    int x_stream;       // this CTA timed out waiting for a streamed cost row (cluster lanes)
+    int x_ck, x_cs;     // kept / surviving candidates of this CTA (compaction bases)
+    u64 x_run_min;      // this CTA's exact emitting minimum (expand)
+    long long x_cnt[4]; // per-CTA counters summed at the utterance end
     double tok_lo, tok_hi;  // cost range of the current live tokens (from the last prune)
     float ma_frac;          // max-active early cutoff: split point in [tok_lo, tok_hi]
     u64 ma_thr;             // its bound key for the step
@@ -210,6 +225,29 @@ __device__ __forceinline__ void tick(int ph) {
         sh.pc[ph] += t - sh.t_mark;
         sh.t_mark = t;
     }
+}
+
+// ------------------------------------------------------------------ cluster lanes
+// With K > 1 an utterance lane is a thread-block cluster: the K CTAs (on K SMs of one GPC)
+// split every per-step phase and meet at cluster barriers; per-CTA partial results are read
+// by the others straight from their shared memory (DSMEM, mapa).  K == 1 is the plain CTA.
+__device__ __forceinline__ int cta_rank() {
+    u32 r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return (int)r;
+}
+// Every thread of every CTA of the lane; release/acquire at cluster scope, so global and
+// shared writes before it are visible to all CTAs of the lane after it.
+__device__ __forceinline__ void lane_sync(int K) {
+    if (K > 1)
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    else
+        __syncthreads();
+}
+// The same shared-memory object in CTA `rank` of this cluster (generic address into DSMEM).
+template <class T>
+__device__ __forceinline__ T *peer(T *p, int rank) {
+    return cooperative_groups::this_cluster().map_shared_rank(p, (unsigned)rank);
 }
 
 // ------------------------------------------------------------------ block primitives
@@ -278,8 +316,10 @@ struct Lane {
     // parameters on use (constant-bank loads + one IMAD) instead of living in registers or
     // on the stack across the persistent loop.
     const WorkDev &ws;
-    __device__ __forceinline__ size_t so() const { return (size_t)blockIdx.x * (size_t)ws.S; }
-    __device__ __forceinline__ size_t co() const { return (size_t)blockIdx.x * (size_t)ws.cap; }
+    // the lane of this CTA: a cluster of K CTAs shares one lane's workspace
+    __device__ __forceinline__ size_t lane() const { return (size_t)(blockIdx.x >> ws.kshift); }
+    __device__ __forceinline__ size_t so() const { return lane() * (size_t)ws.S; }
+    __device__ __forceinline__ size_t co() const { return lane() * (size_t)ws.lcap; }
     __device__ __forceinline__ Slot *slot() const { return ws.slot + so(); }
     __device__ __forceinline__ u32 *cand_of() const { return ws.cand_of + so(); }
     __device__ __forceinline__ u32 *qtag() const { return ws.qtag + so(); }
@@ -289,16 +329,16 @@ struct Lane {
     __device__ __forceinline__ u32 *cand_pay() const { return ws.cand_pay + co(); }
     __device__ __forceinline__ u64 *cand_key() const { return ws.cand_key + co(); }
     __device__ __forceinline__ u32 *cand_ca() const { return ws.cand_ca + co(); }
-    __device__ __forceinline__ u32 *front(int k) const { return ws.front + 2 * co() + (size_t)k * ws.cap; }
-    __device__ __forceinline__ int4 *frng(int k) const { return ws.frng + 2 * co() + (size_t)k * ws.cap; }
+    __device__ __forceinline__ u32 *front(int k) const { return ws.front + 2 * co() + (size_t)k * ws.lcap; }
+    __device__ __forceinline__ int4 *frng(int k) const { return ws.frng + 2 * co() + (size_t)k * ws.lcap; }
     __device__ __forceinline__ int4 *tok_info(int k) const {
-        return ws.tok_info + 2 * co() + (size_t)k * ws.cap;
+        return ws.tok_info + 2 * co() + (size_t)k * ws.lcap;
     }
     __device__ __forceinline__ double *tok_cost(int k) const {
-        return ws.tok_cost + 2 * co() + (size_t)k * ws.cap;
+        return ws.tok_cost + 2 * co() + (size_t)k * ws.lcap;
     }
-    __device__ __forceinline__ int *frames() const { return ws.frames + (size_t)blockIdx.x * ws.T_cap; }
-    __device__ __forceinline__ u64 *arena() const { return ws.arena + (size_t)blockIdx.x * ws.arena_cap; }
+    __device__ __forceinline__ int *frames() const { return ws.frames + lane() * ws.T_cap; }
+    __device__ __forceinline__ u64 *arena() const { return ws.arena + lane() * ws.arena_cap; }
 };
 
 
@@ -308,10 +348,12 @@ struct Lane {
 // candidate indices from one shared-memory atomic per warp.  `rng` = the state's
 // {eps_lo, emit_lo, emit_hi} from the arc record.  Epsilon graphs: states with epsilon arcs
 // record their candidate index (frontier lookups) and, if `push`, join the frontier.
+// Candidate indices of CTA rank r are r*capK + (its local count): appends stay CTA-local.
+// Frontier pushes go to this CTA's frontier region (`front_out`, counter `*nfront`).
 template <int BLOCK>
 __device__ __forceinline__ int warp_append(bool first, u32 d, int4 rng, bool push,
                                            const GraphDev &g, const WorkDev &ws,
-                                           u32 *front_out, int4 *frng_out) {
+                                           u32 *front_out, int4 *frng_out, int *nfront, int cbase) {
     Smem<BLOCK> &sh = SH<BLOCK>();
     const Lane c{ws};
     const u32 m = __ballot_sync(FULL, first);
@@ -321,10 +363,11 @@ __device__ __forceinline__ int warp_append(bool first, u32 d, int4 rng, bool pus
     int base = 0;
     if (l == leader) base = atomicAdd(&sh.n_cand, __popc(m));
     base = __shfl_sync(FULL, base, leader);
-    const int idx = base + __popc(m & lanemask_lt());
+    const int loc = base + __popc(m & lanemask_lt());
+    const int idx = cbase + loc;
     bool pf = false;
     if (first) {
-        if (idx < ws.cap) {
+        if (loc < ws.cap) {
             c.cand_state()[idx] = d;
             c.cand_rng()[idx] = make_int4(rng.x, rng.y, rng.z, 0);
             if (g.has_eps && rng.x < rng.y) {
@@ -340,7 +383,7 @@ __device__ __forceinline__ int warp_append(bool first, u32 d, int4 rng, bool pus
         if (mf) {
             const int lf = __ffs(mf) - 1;
             int fb = 0;
-            if (l == lf) fb = atomicAdd(&sh.n_front, __popc(mf));
+            if (l == lf) fb = atomicAdd(nfront, __popc(mf));
             fb = __shfl_sync(FULL, fb, lf);
             if (pf) {
                 const int f = fb + __popc(mf & lanemask_lt());
@@ -349,7 +392,7 @@ __device__ __forceinline__ int warp_append(bool first, u32 d, int4 rng, bool pus
             }
         }
     }
-    return (first && idx < ws.cap) ? idx : -1;
+    return (first && loc < ws.cap) ? idx : -1;
 }
 
 // Install `want` in *p under the (cost, arc) total order, optimistic first attempt already
@@ -477,7 +520,7 @@ __device__ __noinline__ u64 ma_bound(int max_active, const WorkDev &ws) {
     return sh.ma_thr ? sh.ma_thr : EMPTY_KEY;
 }
 
-template <int BLOCK>
+template <int BLOCK, int KC>
 __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const double *row,
                                                      const GraphDev &g, const WorkDev &ws,
                                                      double beam, bool row_nonneg, bool piloted,
@@ -490,15 +533,25 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
     const int4 *__restrict__ tinfo = c.tok_info(cur);
     const double *__restrict__ tcost = c.tok_cost(cur);
     Slot *slot = c.slot();
-    u32 *front0 = c.front(0);
-    int4 *frng0 = c.frng(0);
-    const int nchunks = (n_live + 31) >> 5;
+    // cluster lanes: this CTA expands the 32-token chunks ch = r + K * j (j = 0, 1, ...) and
+    // registers its candidates / frontier pushes in its own index range
+    constexpr int KS = KC >= 8 ? 3 : KC >= 4 ? 2 : KC >= 2 ? 1 : 0;
+    const int r = KC > 1 ? cta_rank() : 0;
+    const int cbase = r * ws.cap;
+    u32 *front0 = c.front(0) + cbase;
+    int4 *frng0 = c.frng(0) + cbase;
+    int *nfr0 = &SH<BLOCK>().nfr[0];
+    const int nchunks_all = (n_live + 31) >> 5;
+    const int nchunks = (nchunks_all - r + KC - 1) >> KS;   // this CTA's chunks
+    auto chunk_of = [&](int j) { return r + (j << KS); };
     const Slot empty = {EMPTY_KEY, 0xFFFFFFFFu, 0xFFFFFFFFu};
     if (ws.stage_off) {
         // Software-pipelined: each lane prefetches its next arc record into shared memory
         // (cp.async, no registers held) while its current relaxation's CAS is in flight, so an
-        // iteration costs one memory round trip instead of two.
-        int4 *stage = reinterpret_cast<int4 *>(dyn_smem() + ws.stage_off) + 2 * threadIdx.x;
+        // iteration costs one memory round trip instead of two.  The two-deep ring is
+        // buffer-major ([2][BLOCK] x 16 B): a warp's 16-byte reads are contiguous (4
+        // wavefronts, no bank conflicts).
+        int4 *stage = reinterpret_cast<int4 *>(dyn_smem() + ws.stage_off) + threadIdx.x;
         const bool skip_on = g.nonneg && beam < INFINITY && ws.beam_skip;
         auto sh_run_min = [&]() -> u64 { return *(volatile u64 *)&SH<BLOCK>().run_min; };
         bool exact = false;
@@ -524,12 +577,12 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
                   double tcs[2];
 #pragma unroll
                   for (int q = 0; q < 2; ++q) {
-                    const int t = ((ch0 + q * NW) << 5) + l;
-                    tcs[q] = t < n_live ? tcost[t] : INFINITY;
+                    const int t = (chunk_of(ch0 + q * NW) << 5) + l;
+                    tcs[q] = (ch0 + q * NW < nchunks && t < n_live) ? tcost[t] : INFINITY;
                   }
 #pragma unroll
                   for (int q = 0; q < 2; ++q) {
-                    const int t = ((ch0 + q * NW) << 5) + l;
+                    const int t = (chunk_of(ch0 + q * NW) << 5) + l;
                     const double tc = tcs[q];
                     const bool pass = tc < bound && t != bt;
                     if (!__any_sync(FULL, pass)) continue;
@@ -570,7 +623,7 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
         // max-active early cutoff: pass 0 expands the tokens up to a split cost, ma_bound
         // turns the candidates it registered into a bound, pass 1 expands the rest against it
         const bool ma_on = ws.ma_early > 0 && n_live >= ws.ma_early && max_active > 0 && !ws.rlog &&
-                           g.nonneg && ws.beam_skip;
+                           g.nonneg && ws.beam_skip && KC == 1;
         u64 ma_thr = EMPTY_KEY;
         double split = INFINITY;
         if (ma_on) {
@@ -591,9 +644,10 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
         }
         // warps claim 32-token chunks dynamically (first chunk = warp id), so no warp idles at
         // the closing barrier while another still has two chunks to go
-        for (int ch = w; ch < nchunks;) {
+        for (int lc = w; lc < nchunks;) {
             int ch_claim = 0;
             if (l == 0) ch_claim = atomicAdd(&SH<BLOCK>().next_chunk, 1);  // used after this chunk
+            const int ch = chunk_of(lc);
             const int t = (ch << 5) + l;
             int4 ti = make_int4(0, 0, 0, 0);
             double tc = 0.0;
@@ -611,13 +665,14 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
             int k_next, arc_next = arc_of(l, k_next);
             if (l < total)
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s0), "l"(&g.arcs[2 * arc_next]));
+            constexpr u32 RING = 16u * BLOCK;  // byte distance between the two ring buffers
             asm volatile("cp.async.commit_group;");
             for (int j0 = 0, it = 0; j0 < total; j0 += 32, ++it) {
                 const int j = j0 + l, k = k_next, arc = arc_next;
                 if (j0 + 32 < total) {  // prefetch the next iteration's record
                     arc_next = arc_of(j + 32, k_next);
                     if (j + 32 < total)
-                        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s0 + 16u * ((it + 1) & 1)),
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s0 + RING * ((it + 1) & 1)),
                                      "l"(&g.arcs[2 * arc_next]));
                 }
                 asm volatile("cp.async.commit_group;");
@@ -629,7 +684,7 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
                 bool act = j < total;
                 int4 rec = make_int4(0, 0, 0, 0);
                 if (act) {
-                    rec = stage[it & 1];
+                    rec = stage[(it & 1) * BLOCK];
                     const double ac = row[rec.y];
                     if (ac == INFINITY) {  // decoder.py:219-220: no relaxation, no record
                         act = false;
@@ -675,16 +730,17 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
                 }
                 int4 r1 = make_int4(0, 0, 0, 0);
                 if (first) r1 = __ldg(&g.arcs[2 * arc + 1]);
-                const int ci = warp_append<BLOCK>(first, (u32)rec.x, r1, true, g, ws, front0, frng0);
+                const int ci = warp_append<BLOCK>(first, (u32)rec.x, r1, true, g, ws, front0, frng0, nfr0, cbase);
                 if (ma_on && pass == 0 && ci >= 0) c.cand_key()[ci] = want.key;
             }
             asm volatile("cp.async.wait_all;" ::: "memory");
-            ch = __shfl_sync(FULL, ch_claim, 0);
+            lc = __shfl_sync(FULL, ch_claim, 0);
         }
         }
         return ExpandCounts{a_emit, a_fin, a_cas};
     }
-    for (int ch = w; ch < nchunks; ch += NW) {
+    for (int lc = w; lc < nchunks; lc += NW) {
+        const int ch = chunk_of(lc);
         int t = (ch << 5) + l;
         int4 ti = make_int4(0, 0, 0, 0);
         double tc = 0.0;
@@ -754,7 +810,7 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
                 }
                 int4 r1 = make_int4(0, 0, 0, 0);
                 if (first) r1 = __ldg(&g.arcs[2 * (want[u].arcp1 - 1u) + 1]);
-                warp_append<BLOCK>(first, (u32)rec[u].x, r1, true, g, ws, front0, frng0);
+                warp_append<BLOCK>(first, (u32)rec[u].x, r1, true, g, ws, front0, frng0, nfr0, cbase);
             }
         }
     }
@@ -770,13 +826,14 @@ struct EpsOut {
     int status;
 };
 
-template <int BLOCK>
+template <int BLOCK, int KC>
 __noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev &ws, u32 tag_in,
                                                double beam) {
     Smem<BLOCK> &sh = SH<BLOCK>();
     const Lane c{ws};
     // beam skip as in expand: with non-negative weights every candidate of this step costs at
-    // least run_min (the emitting minimum), so run_min + beam is the step's final cutoff
+    // least the emitting minimum, and run_min is an upper bound of it (this CTA's minimum), so
+    // run_min + beam is at or above the step's final cutoff
     const u64 rm = sh.run_min;
     const bool skip_on = g.nonneg && ws.beam_skip && beam < INFINITY && rm != EMPTY_KEY;
     const u64 thr = skip_on ? cost_key(__dadd_rn(key_cost(rm), beam)) : EMPTY_KEY;
@@ -784,30 +841,37 @@ __noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev 
     int status = WB_OK;
     constexpr int NW = BLOCK / 32;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    constexpr int K = KC;
+    const int r = K > 1 ? cta_rank() : 0, cbase = r * ws.cap;
     Slot *slot = c.slot();
     const Slot empty = {EMPTY_KEY, 0xFFFFFFFFu, 0xFFFFFFFFu};
-    int which = 0;
-    int rounds = 0;
-    for (;;) {
-        int n_front = min(sh.n_front, ws.cap);  // overflowed pushes were dropped (flagged)
-        const int ovf = sh.overflow;
-        __syncthreads();
-        if (n_front == 0) break;
+    // Round k consumes the frontier pushed in round k-1 (round 0: by expand) from buffer k & 1
+    // and pushes into the other; each CTA of a cluster lane works its own frontier region and
+    // the round ends at a lane barrier, after which every CTA reads every CTA's count.
+    for (int rounds = 0;; ++rounds) {
+        const int par = rounds & 1;
+        const int n_front = min(sh.nfr[par], ws.cap);  // overflowed pushes were dropped (flagged)
+        int total = n_front, ovf = sh.overflow;
+        for (int q = 1; q < K; ++q) {
+            const int o = (r + q) & (K - 1);
+            total += *peer(&sh.nfr[par], o);
+            ovf |= *peer(&sh.overflow, o);
+        }
+        if (total == 0) break;
         // a candidate overflow leaves frontier states without a candidate index: the step
         // has failed (WB_CAP_CANDIDATES), stop before following stale indices
         if (ovf) { status = wb_cap(WB_CAP_CANDIDATES); break; }
-        if (++rounds > MAX_EPS_ROUNDS) { status = wb_cap(WB_CAP_EPS_ROUNDS); break; }
-        if (threadIdx.x == 0) {
-            sh.n_front = 0;
-            sh.tag_round = (int)(tag_cur + 1u);
-        }
+        if (rounds >= MAX_EPS_ROUNDS) { status = wb_cap(WB_CAP_EPS_ROUNDS); break; }
+        // the other buffer's count was last read before the barrier that ended the last round
+        if (threadIdx.x == 0) sh.nfr[par ^ 1] = 0;
         __syncthreads();
-        const u32 tag = (u32)sh.tag_round;
+        const u32 tag = tag_cur + 1u;
         tag_cur = tag;
-        const u32 *fin = c.front(which);
-        u32 *fout = c.front(which ^ 1);
-        const int4 *frin = c.frng(which);
-        int4 *frout = c.frng(which ^ 1);
+        const u32 *fin = c.front(par) + cbase;
+        u32 *fout = c.front(par ^ 1) + cbase;
+        const int4 *frin = c.frng(par) + cbase;
+        int4 *frout = c.frng(par ^ 1) + cbase;
+        int *nfout = &sh.nfr[par ^ 1];
         const int nchunks = (n_front + 31) >> 5;
         for (int ch = w; ch < nchunks; ch += NW) {
             int i = (ch << 5) + l;
@@ -820,15 +884,15 @@ __noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev 
                 uu = fin[i];
                 const int4 fe = frin[i];
                 Slot us = ld_slot(&slot[uu]);
-                ui = fe.x >= 0 ? (u32)fe.x : min(c.cand_of()[uu], (u32)ws.cap - 1u);
+                ui = fe.x >= 0 ? (u32)fe.x : min(c.cand_of()[uu], (u32)ws.lcap - 1u);
                 lo = fe.y;
                 deg = fe.z - fe.y;
                 ucost = key_cost(us.key);
             }
             int incl = warp_incl_scan(deg);
-            int total = __shfl_sync(FULL, incl, 31);
+            int total_d = __shfl_sync(FULL, incl, 31);
             int excl = incl - deg;
-            for (int j0 = 0; j0 < total; j0 += 32) {
+            for (int j0 = 0; j0 < total_d; j0 += 32) {
                 int j = j0 + l;
                 int k = warp_owner(excl, j);
                 int lo_k = __shfl_sync(FULL, lo, k);
@@ -836,7 +900,7 @@ __noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev 
                 double uc_k = __shfl_sync(FULL, ucost, k);
                 u32 u_k = __shfl_sync(FULL, uu, k);
                 u32 ui_k = __shfl_sync(FULL, ui, k);
-                bool act = j < total;
+                bool act = j < total_d;
                 int a = lo_k + j - ex_k;
                 int4 rec = make_int4(0, 0, 0, 0);
                 if (act) {
@@ -857,7 +921,8 @@ __noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev 
                 }
                 int4 r1 = make_int4(0, 0, 0, 0);
                 if (dec) r1 = __ldg(&g.arcs[2 * a + 1]);
-                const int nidx = warp_append<BLOCK>(first, (u32)rec.x, r1, false, g, ws, fout, frout);
+                const int nidx = warp_append<BLOCK>(first, (u32)rec.x, r1, false, g, ws, fout, frout,
+                                                    nfout, cbase);
                 // states whose cost dropped (or that are new) re-relax their epsilon arcs
                 bool push = dec && r1.x < r1.y &&
                             (!ws.eps_dedup || atomicExch(&c.qtag()[rec.x], tag) != tag);
@@ -865,7 +930,7 @@ __noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev 
                 if (mp) {
                     const int lp = __ffs(mp) - 1;
                     int fb = 0;
-                    if (l == lp) fb = atomicAdd(&sh.n_front, __popc(mp));
+                    if (l == lp) fb = atomicAdd(nfout, __popc(mp));
                     fb = __shfl_sync(FULL, fb, lp);
                     int f = fb + __popc(mp & lanemask_lt());
                     if (push) {
@@ -879,8 +944,7 @@ __noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev 
                 }
             }
         }
-        __syncthreads();
-        which ^= 1;
+        lane_sync(K);
     }
     return EpsOut{tag_cur, e_eps, status};
 }
@@ -892,71 +956,94 @@ __device__ __forceinline__ int bucket_of(double cst, double best, double scale) 
 }
 
 // Exact max-active cut: K* = the max_active-th smallest (cost, state) among kept candidates
-// (decoder.py:188-191).  Expects sh.u.hist filled; sets sh.thr_bucket / thr_key / thr_state.
-template <int BLOCK>
-__noinline__ __device__ void select_threshold(int n_cand, int max_active, double best, double cutoff,
-                                 double scale, const u64 *ckey, const WorkDev &ws) {
+// (decoder.py:188-191).  Expects sh.u.hist filled with this CTA's candidates; rank 0 of a
+// cluster lane merges the CTAs' histograms, finds the boundary bucket, collects its members
+// from every CTA and ranks them.  Sets thr_bucket / thr_key / thr_state, returned uniformly.
+struct Thr {
+    int bucket;
+    u64 key;
+    u32 state;
+};
+
+template <int BLOCK, int KC>
+__noinline__ __device__ Thr select_threshold(int n_loc, int max_active, double best, double cutoff,
+                                             double scale, const u64 *ckey, const u32 *cst,
+                                             const WorkDev &ws) {
     Smem<BLOCK> &sh = SH<BLOCK>();
-    const Lane c{ws};
     constexpr int PER = NB / BLOCK;
-    u32 loc[PER];
-    u32 s = 0;
-#pragma unroll
-    for (int q = 0; q < PER; ++q) { loc[q] = sh.u.hist[threadIdx.x * PER + q]; s += loc[q]; }
     constexpr int NW = BLOCK / 32;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    int incl = warp_incl_scan((int)s);
-    if (l == 31) sh.wa[w] = incl;
-    __syncthreads();
-    if (w == 0) {
-        int v = l < NW ? sh.wa[l] : 0;
-        int iv = warp_incl_scan(v);
-        if (l < NW) sh.wa[l] = iv - v;
-    }
-    __syncthreads();
-    u32 run = sh.wa[w] + incl - s;
+    constexpr int K = KC;
+    const int r = K > 1 ? cta_rank() : 0;
+    Smem<BLOCK> &s0 = K > 1 ? *peer(&sh, 0) : sh;   // rank 0's header (itself when K == 1)
+    if (K > 1) lane_sync(K);                         // every CTA's histogram is complete
+    if (r == 0) {
+        u32 loc[PER];
+        u32 s = 0;
 #pragma unroll
-    for (int q = 0; q < PER; ++q) {
-        if (run < (u32)max_active && run + loc[q] >= (u32)max_active) {
-            sh.thr_bucket = threadIdx.x * PER + q;
-            sh.thr_below = (int)run;
-            sh.ng = (int)loc[q];
+        for (int q = 0; q < PER; ++q) {
+            const int b = threadIdx.x * PER + q;
+            u32 v = sh.u.hist[b];
+            for (int o = 1; o < K; ++o) v += peer(&sh, o)->u.hist[b];
+            loc[q] = v;
+            s += v;
         }
-        run += loc[q];
+        int incl = warp_incl_scan((int)s);
+        if (l == 31) sh.wa[w] = incl;
+        __syncthreads();
+        if (w == 0) {
+            int v = l < NW ? sh.wa[l] : 0;
+            int iv = warp_incl_scan(v);
+            if (l < NW) sh.wa[l] = iv - v;
+        }
+        __syncthreads();
+        u32 run = sh.wa[w] + incl - s;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            if (run < (u32)max_active && run + loc[q] >= (u32)max_active) {
+                sh.thr_bucket = threadIdx.x * PER + q;
+                sh.thr_below = (int)run;
+                sh.ng = (int)loc[q];
+            }
+            run += loc[q];
+        }
+        if (threadIdx.x == 0) sh.x_gn = 0;   // boundary members collected below
     }
-    __syncthreads();
-    const int bstar = sh.thr_bucket;
-    int r = max_active - sh.thr_below;  // 1-based rank inside the boundary bucket
-    const int cnt = sh.ng;
-    __syncthreads();
+    lane_sync(K);
+    const int bstar = s0.thr_bucket;
+    int rk = max_active - s0.thr_below;  // 1-based rank inside the boundary bucket
+    const int cnt = s0.ng;
     if (cnt <= GCAP && !ws.force_radix) {
-        if (threadIdx.x == 0) sh.ng = 0;
-        __syncthreads();
-        for (int i = threadIdx.x; i < n_cand; i += BLOCK) {
-            u64 k = ckey[i];
-            double cst = key_cost(k);
-            if (cst <= cutoff && bucket_of(cst, best, scale) == bstar) {
-                int j = atomicAdd(&sh.ng, 1);
-                sh.u.g.key[j] = k;
-                sh.u.g.st[j] = c.cand_state()[i];
+        for (int j = threadIdx.x; j < n_loc; j += BLOCK) {
+            const u64 k = ckey[j];
+            const double cs = key_cost(k);
+            if (cs <= cutoff && bucket_of(cs, best, scale) == bstar) {
+                const int q = atomicAdd(&s0.x_gn, 1);
+                s0.u.g.key[q] = k;
+                s0.u.g.st[q] = cst[j];
             }
         }
-        __syncthreads();
-        const int m = sh.ng;
-        for (int j = threadIdx.x; j < m; j += BLOCK) {
-            u64 kj = sh.u.g.key[j];
-            u32 sj = sh.u.g.st[j];
-            int rank = 0;
-            for (int q = 0; q < m; ++q) {
-                u64 kq = sh.u.g.key[q];
-                rank += (kq < kj || (kq == kj && sh.u.g.st[q] < sj)) ? 1 : 0;
+        lane_sync(K);
+        if (r == 0) {
+            const int m = sh.x_gn;
+            for (int j = threadIdx.x; j < m; j += BLOCK) {
+                const u64 kj = sh.u.g.key[j];
+                const u32 sj = sh.u.g.st[j];
+                int rank = 0;
+                for (int q = 0; q < m; ++q) {
+                    const u64 kq = sh.u.g.key[q];
+                    rank += (kq < kj || (kq == kj && sh.u.g.st[q] < sj)) ? 1 : 0;
+                }
+                if (rank == rk - 1) { sh.thr_key = kj; sh.thr_state = sj; }
             }
-            if (rank == r - 1) { sh.thr_key = kj; sh.thr_state = sj; }
         }
-        __syncthreads();
-        return;
+        lane_sync(K);
+        Thr t{bstar, s0.thr_key, s0.thr_state};
+        lane_sync(K);   // rank 0's header is reused by the caller
+        return t;
     }
-    // radix select over the 96-bit (key, state) of the boundary-bucket members, MSB first
+    // radix select over the 96-bit (key, state) of the boundary-bucket members, MSB first;
+    // per digit every CTA counts its members, rank 0 sums the counts and picks the digit
     if (threadIdx.x == 0) sh.pflags |= WB_PATH_RADIX;
     u64 kpre = 0, kmask = 0;
     u32 spre = 0, smask = 0;
@@ -965,72 +1052,79 @@ __noinline__ __device__ void select_threshold(int n_cand, int max_active, double
         __syncthreads();
         const bool in_key = dig < 8;
         const int shift = in_key ? (56 - 8 * dig) : (24 - 8 * (dig - 8));
-        for (int i = threadIdx.x; i < n_cand; i += BLOCK) {
-            u64 k = ckey[i];
-            double cst = key_cost(k);
-            if (!(cst <= cutoff) || bucket_of(cst, best, scale) != bstar) continue;
-            u32 st = c.cand_state()[i];
+        for (int j = threadIdx.x; j < n_loc; j += BLOCK) {
+            const u64 k = ckey[j];
+            const double cs = key_cost(k);
+            if (!(cs <= cutoff) || bucket_of(cs, best, scale) != bstar) continue;
+            const u32 st = cst[j];
             if ((k & kmask) != kpre || (st & smask) != spre) continue;
-            u32 d = in_key ? (u32)((k >> shift) & 0xFF) : ((st >> shift) & 0xFF);
+            const u32 d = in_key ? (u32)((k >> shift) & 0xFF) : ((st >> shift) & 0xFF);
             atomicAdd(&sh.u.hist[d], 1u);
         }
-        __syncthreads();
-        if (threadIdx.x == 0) {
+        lane_sync(K);
+        if (r == 0 && threadIdx.x == 0) {
             u32 acc = 0;
             int d = 0;
             for (; d < 256; ++d) {
-                if (acc + sh.u.hist[d] >= (u32)r) break;
-                acc += sh.u.hist[d];
+                u32 h = sh.u.hist[d];
+                for (int o = 1; o < K; ++o) h += peer(&sh, o)->u.hist[d];
+                if (acc + h >= (u32)rk) break;
+                acc += h;
             }
             sh.thr_below = (int)acc;
             sh.ng = d;
         }
-        __syncthreads();
-        r -= sh.thr_below;
-        u32 d = (u32)sh.ng;
+        lane_sync(K);
+        rk -= s0.thr_below;
+        const u32 d = (u32)s0.ng;
         if (in_key) { kpre |= (u64)d << shift; kmask |= 0xFFull << shift; }
         else { spre |= d << shift; smask |= 0xFFu << shift; }
-        __syncthreads();
+        lane_sync(K);   // rank 0 rewrites thr_below / ng for the next digit
     }
-    if (threadIdx.x == 0) { sh.thr_key = kpre; sh.thr_state = spre; }
-    __syncthreads();
+    return Thr{bstar, kpre, spre};
 }
 
 // Finish a step: gather candidates, beam/max-active prune, backpointer records, next tokens.
-// Returns the number of survivors (0 = search death).
+// Returns the number of survivors (0 = search death).  In a cluster lane every CTA handles
+// its own candidates; the minimum, the counts, the histogram and the compaction bases are
+// combined through DSMEM, and epsilon-chain marks reach other CTAs' flags directly.
 struct StepOut {
-    int n_surv, n_keep, status;
+    int n_surv, n_keep, status, n_cand;
 };
 
-template <int BLOCK>
+template <int BLOCK, int KC>
 __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const WorkDev &ws,
                                             const CfgDev &cfg) {
     Smem<BLOCK> &sh = SH<BLOCK>();
     const Lane c{ws};
-    const int n_cand = min(sh.n_cand, ws.cap);
-    int status = sh.overflow ? wb_cap(WB_CAP_CANDIDATES) : WB_OK;
-    const bool in_smem = n_cand <= ws.smem_cands;
+    constexpr int K = KC;
+    const int r = K > 1 ? cta_rank() : 0, cbase = r * ws.cap;
+    const int n_loc = min(sh.n_cand, ws.cap);
+    const bool in_smem = n_loc <= ws.smem_cands;
     if (!in_smem && threadIdx.x == 0) sh.pflags |= WB_PATH_GLOBAL_CANDS;
-    u64 *ckey = in_smem ? s_key<BLOCK>() : c.cand_key();
-    u32 *ca = in_smem ? s_ca<BLOCK>(ws) : c.cand_ca();
+    // this CTA's candidates, by local index j (lane candidate index cbase + j)
+    u64 *ckey = in_smem ? s_key<BLOCK>() : c.cand_key() + cbase;
+    u32 *ca = in_smem ? s_ca<BLOCK>(ws) : c.cand_ca() + cbase;
     volatile u32 *vca = ca;
+    u32 *cst = c.cand_state() + cbase;
+    u32 *carc = c.cand_arc() + cbase, *cpay = c.cand_pay() + cbase;
 
     // P1: gather slot contents (batched loads), reset slots, min / max
     if (threadIdx.x == 0) sh.best_tok = -1;
     u64 mn = EMPTY_KEY, mx = 0;
     constexpr int G1 = Tune<BLOCK>::GATHER_P1;
-    for (int i0 = threadIdx.x; i0 < n_cand; i0 += BLOCK * G1) {
+    for (int i0 = threadIdx.x; i0 < n_loc; i0 += BLOCK * G1) {
         u32 st[G1];
         Slot v[G1];
 #pragma unroll
         for (int q = 0; q < G1; ++q) {
             int i = i0 + q * BLOCK;
-            if (i < n_cand) st[q] = c.cand_state()[i];
+            if (i < n_loc) st[q] = cst[i];
         }
 #pragma unroll
         for (int q = 0; q < G1; ++q) {
             int i = i0 + q * BLOCK;
-            if (i < n_cand) {
+            if (i < n_loc) {
                 if (ws.xchg_gather) v[q] = xchg_slot_empty(&c.slot()[st[q]], ws.xchg_gather > 1);
                 else v[q] = ld_slot(&c.slot()[st[q]]);
             }
@@ -1038,10 +1132,10 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
 #pragma unroll
         for (int q = 0; q < G1; ++q) {
             int i = i0 + q * BLOCK;
-            if (i < n_cand) {
+            if (i < n_loc) {
                 ckey[i] = v[q].key;
-                c.cand_arc()[i] = v[q].arcp1;
-                c.cand_pay()[i] = v[q].pay;
+                carc[i] = v[q].arcp1;
+                cpay[i] = v[q].pay;
                 ca[i] = 0u;
                 if (!ws.xchg_gather) st_slot_empty(&c.slot()[st[q]]);
                 mn = v[q].key < mn ? v[q].key : mn;
@@ -1050,78 +1144,111 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
         }
     }
     block_minmax<BLOCK>(mn, mx);
+    // lane-wide: min / max, candidate count, overflow, where each CTA keeps its flags
+    int n_all = n_loc, flags = (sh.overflow ? 1 : 0) | (in_smem ? 0 : 2) | (sh.x_stream ? 4 : 0);
+    u32 glob_mask = in_smem ? 0u : 1u << r;   // CTAs whose flags live in global memory
+    if (K > 1) {
+        if (threadIdx.x == 0) { sh.x_mn = mn; sh.x_mx = mx; sh.x_n = n_loc; sh.x_flags = flags; }
+        lane_sync(K);
+        for (int q = 1; q < K; ++q) {
+            const int o = (r + q) & (K - 1);
+            const Smem<BLOCK> *po = peer(&sh, o);
+            const u64 a = po->x_mn, b = po->x_mx;
+            mn = a < mn ? a : mn;
+            mx = b > mx ? b : mx;
+            n_all += po->x_n;
+            flags |= po->x_flags;
+            if (po->x_flags & 2) glob_mask |= 1u << o;
+        }
+    }
+    int status = (flags & 4) ? wb_cap(WB_CAP_STREAM) : (flags & 1) ? wb_cap(WB_CAP_CANDIDATES) : WB_OK;
     tick<BLOCK>(3);
-    if (n_cand == 0) return StepOut{0, 0, status};
+    if (n_all == 0) { lane_sync(K); return StepOut{0, 0, status, 0}; }
     const double best = key_cost(mn);
     const double cutoff = __dadd_rn(best, cfg.beam);  // cutoff = best + beam (decoder.py:186)
 
     // P2: max-active histogram (only when it can bind)
     bool need_select = false;
     double scale = 0.0;
-    if (cfg.max_active > 0 && n_cand > cfg.max_active) {
+    Thr thr{0, 0, 0};
+    if (cfg.max_active > 0 && n_all > cfg.max_active) {
         double hi = key_cost(mx);
         double top = cutoff < hi ? cutoff : hi;
         double range = __dsub_rn(top, best);
         if (range > 0.0 && range < INFINITY) scale = __ddiv_rn((double)NB, range);
         // count the beam survivors first (no atomics); the histogram only if max-active binds
         long long kept = 0;
-        for (int i = threadIdx.x; i < n_cand; i += BLOCK) kept += key_cost(ckey[i]) <= cutoff;
+        for (int i = threadIdx.x; i < n_loc; i += BLOCK) kept += key_cost(ckey[i]) <= cutoff;
         kept = block_sum<BLOCK>(kept);
+        if (K > 1) {
+            if (threadIdx.x == 0) sh.x_sum = kept;
+            lane_sync(K);
+            for (int q = 1; q < K; ++q) kept += peer(&sh, (r + q) & (K - 1))->x_sum;
+        }
         need_select = kept > cfg.max_active;
         if (need_select) {
             if (threadIdx.x == 0) sh.pflags |= WB_PATH_SELECT;
             for (int b = threadIdx.x; b < NB; b += BLOCK) sh.u.hist[b] = 0;
             __syncthreads();
-            for (int i = threadIdx.x; i < n_cand; i += BLOCK) {
-                const double cst = key_cost(ckey[i]);
-                if (cst <= cutoff) atomicAdd(&sh.u.hist[bucket_of(cst, best, scale)], 1u);
+            for (int i = threadIdx.x; i < n_loc; i += BLOCK) {
+                const double cs = key_cost(ckey[i]);
+                if (cs <= cutoff) atomicAdd(&sh.u.hist[bucket_of(cs, best, scale)], 1u);
             }
             __syncthreads();
-            select_threshold<BLOCK>(n_cand, cfg.max_active, best, cutoff, scale, ckey, ws);
+            thr = select_threshold<BLOCK, KC>(n_loc, cfg.max_active, best, cutoff, scale, ckey, cst, ws);
         }
     }
     tick<BLOCK>(4);
     if (threadIdx.x == 0) {  // cost range of the next live tokens (the early cutoff's split)
         const double top = key_cost(mx) < cutoff ? key_cost(mx) : cutoff;
         sh.tok_lo = best;
-        sh.tok_hi = need_select ? key_cost(sh.thr_key) : top;
+        sh.tok_hi = need_select ? key_cost(thr.key) : top;
     }
-    const int bstar = need_select ? sh.thr_bucket : 0;
-    const u64 tkey = need_select ? sh.thr_key : 0;
-    const u32 tst = need_select ? sh.thr_state : 0;
+    const int bstar = thr.bucket;
+    const u64 tkey = thr.key;
+    const u32 tst = thr.state;
 
-    // P3: survivor flags + epsilon-chain marks (atomicOr: flags of other candidates change)
-    for (int i = threadIdx.x; i < n_cand; i += BLOCK) {
+    // P3: survivor flags + epsilon-chain marks (atomicOr: flags of other candidates change;
+    // a chain may continue into another CTA's candidates: its flags via DSMEM or global)
+    auto flag_of = [&](u32 uix) -> u32 * {
+        if (K == 1) return ca + uix;
+        const int o = (int)(uix / (u32)ws.cap);
+        const u32 j = uix - (u32)(o * ws.cap);
+        if (o == r) return ca + j;
+        if (glob_mask & (1u << o)) return c.cand_ca() + uix;
+        return peer(s_ca<BLOCK>(ws), o) + j;
+    };
+    for (int i = threadIdx.x; i < n_loc; i += BLOCK) {
         u64 k = ckey[i];
-        double cst = key_cost(k);
-        bool surv = cst <= cutoff;
+        double cs = key_cost(k);
+        bool surv = cs <= cutoff;
         if (surv && need_select) {
-            int b = bucket_of(cst, best, scale);
-            surv = b < bstar ||
-                   (b == bstar && (k < tkey || (k == tkey && c.cand_state()[i] <= tst)));
+            int b = bucket_of(cs, best, scale);
+            surv = b < bstar || (b == bstar && (k < tkey || (k == tkey && cst[i] <= tst)));
         }
         if (!surv) continue;
         atomicOr(&ca[i], F_SURV);
         if (!g.has_eps) continue;
-        int v = i;
+        u32 v = (u32)(cbase + i);
         for (;;) {
             u32 a = c.cand_arc()[v], p = c.cand_pay()[v];
             if (a == 0u || !(p & EPS_BIT)) break;
-            int uix = (int)(p & ~EPS_BIT);
-            u32 old = atomicOr(&ca[uix], F_MARK);
+            u32 uix = p & ~EPS_BIT;
+            u32 old = atomicOr(flag_of(uix), F_MARK);
             if (old & (F_MARK | F_SURV)) break;
             v = uix;
         }
     }
-    __syncthreads();
+    lane_sync(K);
     tick<BLOCK>(5);
 
     // P4: order-preserving compaction of kept candidates (arena records) and survivors
-    // (next tokens).  Warps own contiguous segments; ballots count; one scan.
+    // (next tokens).  Warps own contiguous segments; ballots count; one scan per CTA; the
+    // CTAs of a lane take consecutive ranges in rank order.
     constexpr int NW = BLOCK / 32;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    const int seg = ((n_cand + NW - 1) / NW + 31) & ~31;
-    const int lo = min(n_cand, w * seg), hi = min(n_cand, lo + seg);
+    const int seg = ((n_loc + NW - 1) / NW + 31) & ~31;
+    const int lo = min(n_loc, w * seg), hi = min(n_loc, lo + seg);
     int ck = 0, cs = 0;
     for (int i0 = lo; i0 < hi; i0 += 32) {
         int i = i0 + l;
@@ -1135,27 +1262,35 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
         int va = l < NW ? (int)sh.wa[l] : 0, vb = l < NW ? (int)sh.wb[l] : 0;
         int ia = warp_incl_scan(va), ib = warp_incl_scan(vb);
         if (l < NW) { sh.wa[l] = ia - va; sh.wb[l] = ib - vb; }
-        if (l == 31) {
-            sh.wa[NW] = ia;
-            sh.wb[NW] = ib;
-            u64 base = sh.arena_used;
-            if (base + (u64)ia > ws.arena_cap || base + (u64)ia >= (u64)EPS_BIT) sh.overflow = 2;
-            sh.arena_base = base;
-            sh.arena_used = base + (u64)ia;
-            sh.n_pend = 0;
+        if (l == 31) { sh.wa[NW] = ia; sh.wb[NW] = ib; sh.x_ck = ia; sh.x_cs = ib; }
+    }
+    lane_sync(K);
+    int keep_before = 0, surv_before = 0, n_keep = (int)sh.wa[NW], n_surv = (int)sh.wb[NW];
+    for (int q = 1; q < K; ++q) {
+        const int o = (r + q) & (K - 1);
+        const Smem<BLOCK> *po = peer(&sh, o);
+        const int a = po->x_ck, b = po->x_cs;
+        if (o < r) { keep_before += a; surv_before += b; }
+        n_keep += a;
+        n_surv += b;
+    }
+    const u64 base = sh.arena_used + (u64)keep_before;
+    {
+        const u64 used = sh.arena_used + (u64)n_keep;
+        if (used > ws.arena_cap || used >= (u64)EPS_BIT) {
+            lane_sync(K);
+            return StepOut{0, 0, wb_cap(WB_CAP_ARENA), n_all};
         }
     }
-    __syncthreads();
-    const int n_keep = (int)sh.wa[NW], n_surv = (int)sh.wb[NW];
-    if (sh.overflow == 2) { __syncthreads(); return StepOut{0, 0, wb_cap(WB_CAP_ARENA)}; }
-    const u64 base = sh.arena_base;
+    __syncthreads();   // everyone has read arena_used
+    if (threadIdx.x == 0) { sh.arena_used += (u64)n_keep; sh.n_pend = 0; }
     int4 *tinfo = c.tok_info(nxt);
     double *tcost = c.tok_cost(nxt);
-    u32 *pend = c.front(0);
-    u32 *tokidx = c.front(1);  // survivor -> next-token slot (frontier buffers are free here)
+    u32 *pend = c.front(0) + cbase;
+    u32 *tokidx = c.front(1) + cbase;  // survivor -> next-token slot (frontier buffers are free here)
     {
-        // E1: indices from the shared-memory flags only (ballot ranks within warp segments)
-        int ra = (int)sh.wa[w], rb = (int)sh.wb[w];
+        // E1: indices from the flags only (ballot ranks within warp segments)
+        int ra = (int)sh.wa[w], rb = (int)sh.wb[w] + surv_before;
         const u32 lt = lanemask_lt();
         for (int i0 = lo; i0 < hi; i0 += 32) {
             int i = i0 + l;
@@ -1170,26 +1305,24 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
             rb += __popc(ms);
         }
     }
-    __syncthreads();
+    // epsilon winners resolve their source's record index, possibly another CTA's
+    if (g.has_eps) lane_sync(K); else __syncthreads();
     {
         // E2: records + next tokens, G candidates per thread with their loads in flight
         constexpr int G = Tune<BLOCK>::GATHER;
-        const u32 *__restrict__ cst_ = c.cand_state();
-        const int4 *__restrict__ rng_ = c.cand_rng();
-        const u32 *__restrict__ arc_ = c.cand_arc();
-        const u32 *__restrict__ pay_ = c.cand_pay();
-        for (int i0 = threadIdx.x; i0 < n_cand; i0 += BLOCK * G) {
+        const int4 *__restrict__ rng_ = c.cand_rng() + cbase;
+        for (int i0 = threadIdx.x; i0 < n_loc; i0 += BLOCK * G) {
             u32 rec[G], tj[G], a[G], p[G];
 #pragma unroll
             for (int q = 0; q < G; ++q) {
                 int i = i0 + q * BLOCK;
                 rec[q] = CA_NONE;
                 tj[q] = CA_NONE;
-                if (i < n_cand) {
+                if (i < n_loc) {
                     rec[q] = vca[i];
                     tj[q] = tokidx[i];
-                    a[q] = arc_[i];
-                    p[q] = pay_[i];
+                    a[q] = carc[i];
+                    p[q] = cpay[i];
                 }
             }
 #pragma unroll
@@ -1197,10 +1330,10 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
                 int i = i0 + q * BLOCK;
                 if (tj[q] != CA_NONE) {
                     int4 rg = rng_[i];
-                    tinfo[tj[q]] = make_int4((int)cst_[i], (int)rec[q], rg.y, rg.z);
+                    tinfo[tj[q]] = make_int4((int)cst[i], (int)rec[q], rg.y, rg.z);
                     tcost[tj[q]] = key_cost(ckey[i]);
                     if (ckey[i] == mn) sh.best_tok = (int)tj[q];  // any minimal token will do
-                    if (ws.tok_eps) ws.tok_eps[2 * c.co() + (size_t)nxt * ws.cap + tj[q]] = rg.x;
+                    if (ws.tok_eps) ws.tok_eps[2 * c.co() + (size_t)nxt * ws.lcap + tj[q]] = rg.x;
                 }
                 if (rec[q] != CA_NONE) {
                     if (a[q] != 0u && (p[q] & EPS_BIT)) {
@@ -1218,19 +1351,20 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
     const int n_pend = sh.n_pend;
     for (int q = threadIdx.x; q < n_pend; q += BLOCK) {
         int i = (int)pend[q];
-        u32 a = c.cand_arc()[i], p = c.cand_pay()[i];
-        c.arena()[vca[i]] = (u64)a | ((u64)vca[p & ~EPS_BIT] << 32);
+        u32 a = carc[i], p = cpay[i];
+        const u32 src = *(volatile u32 *)flag_of(p & ~EPS_BIT);
+        c.arena()[vca[i]] = (u64)a | ((u64)src << 32);
     }
-    __syncthreads();
+    lane_sync(K);   // next tokens / records complete in every CTA of the lane
     tick<BLOCK>(6);
-    return StepOut{n_surv, n_keep, status};
+    return StepOut{n_surv, n_keep, status, n_all};
 }
 
 // LSD pre-pass (classify_blank_frames + nonblank_frames, posteriors.py:116-125,109-110): a
 // frame is blank iff its blank probability strictly exceeds the threshold; non-blank frame
 // ids are compacted in order.
 template <int BLOCK>
-__device__ int lsd_prepass(const double *bl, int T, double thr, int *fr) {
+__device__ int lsd_prepass(const double *bl, int T, double thr, int *fr, bool write) {
     Smem<BLOCK> &sh = SH<BLOCK>();
     constexpr int NW = BLOCK / 32;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -1244,7 +1378,7 @@ __device__ int lsd_prepass(const double *bl, int T, double thr, int *fr) {
     int tot;
     int r = warp_offsets<BLOCK>(cnt, sh.wa, &tot);
     const u32 lt = lanemask_lt();
-    for (int i0 = lo; i0 < hi; i0 += 32) {
+    for (int i0 = lo; write && i0 < hi; i0 += 32) {
         int f = i0 + l;
         bool nb = f < hi && !(bl[f] > thr);
         u32 m = __ballot_sync(FULL, nb);
@@ -1315,7 +1449,7 @@ __noinline__ __device__ int record_lattice_step(int k, int nxt, int n_surv, int 
     const int arc_base = k == 0 ? 0 : lst[k - 1].y + lst[k - 1].w + lse[k - 1];
     const int prev_base = k == 0 ? 0 : lst[k - 1].x;
     const int4 *tn = c.tok_info(nxt);
-    const int *te = ws.tok_eps + 2 * c.co() + (size_t)nxt * ws.cap;
+    const int *te = ws.tok_eps + 2 * c.co() + (size_t)nxt * ws.lcap;
     int status = WB_OK;
     // step 0 keeps the start node even when the prune dropped it
     if (threadIdx.x == 0) { sh.ng = -1; sh.n_pend = 0; }
@@ -1673,28 +1807,31 @@ __device__ __noinline__ void backtrace(const GraphDev &g, const u64 *arena, long
     *n_i = ni;
 }
 
-template <int BLOCK>
+template <int BLOCK, int KC>
 __global__ void __launch_bounds__(BLOCK, Tune<BLOCK>::MINB)
 decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDev ws,
               const __grid_constant__ BatchDev b, const __grid_constant__ CfgDev cfg,
               wb_utt_result *res) {
     Smem<BLOCK> &sh = SH<BLOCK>();
     const Lane c{ws};
-    const int slot_id = blockIdx.x;
+    constexpr int K = KC;   // a lane = a cluster of K CTAs
+    const int rank = K > 1 ? cta_rank() : 0;
+    const int slot_id = (int)c.lane();
     u32 tag = ws.tag_ctr[slot_id];
     const bool row_in_smem = ws.row_in_smem != 0;
     const bool pilot_on = g.nonneg && cfg.beam < INFINITY && ws.beam_skip && ws.stage_off;
     double *srow = s_row<BLOCK>();
 
     for (;;) {
-        if (threadIdx.x == 0) sh.utt = (int)atomicAdd(ws.utt_ctr, 1u);
-        __syncthreads();
-        const int u = sh.utt;
+        if (rank == 0 && threadIdx.x == 0) sh.utt = (int)atomicAdd(ws.utt_ctr, 1u);
+        lane_sync(K);
+        const int u = K > 1 ? peer(&sh, 0)->utt : sh.utt;
         if (u >= b.n) break;
         if (threadIdx.x < 8) sh.pc[threadIdx.x] = 0;
         if (threadIdx.x == 0) {
             sh.t_mark = clock64(); sh.arena_used = 0; sh.ready_seen = 0; sh.run_min = EMPTY_KEY;
             sh.pflags = ws.stage_off ? WB_PATH_PREFETCH : 0;
+            sh.best_tok = -1;
             sh.tok_lo = 0.0; sh.tok_hi = 0.0; sh.ma_frac = 0.5f;
         }
         const int T = b.T[u];
@@ -1708,37 +1845,41 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
                 status = wb_cap(WB_CAP_FRAMES);
                 nf = 0;
             } else {
-                nf = lsd_prepass<BLOCK>(b.blank + row0, T, cfg.thr, c.frames());
+                nf = lsd_prepass<BLOCK>(b.blank + row0, T, cfg.thr, c.frames(), rank == 0);
             }
         }
 
         // ---- initial tokens: start entry + epsilon closure + prune (decoder.py:236-249)
-        if (threadIdx.x == 0) {
-            u64 k0 = cost_key(0.0);
-            __stcg(reinterpret_cast<ulonglong2 *>(&c.slot()[g.start]),
-                   make_ulonglong2(k0, (u64)0u | ((u64)ROOT_PREV << 32)));
-            c.cand_state()[0] = (u32)g.start;
-            c.cand_rng()[0] = g.start_rng;
-            if (g.has_eps) c.cand_of()[g.start] = 0u;
-            sh.n_cand = 1;
+        if (threadIdx.x == 0) {   // rank 0 holds the start entry as its candidate 0
+            sh.n_cand = 0;
             sh.overflow = 0;
-            sh.n_front = 0;
-            if (g.has_eps && g.start_rng.x < g.start_rng.y) {
-                c.front(0)[0] = (u32)g.start;
-                c.frng(0)[0] = make_int4(0, g.start_rng.x, g.start_rng.y, 0);
-                sh.n_front = 1;
+            sh.nfr[0] = sh.nfr[1] = 0;
+            sh.x_stream = 0;
+            if (rank == 0) {
+                u64 k0 = cost_key(0.0);
+                __stcg(reinterpret_cast<ulonglong2 *>(&c.slot()[g.start]),
+                       make_ulonglong2(k0, (u64)0u | ((u64)ROOT_PREV << 32)));
+                c.cand_state()[0] = (u32)g.start;
+                c.cand_rng()[0] = g.start_rng;
+                if (g.has_eps) c.cand_of()[g.start] = 0u;
+                sh.n_cand = 1;
+                if (g.has_eps && g.start_rng.x < g.start_rng.y) {
+                    c.front(0)[0] = (u32)g.start;
+                    c.frng(0)[0] = make_int4(0, g.start_rng.x, g.start_rng.y, 0);
+                    sh.nfr[0] = 1;
+                }
             }
         }
-        __syncthreads();
+        lane_sync(K);
         if (g.has_eps) {
-            EpsOut eo = epsilon_closure<BLOCK>(g, ws, tag, cfg.beam);
+            EpsOut eo = epsilon_closure<BLOCK, KC>(g, ws, tag, cfg.beam);
             tag = eo.tag;
             e_eps += eo.e_eps;
             if (eo.status) status = eo.status;
         }
-        n_cand_tot += min(sh.n_cand, ws.cap);
         int cur = 0;
-        StepOut so = finish_step<BLOCK>(cur, g, ws, cfg);
+        StepOut so = finish_step<BLOCK, KC>(cur, g, ws, cfg);
+        n_cand_tot += so.n_cand;
         if (so.status) status = so.status;
         n_rec += so.n_keep;
         long long lat_arcs = 0;
@@ -1774,18 +1915,29 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
                 }
                 __syncthreads();
                 if (sh.ready_seen < 0) {  // the host never published this row: give up
-                    status = wb_cap(WB_CAP_STREAM);
-                    break;
+                    if (K == 1) {
+                        status = wb_cap(WB_CAP_STREAM);
+                        break;
+                    }
+                    // a cluster lane finishes the step with the others; the failure is
+                    // combined with theirs in the prune (every CTA then stops together)
+                    if (threadIdx.x == 0) { sh.x_stream = 1; sh.ready_seen = 0; }
                 }
             }
             int neg = !row_in_smem;  // acoustic costs of this row all >= 0? (checked while staging)
+            if (threadIdx.x == 0) {
+                sh.n_cand = 0; sh.nfr[0] = sh.nfr[1] = 0; sh.overflow = 0; sh.n_log = 0;
+                sh.run_min = EMPTY_KEY;
+                sh.next_chunk = BLOCK / 32;
+                // the pilot needs one minimal live token; in a cluster lane only the CTA that
+                // wrote it (in the last compaction) has one
+                for (int q = 1; q < K && sh.best_tok < 0; ++q)
+                    sh.best_tok = peer(&sh, (rank + q) & (K - 1))->best_tok;
+            }
+            __syncthreads();
             // Pilot of the beam skip (expand_emitting): warp 0 evaluates the arcs of a cheapest
             // live token against the row in global memory while the other warps stage it.
             const bool pilot = row_in_smem && pilot_on && sh.best_tok >= 0 && sh.best_tok < n_live;
-            if (threadIdx.x == 0) {
-                sh.n_cand = 0; sh.n_front = 0; sh.overflow = 0; sh.n_log = 0; sh.run_min = EMPTY_KEY;
-                sh.next_chunk = BLOCK / 32;
-            }
             if (pilot && threadIdx.x < 32) {
                 __syncwarp();
                 pilot_min<BLOCK>(sh.best_tok, cur, grow, g, ws);
@@ -1804,22 +1956,22 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             tick<BLOCK>(0);
             expanded += n_live;
             n_tok += n_live;
-            ExpandCounts ec = expand_emitting<BLOCK>(n_live, cur, row, g, ws, cfg.beam, row_nonneg, pilot,
+            ExpandCounts ec = expand_emitting<BLOCK, KC>(n_live, cur, row, g, ws, cfg.beam, row_nonneg, pilot,
                                                     cfg.max_active);
             a_emit += ec.a_emit;
             a_fin += ec.a_fin;
             a_cas += ec.a_cas;
-            __syncthreads();
+            lane_sync(K);   // every CTA's relaxations have landed in the lane's slots
             tick<BLOCK>(1);
             if (g.has_eps) {
-                EpsOut eo = epsilon_closure<BLOCK>(g, ws, tag, cfg.beam);
+                EpsOut eo = epsilon_closure<BLOCK, KC>(g, ws, tag, cfg.beam);
                 tag = eo.tag;
                 e_eps += eo.e_eps;
                 if (eo.status) status = eo.status;
             }
             tick<BLOCK>(2);
-            n_cand_tot += min(sh.n_cand, ws.cap);
-            so = finish_step<BLOCK>(cur ^ 1, g, ws, cfg);
+            so = finish_step<BLOCK, KC>(cur ^ 1, g, ws, cfg);
+            n_cand_tot += so.n_cand;
             if (so.status) status = so.status;
             n_rec += so.n_keep;
             steps_run++;
@@ -1839,11 +1991,32 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
         if (status != WB_OK) {
             // a failed step may leave slots beyond the candidate capacity dirty: restore the
             // lane's whole slot array so later utterances on this lane start clean
-            __syncthreads();
+            lane_sync(K);
             Slot *sl = c.slot();
-            for (long long q = threadIdx.x; q < ws.S; q += BLOCK) st_slot_empty(&sl[q]);
+            for (long long q = threadIdx.x + (long long)rank * BLOCK; q < ws.S; q += (long long)BLOCK * K)
+                st_slot_empty(&sl[q]);
+        }
+        long long t_emit = block_sum<BLOCK>(a_emit);
+        long long t_fin = block_sum<BLOCK>(a_fin);
+        long long t_cas = block_sum<BLOCK>(a_cas);
+        long long t_eps = block_sum<BLOCK>(e_eps);
+        int pflags = sh.pflags;
+        if (K > 1) {   // rank 0 reports the lane: sum the other CTAs' counters
+            if (threadIdx.x == 0) {
+                sh.x_cnt[0] = t_emit; sh.x_cnt[1] = t_fin; sh.x_cnt[2] = t_cas; sh.x_cnt[3] = t_eps;
+            }
+            lane_sync(K);
+            if (rank == 0)
+                for (int q = 1; q < K; ++q) {
+                    const Smem<BLOCK> *po = peer(&sh, q);
+                    t_emit += po->x_cnt[0]; t_fin += po->x_cnt[1]; t_cas += po->x_cnt[2];
+                    t_eps += po->x_cnt[3];
+                    pflags |= po->pflags;
+                }
+        } else {
             __syncthreads();
         }
+        if (rank != 0) continue;   // the lane's last writes are visible to rank 0 (lane_sync)
         // ---- final transition / death fallback (decoder.py:252-273, 327-333)
         const int4 *tinfo = c.tok_info(cur);
         const double *tcost = c.tok_cost(cur);
@@ -1890,10 +2063,6 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
                 ws.o_meta[6 * (size_t)u] = -1;
             }
         }
-        long long t_emit = block_sum<BLOCK>(a_emit);
-        long long t_fin = block_sum<BLOCK>(a_fin);
-        long long t_cas = block_sum<BLOCK>(a_cas);
-        long long t_eps = block_sum<BLOCK>(e_eps);
         tick<BLOCK>(7);
         if (threadIdx.x == 0) {
             wb_utt_result r;
@@ -1917,7 +2086,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             }
             r.status = status & 0xFF;
             r.capacity_flags = capf;
-            r.path_flags = sh.pflags;
+            r.path_flags = pflags;
             r.n_tok = n_tok;
             r.a_emit = t_emit;
             r.a_fin = t_fin;
@@ -1931,7 +2100,9 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
         }
         __syncthreads();
     }
-    if (threadIdx.x == 0) ws.tag_ctr[slot_id] = tag;
+    if (rank == 0 && threadIdx.x == 0) ws.tag_ctr[slot_id] = tag;
+    // no CTA of a cluster may exit while another can still read its shared memory
+    if (K > 1) lane_sync(K);
 }
 
 }  // namespace wb

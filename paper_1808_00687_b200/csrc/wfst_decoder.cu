@@ -45,6 +45,8 @@ struct wb_graph_s {
 struct wb_decoder_s {
     wb_graph_s *g = nullptr;
     int slots = 0, cap = 0, T_cap = 0, block = 0, num_sms = 0;
+    int cluster = 0, last_cluster = 1;   // CTAs per lane requested (0 = auto) / used last
+    int kmax = 1;   // candidate-side workspace holds slots * kmax CTAs (clusters of kmax CTAs)
     u64 arena_cap = 0;
     Slot *slot = nullptr;
     u32 *cand_of = nullptr, *qtag = nullptr, *tag_ctr = nullptr;
@@ -280,7 +282,7 @@ static int alloc_lattice(wb_decoder_s *d) {
     return WB_OK;
 }
 
-template <int BLOCK>
+template <int BLOCK, int K>
 static cudaError_t launch_decode(int max_grid, int num_sms, int num_cols, cudaStream_t st,
                                  const GraphDev &gd, WorkDev wd, const BatchDev &bd,
                                  const CfgDev &cd, wb_utt_result *res, bool zero_copy) {
@@ -291,10 +293,10 @@ static cudaError_t launch_decode(int max_grid, int num_sms, int num_cols, cudaSt
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(decode_kernel<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+        e = cudaFuncSetAttribute(decode_kernel<BLOCK, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     if (e != cudaSuccess) return e;
     size_t avail = 0;
-    e = cudaOccupancyAvailableDynamicSMemPerBlock(&avail, decode_kernel<BLOCK>, 1, BLOCK);
+    e = cudaOccupancyAvailableDynamicSMemPerBlock(&avail, decode_kernel<BLOCK, K>, 1, BLOCK);
     if (e != cudaSuccess) return e;
     const size_t hdr = smem_hdr<BLOCK>();
     // Cap the carve-out at 100 KB: the rest of the SM's 256 KB stays L1 for the graph's arc
@@ -307,6 +309,10 @@ static cudaError_t launch_decode(int max_grid, int num_sms, int num_cols, cudaSt
     size_t row = num_cols <= ROW_SMEM_MAX ? sizeof(double) * (size_t)num_cols : 0;
     if (row > avail) row = 0;  // the kernel reads the row from global memory instead
     if (zero_copy && row == 0) return cudaErrorNotSupported;  // host rows must be staged
+    // K CTAs per lane (a thread-block cluster): CTA r owns candidate indices [r*cap, (r+1)*cap)
+    wd.K = K;
+    wd.kshift = K >= 8 ? 3 : K >= 4 ? 2 : K >= 2 ? 1 : 0;
+    wd.lcap = K * wd.cap;
     wd.smem_cands = (int)std::min<size_t>(avail / (sizeof(u64) + sizeof(u32)), (size_t)wd.cap);
     // WB_SMEM_CANDS caps the candidates kept in shared memory (tests force the global path)
     if (const char *sc = std::getenv("WB_SMEM_CANDS")) wd.smem_cands = std::min(wd.smem_cands, std::max(0, std::atoi(sc)));
@@ -330,14 +336,37 @@ static cudaError_t launch_decode(int max_grid, int num_sms, int num_cols, cudaSt
     size_t smem = hdr + std::max(wd.stage_off ? row_r + stage : row,
                                  (size_t)wd.smem_cands * (sizeof(u64) + sizeof(u32)));
     smem = (smem + 15) & ~(size_t)15;
-    e = cudaFuncSetAttribute(decode_kernel<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(decode_kernel<BLOCK, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
     if (e != cudaSuccess) return e;
-    int occ = 1;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decode_kernel<BLOCK>, BLOCK, smem);
+    if (K == 1) {
+        int occ = 1;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decode_kernel<BLOCK, K>, BLOCK, smem);
+        if (e != cudaSuccess) return e;
+        int grid = std::min(max_grid, num_sms * std::max(occ, 1));
+        decode_kernel<BLOCK, K><<<grid, BLOCK, smem, st>>>(gd, wd, bd, cd, res);
+        return cudaGetLastError();
+    }
+    // cluster lanes: as many K-CTA clusters as fit at once (each CTA on its own SM of a GPC)
+    cudaLaunchConfig_t lc = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)K;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.blockDim = dim3(BLOCK);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    lc.gridDim = dim3((unsigned)(max_grid * K));
+    int clusters = 0;
+    e = cudaOccupancyMaxActiveClusters(&clusters, decode_kernel<BLOCK, K>, &lc);
     if (e != cudaSuccess) return e;
-    int grid = std::min(max_grid, num_sms * std::max(occ, 1));
-    decode_kernel<BLOCK><<<grid, BLOCK, smem, st>>>(gd, wd, bd, cd, res);
+    if (clusters < 1) return cudaErrorNotSupported;
+    lc.gridDim = dim3((unsigned)(std::min(max_grid, clusters) * K));
+    e = cudaLaunchKernelEx(&lc, decode_kernel<BLOCK, K>, gd, wd, bd, cd, res);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
@@ -370,11 +399,17 @@ int wb_decoder_create(wb_graph_t g, const wb_decoder_opts *o, wb_decoder_t *out)
     d->g = g;
     d->num_sms = prop.multiProcessorCount;
     d->block = opts.block_threads;
+    d->cluster = opts.cluster_ctas;
     // one persistent lane per SM (the kernel's shared-memory candidate store fills an SM)
     d->slots = opts.max_utts_in_flight > 0 ? opts.max_utts_in_flight : d->num_sms;
     d->cap = opts.cand_capacity > 0 ? opts.cand_capacity : std::min(g->S, 1 << 18);
     d->cap = std::max(1, std::min(d->cap, g->S));
+    // cluster lanes: when the lanes leave SMs idle, a lane may be a cluster of up to 4 CTAs
+    // (8 on request), each with its own candidate / token / frontier region
+    d->kmax = std::max(1, opts.cluster_ctas);
+    while (d->kmax < 4 && d->slots * d->kmax * 2 <= d->num_sms) d->kmax *= 2;
     size_t S = (size_t)g->S, slots = (size_t)d->slots, cap = (size_t)d->cap;
+    const size_t cslots = slots * (size_t)d->kmax;   // CTAs with candidate workspace
     size_t acc = 0;
     cudaError_t e = cudaSuccess;
 #define DA(p, n) if (e == cudaSuccess) e = dalloc(&d->p, (n), acc)
@@ -382,16 +417,16 @@ int wb_decoder_create(wb_graph_t g, const wb_decoder_opts *o, wb_decoder_t *out)
     DA(cand_of, g->has_eps ? slots * S : 1);
     DA(qtag, g->has_eps ? slots * S : 1);
     DA(tag_ctr, slots);
-    DA(cand_state, slots * cap);
-    DA(cand_rng, slots * cap);
-    DA(cand_arc, slots * cap);
-    DA(cand_pay, slots * cap);
-    DA(cand_key, slots * cap);
-    DA(cand_ca, slots * cap);
-    DA(front, slots * 2 * cap);
-    DA(frng, g->has_eps ? slots * 2 * cap : 1);
-    DA(tok_info, slots * 2 * cap);
-    DA(tok_cost, slots * 2 * cap);
+    DA(cand_state, cslots * cap);
+    DA(cand_rng, cslots * cap);
+    DA(cand_arc, cslots * cap);
+    DA(cand_pay, cslots * cap);
+    DA(cand_key, cslots * cap);
+    DA(cand_ca, cslots * cap);
+    DA(front, cslots * 2 * cap);
+    DA(frng, g->has_eps ? cslots * 2 * cap : 1);
+    DA(tok_info, cslots * 2 * cap);
+    DA(tok_cost, cslots * 2 * cap);
     DA(counters, 4);
 #undef DA
     if (e == cudaSuccess) e = cudaMemset(d->slot, 0xFF, sizeof(Slot) * slots * S);
@@ -434,6 +469,12 @@ int wb_decoder_device_bytes(wb_decoder_t d, int64_t *bytes) {
                        sizeof(u64) * d->arena_cap * (size_t)d->slots + d->lat_bytes +
                        sizeof(int2) * d->o_node_n + (sizeof(uint4) + sizeof(double)) * d->o_arc_n +
                        (sizeof(u32) + sizeof(double)) * d->o_fin_n);
+    return WB_OK;
+}
+
+int wb_last_launch(wb_decoder_t d, int32_t *cluster_ctas) {
+    if (!d || !cluster_ctas) return set_err(WB_ERR_VALUE, "null argument");
+    *cluster_ctas = d->last_cluster;
     return WB_OK;
 }
 
@@ -603,16 +644,35 @@ static int decode_impl(wb_decoder_t d, int32_t n, const double *costs, const int
             (rc = grow(&d->p_ctr, d->p_ctr_n, 4)) || (rc = grow(&d->p_meta, d->p_meta_n, (size_t)n * 8)))
             return rc;
     }
-    // 1024 threads per CTA, one persistent CTA (utterance lane) per SM
+    // 1024 threads per CTA, one persistent CTA (utterance lane) per SM; with fewer utterances
+    // than SMs a lane becomes a cluster of K CTAs so the idle SMs share the search
     int block = d->block ? d->block : 1024;
     int max_grid = std::min(n, d->slots);
+    int K = d->cluster;
+    if (const char *kc = std::getenv("WB_CLUSTER")) K = std::atoi(kc);
+    if (K <= 0) {   // auto: the largest K in {1, 2, 4} with max_grid * K CTAs within the SMs
+        K = 1;
+        while (K < 4 && max_grid * K * 2 <= d->num_sms) K *= 2;
+    }
+    if (K != 1 && K != 2 && K != 4 && K != 8)
+        return set_err(WB_ERR_VALUE, "cluster_ctas must be 1, 2, 4 or 8 (0 = auto)");
+    if (cfg->lattice || block != 1024) K = 1;   // lattice recording / tuning blocks: one CTA per lane
+    // a lane of K CTAs uses K CTAs' worth of candidate / token workspace
+    max_grid = std::min(max_grid, std::max(1, d->slots * d->kmax / K));
+    d->last_cluster = K;
     CUDA_TRY(cudaEventRecord(d->ev0, st));
     cudaError_t e;
     auto launch = [&]() {
         switch (block) {
-            case 256: return launch_decode<256>(max_grid, d->num_sms, num_cols, st, gd, wd, bd, cd, dres, zc);
-            case 512: return launch_decode<512>(max_grid, d->num_sms, num_cols, st, gd, wd, bd, cd, dres, zc);
-            default: return launch_decode<1024>(max_grid, d->num_sms, num_cols, st, gd, wd, bd, cd, dres, zc);
+            case 256: return launch_decode<256, 1>(max_grid, d->num_sms, num_cols, st, gd, wd, bd, cd, dres, zc);
+            case 512: return launch_decode<512, 1>(max_grid, d->num_sms, num_cols, st, gd, wd, bd, cd, dres, zc);
+            default:
+                switch (K) {
+                    case 2: return launch_decode<1024, 2>(max_grid, d->num_sms, num_cols, st, gd, wd, bd, cd, dres, zc);
+                    case 4: return launch_decode<1024, 4>(max_grid, d->num_sms, num_cols, st, gd, wd, bd, cd, dres, zc);
+                    case 8: return launch_decode<1024, 8>(max_grid, d->num_sms, num_cols, st, gd, wd, bd, cd, dres, zc);
+                    default: return launch_decode<1024, 1>(max_grid, d->num_sms, num_cols, st, gd, wd, bd, cd, dres, zc);
+                }
         }
     };
     e = launch();

@@ -187,13 +187,13 @@ class BatchDecoder:
 
     def __init__(self, graph, device: int | None = None, *, max_utts_in_flight: int = 0,
                  cand_capacity: int = 0, arena_capacity: int = 0, max_frames: int = 0,
-                 block_threads: int = 0, hash_entries: int = 0, lattice_capacity: int = 0,
+                 block_threads: int = 0, cluster_ctas: int = 0, lattice_capacity: int = 0,
                  lattice_out_capacity: int = 0):
         self.graph = graph if isinstance(graph, DeviceGraph) else DeviceGraph(graph, device)
         self.device = self.graph.device
         self.opts = dict(max_utts_in_flight=max_utts_in_flight, cand_capacity=cand_capacity,
                          arena_capacity=arena_capacity, max_frames=max_frames,
-                         block_threads=block_threads, hash_entries=hash_entries,
+                         block_threads=block_threads, cluster_ctas=cluster_ctas,
                          lattice_capacity=lattice_capacity,
                          lattice_out_capacity=lattice_out_capacity)
         self._h = None
@@ -207,7 +207,7 @@ class BatchDecoder:
         o = self.opts
         opts = N.DecoderOpts(o["max_utts_in_flight"], o["cand_capacity"], o["arena_capacity"],
                              o["max_frames"], o["block_threads"], o["lattice_capacity"],
-                             o["hash_entries"], o["lattice_out_capacity"])
+                             o["cluster_ctas"], 0, o["lattice_out_capacity"])
         h = C.c_void_p()
         N.check(N.load().wb_decoder_create(self.graph.handle, C.byref(opts), C.byref(h)),
                 "decoder workspace")
@@ -247,6 +247,12 @@ class BatchDecoder:
         b, z = C.c_int64(), C.c_int32()
         N.check(N.load().wb_last_transfer(self._h, C.byref(b), C.byref(z)))
         return int(b.value), bool(z.value)
+
+    def last_cluster_ctas(self) -> int:
+        """CTAs per utterance lane (thread-block cluster size) of the last launch."""
+        k = C.c_int32()
+        N.check(N.load().wb_last_launch(self._h, C.byref(k)))
+        return int(k.value)
 
     def last_kernel_ms(self) -> float:
         ms = C.c_float()
