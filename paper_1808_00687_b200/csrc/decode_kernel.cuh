@@ -90,6 +90,7 @@ struct WorkDev {
     int eps_dedup;        // epsilon frontier: drop repeated pushes of a state within a round
     int ma_early;         // expand: max-active early cutoff (cheaper tokens first, see expand)
     int force_radix;      // prune: radix-select every boundary bucket (test knob, WB_FORCE_RADIX)
+    int row_prefetch;     // cost table in device memory: pull the next step's row into L2 early
     int K, kshift;        // CTAs per utterance lane (a thread-block cluster of K = 1 << kshift);
                           // CTA rank r owns candidate / frontier indices [r*cap, (r+1)*cap)
     int lcap;             // K * cap: a lane's candidate / token / frontier capacity
@@ -978,6 +979,7 @@ __noinline__ __device__ Thr select_threshold(int n_loc, int max_active, double b
     Smem<BLOCK> &s0 = K > 1 ? *peer(&sh, 0) : sh;   // rank 0's header (itself when K == 1)
     if (K > 1) lane_sync(K);                         // every CTA's histogram is complete
     if (r == 0) {
+        if (threadIdx.x == 0) sh.thr_bucket = -1;   // stays -1: max-active does not bind
         u32 loc[PER];
         u32 s = 0;
 #pragma unroll
@@ -1011,6 +1013,8 @@ __noinline__ __device__ Thr select_threshold(int n_loc, int max_active, double b
     }
     lane_sync(K);
     const int bstar = s0.thr_bucket;
+    if (bstar < 0) return Thr{-1, 0, 0};  // at most max_active candidates within the beam
+    if (r == 0 && threadIdx.x == 0) sh.pflags |= WB_PATH_SELECT;
     int rk = max_active - s0.thr_below;  // 1-based rank inside the boundary bucket
     const int cnt = s0.ng;
     if (cnt <= GCAP && !ws.force_radix) {
@@ -1038,9 +1042,9 @@ __noinline__ __device__ Thr select_threshold(int n_loc, int max_active, double b
             }
         }
         lane_sync(K);
-        Thr t{bstar, s0.thr_key, s0.thr_state};
-        lane_sync(K);   // rank 0's header is reused by the caller
-        return t;
+        // rank 0 writes thr_key / thr_state again only in the next step's select, many lane
+        // barriers after these reads
+        return Thr{bstar, s0.thr_key, s0.thr_state};
     }
     // radix select over the 96-bit (key, state) of the boundary-bucket members, MSB first;
     // per digit every CTA counts its members, rank 0 sums the counts and picks the digit
@@ -1176,27 +1180,16 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
         double top = cutoff < hi ? cutoff : hi;
         double range = __dsub_rn(top, best);
         if (range > 0.0 && range < INFINITY) scale = __ddiv_rn((double)NB, range);
-        // count the beam survivors first (no atomics); the histogram only if max-active binds
-        long long kept = 0;
-        for (int i = threadIdx.x; i < n_loc; i += BLOCK) kept += key_cost(ckey[i]) <= cutoff;
-        kept = block_sum<BLOCK>(kept);
-        if (K > 1) {
-            if (threadIdx.x == 0) sh.x_sum = kept;
-            lane_sync(K);
-            for (int q = 1; q < K; ++q) kept += peer(&sh, (r + q) & (K - 1))->x_sum;
+        // histogram of the beam survivors' costs; its total says whether max-active binds
+        for (int b = threadIdx.x; b < NB; b += BLOCK) sh.u.hist[b] = 0;
+        __syncthreads();
+        for (int i = threadIdx.x; i < n_loc; i += BLOCK) {
+            const double cs = key_cost(ckey[i]);
+            if (cs <= cutoff) atomicAdd(&sh.u.hist[bucket_of(cs, best, scale)], 1u);
         }
-        need_select = kept > cfg.max_active;
-        if (need_select) {
-            if (threadIdx.x == 0) sh.pflags |= WB_PATH_SELECT;
-            for (int b = threadIdx.x; b < NB; b += BLOCK) sh.u.hist[b] = 0;
-            __syncthreads();
-            for (int i = threadIdx.x; i < n_loc; i += BLOCK) {
-                const double cs = key_cost(ckey[i]);
-                if (cs <= cutoff) atomicAdd(&sh.u.hist[bucket_of(cs, best, scale)], 1u);
-            }
-            __syncthreads();
-            thr = select_threshold<BLOCK, KC>(n_loc, cfg.max_active, best, cutoff, scale, ckey, cst, ws);
-        }
+        __syncthreads();
+        thr = select_threshold<BLOCK, KC>(n_loc, cfg.max_active, best, cutoff, scale, ckey, cst, ws);
+        need_select = thr.bucket >= 0;
     }
     tick<BLOCK>(4);
     if (threadIdx.x == 0) {  // cost range of the next live tokens (the early cutoff's split)
@@ -1953,6 +1946,14 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
                 row = srow;
             }
             const bool row_nonneg = !__syncthreads_or(neg);
+            if (ws.row_prefetch && s + 1 < nf) {
+                // the next step's row into L2 while this step searches (its staging then hits
+                // L2 instead of DRAM): one 128-byte line per thread
+                const int fn = cfg.mode == 1 ? c.frames()[s + 1] : s + 1;
+                const double *nrow = b.costs + (size_t)(row0 + fn) * b.L1;
+                for (int q = threadIdx.x * 16; q < b.L1; q += BLOCK * 16)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + q));
+            }
             tick<BLOCK>(0);
             expanded += n_live;
             n_tok += n_live;

@@ -333,6 +333,8 @@ static cudaError_t launch_decode(int max_grid, int num_sms, int num_cols, cudaSt
     wd.ma_early = ma ? std::atoi(ma) : 0;
     const char *fr = std::getenv("WB_FORCE_RADIX");  // tests: rank every boundary bucket by radix select
     wd.force_radix = (fr && fr[0] == '1') ? 1 : 0;
+    const char *rp = std::getenv("WB_ROW_PREFETCH");
+    wd.row_prefetch = !zero_copy && !bd.ready && !bd.crow_off && !(rp && rp[0] == '0');
     size_t smem = hdr + std::max(wd.stage_off ? row_r + stage : row,
                                  (size_t)wd.smem_cands * (sizeof(u64) + sizeof(u32)));
     smem = (smem + 15) & ~(size_t)15;

@@ -98,7 +98,8 @@ def test_config2_forced_branches(cuda, c2, monkeypatch, env, flag, absent):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     posts = [synth.random_posteriors(100 + i, 250, 3000) for i in range(4)]
-    out = _decode_table(BatchDecoder(g, 0, max_utts_in_flight=4), posts, C2)
+    # one CTA per utterance: the single-CTA branches (tests/test_gpu_cluster.py covers K > 1)
+    out = _decode_table(BatchDecoder(g, 0, max_utts_in_flight=4, cluster_ctas=1), posts, C2)
     _assert_equal(out, _oracle(og, posts, C2), env)
     flags = out.results["path_flags"]
     assert (flags & flag).all(), (env, flags)
@@ -112,8 +113,9 @@ def test_config2_tight_max_active_and_beam(cuda, c2):
     for cfg in (P.DecodeConfig(beam=13.0, max_active=500, mode="fsd"),
                 P.DecodeConfig(beam=6.0, max_active=20000, mode="fsd"),
                 P.DecodeConfig(beam=INF, max_active=3000, mode="fsd")):
-        out = _decode_table(BatchDecoder(g, 0, max_utts_in_flight=4), posts, cfg)
-        _assert_equal(out, _oracle(og, posts, cfg), cfg)
+        for K in (1, 4):
+            out = _decode_table(BatchDecoder(g, 0, max_utts_in_flight=4, cluster_ctas=K), posts, cfg)
+            _assert_equal(out, _oracle(og, posts, cfg), (cfg, K))
 
 
 # --------------------------------------------------------------------------- tie-heavy
