@@ -310,6 +310,22 @@ void wb_parsed_wfst_free(wb_parsed_wfst *p);
 int wb_post1_info(const char *path, int32_t *num_frames, int32_t *num_cols, int32_t *blank_col);
 int wb_post1_read(const char *path, double *dst, int64_t dst_ld);
 
+/*
+ * Checked build (libwfstb200_checked.so, compiled with -DWB_CHECKS): the kernel verifies the
+ * search's synchronisation invariants -- the reference's ClaimLedger.verify_partitions and
+ * debug_epoch (parallel.py:41-61, 92-116) -- on the device: every live token expanded by
+ * exactly one warp per step, every state registered at most once per step (the first-touch
+ * CAS protocol), every touched slot reset at the end of its step and the whole slot array
+ * clean between utterances, workspace indices in bounds.  wb_check_report copies (and
+ * clears) the first violation per lane: code << 32 | kernel source line, 0 = none.
+ * wb_claim_log returns the live-token count of each search step of the last utterance on a
+ * lane and the group (warp) that expanded each token, step after step.
+ */
+int wb_checks_enabled(void);
+int wb_check_report(wb_decoder_t d, int32_t n_lanes, int64_t *first_violation);
+int wb_claim_log(wb_decoder_t d, int32_t lane, int32_t n_steps, int32_t *queue_len,
+                 uint16_t *groups, int64_t groups_cap, int64_t *n_logged);
+
 /* CTAs per utterance lane (thread-block cluster size) of the last decode launch. */
 int wb_last_launch(wb_decoder_t d, int32_t *cluster_ctas);
 

@@ -15,6 +15,9 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("WB_LIB") or os.path.join(_HERE, "_lib", "libwfstb200.so")
+# the same kernels compiled with -DWB_CHECKS: device-side invariant checks (claim ledger,
+# stale slots, bounds) for tests and parallel_decode(claim_ledger=..., debug_epoch=True)
+CHECKED_LIB_PATH = os.path.join(_HERE, "_lib", "libwfstb200_checked.so")
 
 WB_OK, WB_ERR_CUDA, WB_ERR_VALUE, WB_ERR_LATTICE, WB_ERR_WFST, WB_ERR_CAPACITY, WB_ERR_NOMEM = range(7)
 WB_PARSE_ERROR, WB_PARSE_SYMBOL = 7, 8
@@ -91,18 +94,31 @@ EXPORTED = ("wb_last_error", "wb_version", "wb_device_count", "wb_graph_create",
             "wb_lattice_arrays_free", "wb_lattice_best_path", "wb_last_transfer",
             "wb_lattice_canonical", "wb_lattice_pruned_totals", "wb_lattice_pruned_fetch",
             "wb_lattice_split", "wb_decode_stream", "wb_decode_finish", "wb_wfst_parse_text",
-            "wb_parsed_wfst_free", "wb_gather_rows", "wb_post1_info", "wb_post1_read", "wb_last_launch")
+            "wb_parsed_wfst_free", "wb_gather_rows", "wb_post1_info", "wb_post1_read", "wb_last_launch",
+            "wb_checks_enabled", "wb_check_report", "wb_claim_log")
 
 
-def load():
-    """Load and prototype the library (raises if it has not been built)."""
-    global _lib
-    if _lib is not None:
-        return _lib
-    if not os.path.exists(LIB_PATH):
-        raise NativeError(f"{LIB_PATH} is missing: run __graft_entry__.build() first "
+_checked_lib = None
+
+
+def load(checked: bool = False):
+    """Load and prototype the library (raises if it has not been built); ``checked`` = the
+    -DWB_CHECKS build of the same kernels."""
+    global _lib, _checked_lib
+    if checked:
+        if _checked_lib is None:
+            _checked_lib = _open(CHECKED_LIB_PATH)
+        return _checked_lib
+    if _lib is None:
+        _lib = _open(LIB_PATH)
+    return _lib
+
+
+def _open(path):
+    if not os.path.exists(path):
+        raise NativeError(f"{path} is missing: run __graft_entry__.build() first "
                           "(the decoder has no CPU fallback)")
-    L = C.CDLL(LIB_PATH)
+    L = C.CDLL(path)
     L.wb_last_error.restype = C.c_char_p
     L.wb_version.restype = C.c_int
     L.wb_device_count.argtypes = [C.POINTER(C.c_int32)]
@@ -123,6 +139,9 @@ def load():
                                  C.c_int32, C.c_void_p, C.c_int64, C.c_int32]
     L.wb_gather_rows.restype = None
     L.wb_last_launch.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
+    L.wb_check_report.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
+    L.wb_claim_log.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                               C.c_int64, C.POINTER(C.c_int64)]
     L.wb_post1_info.argtypes = [C.c_char_p] + [C.POINTER(C.c_int32)] * 3
     L.wb_post1_read.argtypes = [C.c_char_p, C.c_void_p, C.c_int64]
     L.wb_decode_finish.argtypes = [C.c_void_p] + [C.c_void_p] * 3
@@ -147,7 +166,6 @@ def load():
     L.wb_lattice_best_path.argtypes = [LP, C.POINTER(C.c_double), C.c_void_p,
                                        C.POINTER(C.c_int32), C.c_void_p, C.POINTER(C.c_int32),
                                        C.c_int32]
-    _lib = L
     return L
 
 
@@ -172,10 +190,24 @@ def last_error() -> str:
     return (load().wb_last_error() or b"").decode(errors="replace")
 
 
-def check(rc: int, what: str = "") -> None:
+CHECK_NAMES = {1: "a live token was expanded zero or several times in one step (claim ledger)",
+               2: "a state was registered as a candidate twice in one step (first-touch CAS)",
+               3: "a slot touched in a step was not reset at its end (stale epoch)",
+               4: "a slot was left non-empty between utterances (stale epoch)",
+               5: "a workspace index out of bounds"}
+
+
+class DeviceCheckError(AssertionError):
+    """A device invariant check of the checked build failed (the analogue of the reference's
+    ClaimLedger.verify_partitions / debug_epoch AssertionError, parallel.py:52-61, 113-116)."""
+
+
+def check(rc: int, what: str = "", lib=None) -> None:
     if rc == WB_OK:
         return
-    msg = (load().wb_last_error() or b"").decode(errors="replace")
+    libs = [lib] if lib is not None else [x for x in (_lib, _checked_lib) if x is not None]
+    msg = next((m for m in ((x.wb_last_error() or b"").decode(errors="replace") for x in libs)
+                if m), "")
     text = f"{what}: {msg}" if what else msg
     if rc == WB_ERR_VALUE:
         raise ValueError(text)
@@ -199,21 +231,20 @@ _PENDING: list = []
 _PENDING_LOCK = threading.Lock()
 
 
-def defer_destroy(kind: str, handle) -> None:
+def defer_destroy(kind: str, handle, lib=None) -> None:
     with _PENDING_LOCK:
-        _PENDING.append((kind, handle))
+        _PENDING.append((kind, handle, lib))
 
 
 def flush_destroy() -> None:
     with _PENDING_LOCK:
         items = list(_PENDING)
         _PENDING.clear()
-    if not items or _lib is None:
-        return
     for kind in ("wb_decoder_destroy", "wb_graph_destroy"):
-        for k, h in items:
-            if k == kind:
-                getattr(_lib, k)(h)
+        for k, h, lib in items:
+            L = lib or _lib
+            if k == kind and L is not None:
+                getattr(L, k)(h)
 
 
 atexit.register(flush_destroy)

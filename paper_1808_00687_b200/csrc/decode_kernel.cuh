@@ -91,6 +91,15 @@ struct WorkDev {
     int ma_early;         // expand: max-active early cutoff (cheaper tokens first, see expand)
     int force_radix;      // prune: radix-select every boundary bucket (test knob, WB_FORCE_RADIX)
     int row_prefetch;     // cost table in device memory: pull the next step's row into L2 early
+    // ---- checked build (-DWB_CHECKS, libwfstb200_checked.so): device invariants in place of
+    // the reference's ClaimLedger / debug_epoch (parallel.py:41-61, 92-116)
+    u32 *chk_claim;       // [CTA slots][cap] expansions of each live token this step (must be 1)
+    u32 *chk_seen;        // [slots][S] registrations of each state this step (must be <= 1)
+    unsigned long long *chk_err;  // [slots] first violation: code << 32 | source line
+    unsigned short *chk_log;      // [slots][chk_log_cap] group (warp) that expanded each token
+    long long chk_log_cap;
+    int *chk_steps;       // [slots][T_cap + 1] live tokens of each search step (claim ledger)
+    int chk_inject;       // test knob: leave one slot un-reset (the stale-slot check must fire)
     int K, kshift;        // CTAs per utterance lane (a thread-block cluster of K = 1 << kshift);
                           // CTA rank r owns candidate / frontier indices [r*cap, (r+1)*cap)
     int lcap;             // K * cap: a lane's candidate / token / frontier capacity
@@ -177,6 +186,7 @@ struct Smem {
     int x_n, x_flags;   // this CTA's candidates this step; bit 0 overflow, bit 1 keys in global
     int x_gn;           // rank 0: boundary-bucket members collected from the lane's CTAs
     int x_stream;       // this CTA timed out waiting for a streamed cost row (cluster lanes)
+    long long chk_off;  // checked build: this step's offset in the lane's claim log
     int x_ck, x_cs;     // kept / surviving candidates of this CTA (compaction bases)
     u64 x_run_min;      // this CTA's exact emitting minimum (expand)
     long long x_cnt[4]; // per-CTA counters summed at the utterance end
@@ -249,6 +259,27 @@ __device__ __forceinline__ void lane_sync(int K) {
 template <class T>
 __device__ __forceinline__ T *peer(T *p, int rank) {
     return cooperative_groups::this_cluster().map_shared_rank(p, (unsigned)rank);
+}
+
+// ------------------------------------------------------------------ checked build
+// WB_CHECK(cond, code) records the first violated invariant of a lane; the host turns it into
+// an AssertionError (like the reference's ClaimLedger.verify_partitions / debug_epoch).
+enum : int {
+    CHK_CLAIM = 1,       // a live token was expanded zero or several times in a step
+    CHK_DUP = 2,         // a state was registered as a candidate twice in a step
+    CHK_STALE = 3,       // a touched slot was not reset at the end of its step
+    CHK_STALE_UTT = 4,   // a slot was left non-empty at the end of an utterance
+    CHK_BOUNDS = 5,      // an index outside its workspace array
+};
+#ifdef WB_CHECKS
+#define WB_CHECK(ws, cond, code) \
+    do { if (!(cond)) check_fail((ws), (code), __LINE__); } while (0)
+#else
+#define WB_CHECK(ws, cond, code) do { } while (0)
+#endif
+__device__ __noinline__ void check_fail(const WorkDev &ws, int code, int line) {
+    atomicCAS(&ws.chk_err[blockIdx.x >> ws.kshift], 0ull,
+              ((unsigned long long)code << 32) | (unsigned)line);
 }
 
 // ------------------------------------------------------------------ block primitives
@@ -368,6 +399,7 @@ __device__ __forceinline__ int warp_append(bool first, u32 d, int4 rng, bool pus
     const int idx = cbase + loc;
     bool pf = false;
     if (first) {
+        WB_CHECK(ws, loc >= ws.cap || (idx >= 0 && idx < ws.lcap), CHK_BOUNDS);
         if (loc < ws.cap) {
             c.cand_state()[idx] = d;
             c.cand_rng()[idx] = make_int4(rng.x, rng.y, rng.z, 0);
@@ -521,6 +553,19 @@ __device__ __noinline__ u64 ma_bound(int max_active, const WorkDev &ws) {
     return sh.ma_thr ? sh.ma_thr : EMPTY_KEY;
 }
 
+#ifdef WB_CHECKS
+// Claim-ledger analogue: count the expansions of live token t and log the expanding group
+// (warp) at the step's offset in the lane's claim log.
+template <int BLOCK>
+__device__ __forceinline__ void claim_token(const WorkDev &ws, int t, int group) {
+    const size_t ln = blockIdx.x >> ws.kshift;
+    WB_CHECK(ws, t >= 0 && t < ws.lcap, CHK_BOUNDS);
+    atomicAdd(&ws.chk_claim[ln * ws.lcap + t], 1u);
+    const long long at = SH<BLOCK>().chk_off + t;
+    if (at < ws.chk_log_cap) ws.chk_log[ln * ws.chk_log_cap + at] = (unsigned short)group;
+}
+#endif
+
 template <int BLOCK, int KC>
 __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const double *row,
                                                      const GraphDev &g, const WorkDev &ws,
@@ -655,6 +700,9 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
             if (t < n_live) { ti = tinfo[t]; tc = tcost[t]; }
             const bool in_pass = !ma_on || ((tc <= split) == (pass == 0));
             const int deg = (t < n_live && in_pass) ? ti.w - ti.z : 0;
+#ifdef WB_CHECKS
+            if (t < n_live && in_pass) claim_token<BLOCK>(ws, t, r * NW + w);
+#endif
             a_emit += deg;
             const int incl = warp_incl_scan(deg);
             const int total = __shfl_sync(FULL, incl, 31);
@@ -747,6 +795,9 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
         double tc = 0.0;
         if (t < n_live) { ti = tinfo[t]; tc = tcost[t]; }
         int deg = t < n_live ? ti.w - ti.z : 0;
+#ifdef WB_CHECKS
+        if (t < n_live) claim_token<BLOCK>(ws, t, r * NW + w);
+#endif
         a_emit += deg;
         int incl = warp_incl_scan(deg);
         int total = __shfl_sync(FULL, incl, 31);
@@ -1142,6 +1193,15 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
                 cpay[i] = v[q].pay;
                 ca[i] = 0u;
                 if (!ws.xchg_gather) st_slot_empty(&c.slot()[st[q]]);
+#ifdef WB_CHECKS
+                {   // one registration per state and step (the first-touch CAS protocol)
+                    const u32 old = atomicAdd(&ws.chk_seen[c.so() + st[q]], 1u);
+                    WB_CHECK(ws, old == 0u, CHK_DUP);
+                    if (ws.chk_inject && r == 0 && i == 0 && sh.chk_off > 0)   // test knob
+                        __stcg(reinterpret_cast<ulonglong2 *>(&c.slot()[st[q]]),
+                               make_ulonglong2(v[q].key, 0ull));
+                }
+#endif
                 mn = v[q].key < mn ? v[q].key : mn;
                 mx = v[q].key > mx ? v[q].key : mx;
             }
@@ -1340,6 +1400,15 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
             }
         }
     }
+#ifdef WB_CHECKS
+    // debug_epoch analogue: every slot this step touched is EMPTY again (no relaxation of
+    // this step can leak into the next); registration counters are cleared for the next step
+    for (int i = threadIdx.x; i < n_loc; i += BLOCK) {
+        const u32 st = cst[i];
+        WB_CHECK(ws, ld_slot(&c.slot()[st]).key == EMPTY_KEY, CHK_STALE);
+        ws.chk_seen[c.so() + st] = 0u;
+    }
+#endif
     __syncthreads();
     const int n_pend = sh.n_pend;
     for (int q = threadIdx.x; q < n_pend; q += BLOCK) {
@@ -1825,6 +1894,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             sh.t_mark = clock64(); sh.arena_used = 0; sh.ready_seen = 0; sh.run_min = EMPTY_KEY;
             sh.pflags = ws.stage_off ? WB_PATH_PREFETCH : 0;
             sh.best_tok = -1;
+            sh.chk_off = 0;
             sh.tok_lo = 0.0; sh.tok_hi = 0.0; sh.ma_frac = 0.5f;
         }
         const int T = b.T[u];
@@ -1963,6 +2033,19 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             a_fin += ec.a_fin;
             a_cas += ec.a_cas;
             lane_sync(K);   // every CTA's relaxations have landed in the lane's slots
+#ifdef WB_CHECKS
+            {   // every live token of the step was expanded by exactly one group
+                u32 *cl = ws.chk_claim + c.lane() * ws.lcap;
+                for (int t = threadIdx.x + rank * BLOCK; t < n_live; t += BLOCK * K) {
+                    WB_CHECK(ws, cl[t] == 1u, CHK_CLAIM);
+                    cl[t] = 0u;
+                }
+                if (rank == 0 && threadIdx.x == 0 && s <= ws.T_cap)
+                    ws.chk_steps[c.lane() * (ws.T_cap + 1) + s] = n_live;
+                __syncthreads();
+                if (threadIdx.x == 0) sh.chk_off += n_live;
+            }
+#endif
             tick<BLOCK>(1);
             if (g.has_eps) {
                 EpsOut eo = epsilon_closure<BLOCK, KC>(g, ws, tag, cfg.beam);
@@ -1989,6 +2072,14 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             cur ^= 1;
             n_live = so.n_surv;
         }
+#ifdef WB_CHECKS
+        if (status == WB_OK) {   // the whole slot array is clean between utterances
+            lane_sync(K);
+            const Slot *sl = c.slot();
+            for (long long q = threadIdx.x + (long long)rank * BLOCK; q < ws.S; q += (long long)BLOCK * K)
+                WB_CHECK(ws, ld_slot(&sl[q]).key == EMPTY_KEY, CHK_STALE_UTT);
+        }
+#endif
         if (status != WB_OK) {
             // a failed step may leave slots beyond the candidate capacity dirty: restore the
             // lane's whole slot array so later utterances on this lane start clean

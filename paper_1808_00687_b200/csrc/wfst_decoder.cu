@@ -47,6 +47,12 @@ struct wb_decoder_s {
     int slots = 0, cap = 0, T_cap = 0, block = 0, num_sms = 0;
     int cluster = 0, last_cluster = 1;   // CTAs per lane requested (0 = auto) / used last
     int kmax = 1;   // candidate-side workspace holds slots * kmax CTAs (clusters of kmax CTAs)
+    // checked build (-DWB_CHECKS): invariant counters, first violation per lane, claim log
+    u32 *chk_claim = nullptr, *chk_seen = nullptr;
+    unsigned long long *chk_err = nullptr;
+    unsigned short *chk_log = nullptr;
+    long long chk_log_cap = 0;
+    int *chk_steps = nullptr;
     u64 arena_cap = 0;
     Slot *slot = nullptr;
     u32 *cand_of = nullptr, *qtag = nullptr, *tag_ctr = nullptr;
@@ -201,6 +207,8 @@ int wb_graph_device_bytes(wb_graph_t g, int64_t *bytes) {
 }  // extern "C"
 
 static void free_decoder(wb_decoder_s *d) {
+    void *chk[] = {d->chk_claim, d->chk_seen, d->chk_err, d->chk_log, d->chk_steps};
+    for (void *p : chk) cudaFree(p);
     void *ptrs[] = {d->slot, d->cand_of, d->qtag, d->tag_ctr, d->cand_state, d->cand_rng,
                     d->cand_arc, d->cand_pay, d->cand_key, d->cand_ca, d->front, d->frng, d->tok_info,
                     d->tok_cost, d->frames, d->arena, d->counters, d->h_costs, d->h_blank,
@@ -226,6 +234,11 @@ static int alloc_frames(wb_decoder_s *d, int T_cap) {
     d->frames = nullptr;
     d->T_cap = std::max(T_cap, 1);
     CUDA_TRY(cudaMalloc(&d->frames, sizeof(int) * (size_t)d->slots * d->T_cap));
+#ifdef WB_CHECKS
+    cudaFree(d->chk_steps);
+    d->chk_steps = nullptr;
+    CUDA_TRY(cudaMalloc(&d->chk_steps, sizeof(int) * (size_t)d->slots * (d->T_cap + 1)));
+#endif
     return WB_OK;
 }
 
@@ -333,6 +346,8 @@ static cudaError_t launch_decode(int max_grid, int num_sms, int num_cols, cudaSt
     wd.ma_early = ma ? std::atoi(ma) : 0;
     const char *fr = std::getenv("WB_FORCE_RADIX");  // tests: rank every boundary bucket by radix select
     wd.force_radix = (fr && fr[0] == '1') ? 1 : 0;
+    const char *ci = std::getenv("WB_CHECK_INJECT");
+    wd.chk_inject = ci && ci[0] == '1';
     const char *rp = std::getenv("WB_ROW_PREFETCH");
     wd.row_prefetch = !zero_copy && !bd.ready && !bd.crow_off && !(rp && rp[0] == '0');
     size_t smem = hdr + std::max(wd.stage_off ? row_r + stage : row,
@@ -430,11 +445,24 @@ int wb_decoder_create(wb_graph_t g, const wb_decoder_opts *o, wb_decoder_t *out)
     DA(tok_info, cslots * 2 * cap);
     DA(tok_cost, cslots * 2 * cap);
     DA(counters, 4);
+#ifdef WB_CHECKS
+    d->chk_log_cap = 1ll << 20;   // claim-log entries (tokens expanded) per lane
+    if (const char *lc = std::getenv("WB_CHECK_LOG")) d->chk_log_cap = std::atoll(lc);
+    DA(chk_claim, cslots * cap);
+    DA(chk_seen, slots * S);
+    DA(chk_err, slots);
+    DA(chk_log, slots * (size_t)d->chk_log_cap);
+#endif
 #undef DA
     if (e == cudaSuccess) e = cudaMemset(d->slot, 0xFF, sizeof(Slot) * slots * S);
     if (e == cudaSuccess && g->has_eps) e = cudaMemset(d->qtag, 0, sizeof(u32) * slots * S);
     if (e == cudaSuccess && g->has_eps) e = cudaMemset(d->cand_of, 0, sizeof(u32) * slots * S);
     if (e == cudaSuccess) e = cudaMemset(d->tag_ctr, 0, sizeof(u32) * slots);
+#ifdef WB_CHECKS
+    if (e == cudaSuccess) e = cudaMemset(d->chk_claim, 0, sizeof(u32) * cslots * cap);
+    if (e == cudaSuccess) e = cudaMemset(d->chk_seen, 0, sizeof(u32) * slots * S);
+    if (e == cudaSuccess) e = cudaMemset(d->chk_err, 0, sizeof(unsigned long long) * slots);
+#endif
     if (e == cudaSuccess) e = cudaEventCreate(&d->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&d->ev1);
     if (e != cudaSuccess) {
@@ -471,6 +499,47 @@ int wb_decoder_device_bytes(wb_decoder_t d, int64_t *bytes) {
                        sizeof(u64) * d->arena_cap * (size_t)d->slots + d->lat_bytes +
                        sizeof(int2) * d->o_node_n + (sizeof(uint4) + sizeof(double)) * d->o_arc_n +
                        (sizeof(u32) + sizeof(double)) * d->o_fin_n);
+    return WB_OK;
+}
+
+int wb_checks_enabled(void) {
+#ifdef WB_CHECKS
+    return 1;
+#else
+    return 0;
+#endif
+}
+
+int wb_check_report(wb_decoder_t d, int32_t n_lanes, int64_t *first_violation) {
+    if (!d || !first_violation || n_lanes < 0) return set_err(WB_ERR_VALUE, "bad argument");
+    const int n = std::min(n_lanes, d->slots);
+    for (int i = 0; i < n_lanes; ++i) first_violation[i] = 0;
+    if (!d->chk_err || n == 0) return WB_OK;
+    CUDA_TRY(cudaSetDevice(d->g->device));
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpy(first_violation, d->chk_err, sizeof(int64_t) * n, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemset(d->chk_err, 0, sizeof(unsigned long long) * d->slots));
+    return WB_OK;
+}
+
+int wb_claim_log(wb_decoder_t d, int32_t lane, int32_t n_steps, int32_t *queue_len,
+                 uint16_t *groups, int64_t groups_cap, int64_t *n_logged) {
+    if (!d || !queue_len || !groups || !n_logged) return set_err(WB_ERR_VALUE, "null argument");
+    *n_logged = 0;
+    if (!d->chk_log) return set_err(WB_ERR_VALUE, "claim logs need the checked library");
+    if (lane < 0 || lane >= d->slots || n_steps < 0 || n_steps > d->T_cap + 1)
+        return set_err(WB_ERR_VALUE, "lane / step count out of range");
+    CUDA_TRY(cudaSetDevice(d->g->device));
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpy(queue_len, d->chk_steps + (size_t)lane * (d->T_cap + 1),
+                        sizeof(int) * n_steps, cudaMemcpyDeviceToHost));
+    long long tot = 0;
+    for (int s = 0; s < n_steps; ++s) tot += queue_len[s];
+    const long long n = std::min<long long>(std::min<long long>(tot, d->chk_log_cap), groups_cap);
+    if (n > 0)
+        CUDA_TRY(cudaMemcpy(groups, d->chk_log + (size_t)lane * d->chk_log_cap,
+                            sizeof(uint16_t) * n, cudaMemcpyDeviceToHost));
+    *n_logged = n;
     return WB_OK;
 }
 
@@ -587,6 +656,8 @@ static int decode_impl(wb_decoder_t d, int32_t n, const double *costs, const int
     wd.front = d->front; wd.frng = d->frng; wd.tok_info = d->tok_info; wd.tok_cost = d->tok_cost;
     wd.frames = d->frames;
     wd.arena = d->arena; wd.arena_cap = d->arena_cap;
+    wd.chk_claim = d->chk_claim; wd.chk_seen = d->chk_seen; wd.chk_err = d->chk_err;
+    wd.chk_log = d->chk_log; wd.chk_log_cap = d->chk_log_cap; wd.chk_steps = d->chk_steps;
     wd.utt_ctr = reinterpret_cast<u32 *>(d->counters + 1);
     wd.S = g->S; wd.cap = d->cap; wd.T_cap = d->T_cap;
     if (cfg->lattice) {

@@ -117,18 +117,20 @@ class DeviceGraph:
     """A transducer resident in HBM (``wb_graph_create``): packed 16-byte arc records
     {dst, ilabel, weight}, per-state {eps_lo, emit_lo, emit_hi} ranges, olabels, finals."""
 
-    def __init__(self, wfst, device: int | None = None):
+    def __init__(self, wfst, device: int | None = None, checked: bool = False):
         self.wfst = as_wfst(wfst)
         self.device = _current_device() if device is None else int(device)
+        self.checked = bool(checked)
+        self._L = N.load(self.checked)   # the library (product or checked build) of this handle
         w = self.wfst
         self._arrays = [np.ascontiguousarray(a) for a in (w.row_ptr, w.eps_end, w.dst, w.ilabel,
                                                           w.olabel, w.weight, w.final_w)]
         a = self._arrays
         desc = N.GraphDesc(w.num_states, w.num_arcs, w.start, 0, *(x.ctypes.data for x in a))
         h = C.c_void_p()
-        N.check(N.load().wb_graph_create(C.byref(desc), self.device, C.byref(h)), "graph upload")
+        N.check(self._L.wb_graph_create(C.byref(desc), self.device, C.byref(h)), "graph upload")
         self._h = h
-        self._fin = weakref.finalize(self, N.defer_destroy, "wb_graph_destroy", h)
+        self._fin = weakref.finalize(self, N.defer_destroy, "wb_graph_destroy", h, self._L)
 
     @property
     def handle(self):
@@ -136,7 +138,7 @@ class DeviceGraph:
 
     def device_bytes(self) -> int:
         b = C.c_int64()
-        N.check(N.load().wb_graph_device_bytes(self._h, C.byref(b)))
+        N.check(self._L.wb_graph_device_bytes(self._h, C.byref(b)))
         return int(b.value)
 
 
@@ -188,8 +190,15 @@ class BatchDecoder:
     def __init__(self, graph, device: int | None = None, *, max_utts_in_flight: int = 0,
                  cand_capacity: int = 0, arena_capacity: int = 0, max_frames: int = 0,
                  block_threads: int = 0, cluster_ctas: int = 0, lattice_capacity: int = 0,
-                 lattice_out_capacity: int = 0):
-        self.graph = graph if isinstance(graph, DeviceGraph) else DeviceGraph(graph, device)
+                 lattice_out_capacity: int = 0, checks: bool = False):
+        if isinstance(graph, DeviceGraph):
+            if graph.checked != bool(checks):
+                raise ValueError("the DeviceGraph was uploaded by the other library build")
+            self.graph = graph
+        else:
+            self.graph = DeviceGraph(graph, device, checked=checks)
+        self.checks = bool(checks)   # the -DWB_CHECKS build: device invariants verified
+        self._L = self.graph._L
         self.device = self.graph.device
         self.opts = dict(max_utts_in_flight=max_utts_in_flight, cand_capacity=cand_capacity,
                          arena_capacity=arena_capacity, max_frames=max_frames,
@@ -209,10 +218,10 @@ class BatchDecoder:
                              o["max_frames"], o["block_threads"], o["lattice_capacity"],
                              o["cluster_ctas"], 0, o["lattice_out_capacity"])
         h = C.c_void_p()
-        N.check(N.load().wb_decoder_create(self.graph.handle, C.byref(opts), C.byref(h)),
+        N.check(self._L.wb_decoder_create(self.graph.handle, C.byref(opts), C.byref(h)),
                 "decoder workspace")
         self._h = h
-        self._fin = weakref.finalize(self, N.defer_destroy, "wb_decoder_destroy", h)
+        self._fin = weakref.finalize(self, N.defer_destroy, "wb_decoder_destroy", h, self._L)
 
     def _grow(self, flags: int, lattice_out_need: int = 0, max_frames: int = 0):
         """Recreate the workspace with the capacities named by ``flags`` (WB_CAP_* bits of
@@ -239,24 +248,52 @@ class BatchDecoder:
 
     def device_bytes(self) -> int:
         b = C.c_int64()
-        N.check(N.load().wb_decoder_device_bytes(self._h, C.byref(b)))
+        N.check(self._L.wb_decoder_device_bytes(self._h, C.byref(b)))
         return int(b.value)
 
     def last_transfer(self) -> tuple[int, bool]:
         """(host->device bytes, zero-copy?) of the last host-buffer decode."""
         b, z = C.c_int64(), C.c_int32()
-        N.check(N.load().wb_last_transfer(self._h, C.byref(b), C.byref(z)))
+        N.check(self._L.wb_last_transfer(self._h, C.byref(b), C.byref(z)))
         return int(b.value), bool(z.value)
+
+    def check_report(self, n_lanes: int | None = None) -> None:
+        """Checked build: raise ``DeviceCheckError`` if a device invariant failed during the
+        last decode(s) on any lane (and clear the reports)."""
+        if not self.checks:
+            return
+        n = int(n_lanes or self.opts["max_utts_in_flight"] or 148)
+        rep = np.zeros(max(n, 1), np.int64)
+        N.check(self._L.wb_check_report(self._h, n, rep.ctypes.data), "check report", self._L)
+        bad = np.flatnonzero(rep)
+        if len(bad):
+            lines = [f"lane {int(i)}: {N.CHECK_NAMES.get(int(rep[i]) >> 32, 'check')} "
+                     f"(decode_kernel.cuh:{int(rep[i]) & 0xFFFFFFFF})" for i in bad[:8]]
+            raise N.DeviceCheckError("device invariant violated: " + "; ".join(lines))
+
+    def claim_log(self, n_steps: int, lane: int = 0):
+        """Checked build: per search step of the last utterance on ``lane``, the live-token
+        count and the group (warp) that expanded each token."""
+        q = np.zeros(max(n_steps, 1), np.int32)
+        cap = 1 << 26
+        groups = np.zeros(cap, np.uint16)
+        got = C.c_int64()
+        N.check(self._L.wb_claim_log(self._h, lane, n_steps, q.ctypes.data, groups.ctypes.data,
+                                     cap, C.byref(got)), "claim log", self._L)
+        q = q[:n_steps]
+        if got.value < int(q.sum()):
+            raise ValueError("the claim log overflowed (raise WB_CHECK_LOG)")
+        return q, groups[:got.value]
 
     def last_cluster_ctas(self) -> int:
         """CTAs per utterance lane (thread-block cluster size) of the last launch."""
         k = C.c_int32()
-        N.check(N.load().wb_last_launch(self._h, C.byref(k)))
+        N.check(self._L.wb_last_launch(self._h, C.byref(k)))
         return int(k.value)
 
     def last_kernel_ms(self) -> float:
         ms = C.c_float()
-        N.check(N.load().wb_last_kernel_ms(self._h, C.byref(ms)))
+        N.check(self._L.wb_last_kernel_ms(self._h, C.byref(ms)))
         return float(ms.value)
 
     def reserve(self, n_frames_total: int, max_active: int | None, max_frames: int,
@@ -307,13 +344,14 @@ class BatchDecoder:
             res = np.zeros(n, dtype=N.UTT_RESULT_DTYPE)
             ol = np.zeros((n, cap), dtype=np.int32)
             il = np.zeros((n, cap), dtype=np.int32)
-            rc = N.load().wb_decode(self._h, n, costs.ctypes.data, row_offset.ctypes.data,
+            rc = self._L.wb_decode(self._h, n, costs.ctypes.data, row_offset.ctypes.data,
                                     num_frames.ctypes.data, L1, blank.ctypes.data,
                                     C.byref(ncfg), res.ctypes.data, ol.ctypes.data,
                                     il.ctypes.data, cap, N.WB_MEM_HOST, None)
             N.check(rc, "decode")
             bad = res["status"] != N.WB_OK
             if not bad.any():
+                self.check_report(n)
                 return BatchOutput(res, ol, il, cap)
             flags = int(np.bitwise_or.reduce(res["capacity_flags"][bad]))
             if flags & N.WB_CAP_LABELS:           # labels did not fit: rerun with exact room
@@ -322,7 +360,7 @@ class BatchDecoder:
                 need = 0
                 if flags & N.WB_CAP_LATTICE_OUT:  # exact output-pool need from the counters
                     nu, nn, na, nf = C.c_int32(), C.c_int64(), C.c_int64(), C.c_int64()
-                    N.check(N.load().wb_lattice_totals(self._h, C.byref(nu), C.byref(nn),
+                    N.check(self._L.wb_lattice_totals(self._h, C.byref(nu), C.byref(nn),
                                                        C.byref(na), C.byref(nf)), "lattice")
                     need = max(nn.value, na.value, nf.value)
                 self._grow(flags, lattice_out_need=need, max_frames=maxT)
@@ -401,7 +439,7 @@ class BatchDecoder:
         ncfg = _native_config(cfg, mode, lattice, lattice_beam)
         self._last_max_active = cfg.max_active
         N.flush_destroy()
-        L = N.load()
+        L = self._L
         # producers: row blocks in block-major order; each utterance's ready count advances
         # over its contiguous finished prefix.  They start BEFORE the launch: when launches are
         # serialised (CUDA_LAUNCH_BLOCKING=1, ncu, compute-sanitizer) wb_decode_stream returns
@@ -475,13 +513,14 @@ class BatchDecoder:
                 self._grow(flags, lattice_out_need=need_out, max_frames=maxT)
             return self.decode_posteriors(posts_list, cfg, mode, cap, lattice, lattice_beam,
                                           block_frames, workers, _attempt + 1)
+        self.check_report(n)
         return BatchOutput(res, ol, il, cap)
 
     @_locked
     def fetch_lattices(self, wfst: Wfst) -> list:
         """Trimmed lattices of the last lattice-mode decode, canonically ordered."""
         from .lattice import canonical_batch
-        L = N.load()
+        L = self._L
         n = C.c_int32()
         nn, na, nf = C.c_int64(), C.c_int64(), C.c_int64()
         N.check(L.wb_lattice_totals(self._h, C.byref(n), C.byref(nn), C.byref(na), C.byref(nf)),
@@ -510,7 +549,7 @@ class BatchDecoder:
         import os
         from concurrent.futures import ThreadPoolExecutor
         from .lattice import LatticeError, canonical_batch, split_lattice, EMPTY_LATTICE, COST_EPS
-        L = N.load()
+        L = self._L
         n = C.c_int32()
         nn, na, nf = C.c_int64(), C.c_int64(), C.c_int64()
         N.check(L.wb_lattice_pruned_totals(self._h, C.byref(n), C.byref(nn), C.byref(na),
@@ -567,7 +606,7 @@ class BatchDecoder:
         if stream is None:
             import torch
             stream = torch.cuda.current_stream(self.device).cuda_stream
-        rc = N.load().wb_decode(self._h, n, costs.data_ptr(), row_offset.data_ptr(),
+        rc = self._L.wb_decode(self._h, n, costs.data_ptr(), row_offset.data_ptr(),
                                 num_frames.data_ptr(), int(costs.shape[-1]), blank.data_ptr(),
                                 C.byref(ncfg), results.data_ptr(), olabels.data_ptr(),
                                 ilabels.data_ptr(), int(label_capacity), N.WB_MEM_DEVICE,
@@ -592,14 +631,14 @@ _DECODER_LOCK = threading.Lock()
 _RECORDER_PROTOCOL = ("begin_step", "emitting", "epsilon", "survivors", "finish")
 
 
-def _decoder_for(w: Wfst) -> BatchDecoder:
+def _decoder_for(w: Wfst, checked: bool = False) -> BatchDecoder:
     dev = _current_device()
     with _DECODER_LOCK:
         cache = w.__dict__.setdefault("_b200_decoders", {})
-        dec = cache.get(dev)
+        dec = cache.get((dev, checked))
         if dec is None:
-            dec = BatchDecoder(w, dev)
-            cache[dev] = dec
+            dec = BatchDecoder(w, dev, checks=checked)
+            cache[(dev, checked)] = dec
     return dec
 
 
@@ -674,7 +713,35 @@ def parallel_decode(wfst, posts, cfg: DecodeConfig, workers: int = 1, group_size
         raise ValueError(f"workers must be >= 1, got {workers}")
     if group_size < 1:
         raise ValueError(f"group_size must be >= 1, got {group_size}")
-    return decode(wfst, posts, cfg, recorder=recorder)
+    if claim_ledger is None and not debug_epoch:
+        return decode(wfst, posts, cfg, recorder=recorder)
+    # the reference's race checks (parallel.py:41-61, 92-116) map to the checked build: the
+    # device verifies the per-step claim partition, first-touch registration and slot resets
+    # (a violation raises DeviceCheckError, an AssertionError); the claim log fills the ledger
+    w = as_wfst(wfst)
+    _check_decodable(w, posts)
+    dec = _decoder_for(w, checked=True)
+    with dec.lock:
+        out = dec.decode_posteriors([posts], cfg, cfg.mode, lattice=recorder is not None)
+        res = out.decode_result(0)
+        lat = dec.fetch_lattices(w)[0] if recorder is not None else None
+        if claim_ledger is not None:
+            queue, groups = dec.claim_log(res.search_steps)
+            at = 0
+            for qlen in queue.tolist():
+                claims = claim_ledger.begin_step(qlen)
+                for t, grp in enumerate(groups[at:at + qlen].tolist()):
+                    claims.setdefault(grp, []).append(t)
+                at += qlen
+    if recorder is not None:
+        from .lattice import LatticeRecorder, replay
+        r = out.results[0]
+        args = (int(r["final_step"]), int(r["final_state"]), bool(r["reached_final"]))
+        if isinstance(recorder, LatticeRecorder):
+            recorder._set(lat, *args)
+        else:
+            replay(lat, recorder, *args)
+    return res
 
 
 __all__ = ["BatchDecoder", "BatchOutput", "DecodeConfig", "DecodeResult", "DeviceGraph",
