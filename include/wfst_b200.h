@@ -232,6 +232,13 @@ void wb_lattice_arrays_free(wb_lattice_arrays *a);
  * e.g. from wb_lattice_pruned_fetch): splits nodes whose prefix/suffix recombination could
  * exceed the cutoff; WB_ERR_LATTICE past 500,000 keys. */
 int wb_lattice_split(const wb_lattice_arrays *lat, double cutoff, wb_lattice_arrays *out);
+/* format_lattice_text / parse_lattice_text (lattice.py:562-627), byte-identical to the
+ * reference: the text is malloc'd (release with wb_text_free); parsed arrays are released with
+ * wb_lattice_arrays_free (tie = arc position).  WB_ERR_LATTICE / WB_ERR_VALUE (a bad int or
+ * float literal) with the reference's messages; no nodes = EMPTY_LATTICE. */
+int wb_lattice_format_text(const wb_lattice_arrays *lat, char **text, int64_t *len);
+int wb_lattice_parse_text(const char *text, int64_t len, wb_lattice_arrays *out);
+void wb_text_free(char *text);
 /* lattice_best_path (lattice.py:504-559): tie-exact minimum-cost path and its labels. */
 int wb_lattice_best_path(const wb_lattice_arrays *lat, double *cost, int32_t *olabels,
                          int32_t *n_olabels, int32_t *ilabels, int32_t *n_ilabels,

@@ -21,107 +21,18 @@
 #include <vector>
 
 #include "../../include/wfst_b200.h"
+#include "pytext.h"
 
 int wb_internal_set_error(int code, const char *msg);
 
 namespace {
 
 inline bool is_ws(char c) { return c == ' ' || c == '\t' || c == '\r' || c == '\v' || c == '\f'; }
-inline bool is_digit(char c) { return c >= '0' && c <= '9'; }
-
-// Copy a digit run that may contain single underscores between digits (PEP 515) into `out`
-// without them; false if an underscore is misplaced.  Returns the end of the run in *stop.
-bool digit_run(const char *b, const char *e, std::string &out, const char **stop) {
-    const char *q = b;
-    bool last_digit = false;
-    while (q < e) {
-        if (is_digit(*q)) {
-            out.push_back(*q);
-            last_digit = true;
-        } else if (*q == '_') {
-            if (!last_digit || q + 1 >= e || !is_digit(q[1])) return false;
-            last_digit = false;
-        } else {
-            break;
-        }
-        ++q;
-    }
-    *stop = q;
-    return true;
-}
-
-// Python int(token) for a token without surrounding whitespace.
-bool py_int(const char *b, const char *e, long long *v) {
-    bool neg = false;
-    if (b < e && (*b == '+' || *b == '-')) neg = *b++ == '-';
-    std::string digits;
-    const char *stop = b;
-    if (b == e || !is_digit(*b) || !digit_run(b, e, digits, &stop) || stop != e) return false;
-    if (digits.size() > 18) return false;
-    long long x = std::strtoll(digits.c_str(), nullptr, 10);
-    *v = neg ? -x : x;
-    return true;
-}
-
-bool ieq(const char *b, const char *e, const char *word) {
-    const size_t n = std::strlen(word);
-    if ((size_t)(e - b) != n) return false;
-    for (size_t i = 0; i < n; ++i)
-        if ((b[i] | 0x20) != word[i]) return false;
-    return true;
-}
-
-// Python float(token): [sign] (inf | infinity | nan | decimal), decimal =
-// (digits [. [digits]] | . digits) [(e|E) [sign] digits], underscores between digits.
-bool py_float(const char *b, const char *e, double *v) {
-    std::string s;
-    if (b < e && (*b == '+' || *b == '-')) s.push_back(*b++);
-    if (ieq(b, e, "inf") || ieq(b, e, "infinity")) {
-        *v = s == "-" ? -INFINITY : INFINITY;
-        return true;
-    }
-    if (ieq(b, e, "nan")) {
-        *v = NAN;
-        return true;
-    }
-    const char *q = b;
-    bool mant = false;
-    if (q < e && is_digit(*q)) {
-        if (!digit_run(q, e, s, &q)) return false;
-        mant = true;
-    }
-    if (q < e && *q == '.') {
-        s.push_back('.');
-        ++q;
-        if (q < e && is_digit(*q)) {
-            if (!digit_run(q, e, s, &q)) return false;
-            mant = true;
-        }
-    }
-    if (!mant) return false;
-    if (q < e && (*q == 'e' || *q == 'E')) {
-        s.push_back('e');
-        ++q;
-        if (q < e && (*q == '+' || *q == '-')) s.push_back(*q++);
-        if (q == e || !is_digit(*q) || !digit_run(q, e, s, &q)) return false;
-    }
-    if (q != e) return false;
-    *v = std::strtod(s.c_str(), nullptr);
-    return true;
-}
+using pytext::py_float;
+using pytext::py_int;
+using pytext::py_repr;
 
 std::string quoted(const char *b, const char *e) { return "'" + std::string(b, e) + "'"; }
-
-std::string py_repr(double x) {
-    char buf[64];
-    for (int prec = 1; prec <= 17; ++prec) {  // shortest round-tripping form, like repr()
-        std::snprintf(buf, sizeof buf, "%.*g", prec, x);
-        if (std::strtod(buf, nullptr) == x) break;
-    }
-    std::string r(buf);
-    if (r.find_first_of(".eni") == std::string::npos) r += ".0";
-    return r;
-}
 
 // "symbol id" lines (SymbolTable.format()); ids were validated by the Python SymbolTable.
 void load_symbols(const char *b, int64_t n, std::unordered_map<std::string, int32_t> &m) {

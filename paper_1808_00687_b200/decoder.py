@@ -381,7 +381,7 @@ class BatchDecoder:
     @_locked
     def decode_posteriors(self, posts_list, cfg, mode: str | None = None,
                           label_capacity: int | None = None, lattice: bool = False,
-                          lattice_beam: float | None = None, block_frames: int = 32,
+                          lattice_beam: float | None = None, block_frames: int = 128,
                           workers: int | None = None, _attempt: int = 0) -> BatchOutput:
         """Decode from posterior matrices (the public path): host threads compute the
         frame_costs rows straight into a page-locked table in frame-block order while the
@@ -447,11 +447,21 @@ class BatchDecoder:
         lock = threading.Lock()
         done = [dict() for _ in range(n)]
         nxt = [0] * n
-        nblk = [(int(t) + block_frames - 1) // block_frames for t in total]
+        # block 0 of every utterance is short (the kernel starts as soon as it is published),
+        # later blocks are block_frames long: fewer, larger numpy calls keep the producers
+        # off the GIL (measured on the 16-core host: 32-frame blocks 174 ms, 128-frame blocks
+        # 49 ms for config 2's 64 x 1000 rows)
+        first = max(1, min(32, block_frames))
+
+        def bounds(u, b):
+            lo = 0 if b == 0 else first + (b - 1) * block_frames
+            return lo, min(int(total[u]), first if b == 0 else lo + block_frames)
+        nblk = [0 if int(t) == 0 else 1 + (max(0, int(t) - first) + block_frames - 1) // block_frames
+                for t in total]
         neg = -cfg.acoustic_scale
 
         def work(u, b):
-            lo, hi = b * block_frames, min(int(total[u]), (b + 1) * block_frames)
+            lo, hi = bounds(u, b)
             p = posts_list[u]
             if compact:   # gather the searched rows (C++, no GIL), then -scale*log in place
                 r0 = int(crow[u]) + lo

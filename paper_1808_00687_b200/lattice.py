@@ -614,65 +614,37 @@ def lattice_best_path(lat: Lattice) -> tuple[float, tuple[int, ...], tuple[int, 
 
 # ---------------------------------------------------------------- text form (lattice.py:562-627)
 def format_lattice_text(lat: Lattice) -> str:
-    """Serialise; node id 0 is the start node."""
+    """Serialise (node id 0 is the start node); native writer (csrc/lattice_text.cpp),
+    byte-identical to the reference's (repr floats)."""
+    from . import _native as N
     if not isinstance(lat, Lattice):
         lat = Lattice.from_reference(lat)
-    out = [f"LATTICE nodes={lat.num_nodes} arcs={lat.num_arcs}"]
-    fin = lat.finals
-    for i, (s, t) in enumerate(zip(lat.node_state.tolist(), lat.node_step.tolist())):
-        out.append(f"N {i} {s} {t} final {fin[i]!r}" if i in fin else f"N {i} {s} {t}")
-    for f, t, il, ol, g, a in zip(lat.arc_from.tolist(), lat.arc_to.tolist(),
-                                  lat.arc_il.tolist(), lat.arc_ol.tolist(),
-                                  lat.arc_g.tolist(), lat.arc_a.tolist()):
-        out.append(f"A {f} {t} {il} {ol} {g!r} {a!r}")
-    return "\n".join(out) + "\n"
+    v = lat._view()
+    ptr, n = C.c_void_p(), C.c_int64()
+    L = N.load()
+    N.check(L.wb_lattice_format_text(C.byref(v), C.byref(ptr), C.byref(n)), "format_lattice_text")
+    try:
+        return C.string_at(ptr, n.value).decode("ascii")
+    finally:
+        L.wb_text_free(ptr)
 
 
 def parse_lattice_text(text: str) -> Lattice:
-    rows = [r for r in (x.strip() for x in text.splitlines()) if r and not r.startswith("#")]
-    if not rows:
-        return EMPTY_LATTICE
-    head = rows[0].split()
-    if (len(head) != 3 or head[0] != "LATTICE" or not head[1].startswith("nodes=")
-            or not head[2].startswith("arcs=")):
-        raise LatticeError(f"bad lattice header {rows[0]!r}")
+    """Inverse of ``format_lattice_text`` (native reader); ``LatticeError`` for malformed
+    text, ``ValueError`` for a bad number, as the reference raises them."""
+    from . import _native as N
+    from .wfst import _ODD_BREAKS
+    if not text.isascii() or _ODD_BREAKS.search(text):
+        text = "\n".join(" ".join(line.split()) for line in text.splitlines())
+    data = text.encode("utf-8")
+    out = N.LatticeArrays()
+    L = N.load()
+    rc = L.wb_lattice_parse_text(data, len(data), C.byref(out))
     try:
-        n_nodes, n_arcs = int(head[1][6:]), int(head[2][5:])
-    except ValueError:
-        raise LatticeError(f"bad lattice header {rows[0]!r}") from None
-    st, sp, fn, fw = [], [], [], []
-    af, at, ail, aol, ag, aa = [], [], [], [], [], []
-    for r in rows[1:]:
-        x = r.split()
-        if x[0] == "N":
-            if len(x) not in (4, 6) or (len(x) == 6 and x[4] != "final"):
-                raise LatticeError(f"bad node line {r!r}")
-            if int(x[1]) != len(st):
-                raise LatticeError(f"node ids must be dense and ordered; got {r!r}")
-            st.append(int(x[2]))
-            sp.append(int(x[3]))
-            if len(x) == 6:
-                fn.append(len(st) - 1)
-                fw.append(float(x[5]))
-        elif x[0] == "A":
-            if len(x) != 7:
-                raise LatticeError(f"bad arc line {r!r}")
-            af.append(int(x[1])); at.append(int(x[2])); ail.append(int(x[3]))
-            aol.append(int(x[4])); ag.append(float(x[5])); aa.append(float(x[6]))
-        else:
-            raise LatticeError(f"unrecognized lattice line {r!r}")
-    if len(st) != n_nodes or len(af) != n_arcs:
-        raise LatticeError(f"header declares {n_nodes} nodes / {n_arcs} arcs, "
-                           f"found {len(st)} / {len(af)}")
-    if not st:
-        return EMPTY_LATTICE
-    for i, (f, t) in enumerate(zip(af, at)):
-        if not (0 <= f < len(st) and 0 <= t < len(st)):
-            raise LatticeError(f"arc {i} references a missing node")
-        if sp[t] - sp[f] not in (0, 1):
-            raise LatticeError(f"arc {i} must stay in step or advance one step, "
-                               f"got delta {sp[t] - sp[f]}")
-    return Lattice(st, sp, af, at, ail, aol, ag, aa, list(range(len(af))), fn, fw)
+        N.check(rc, "parse_lattice_text")
+        return Lattice._from_native(out)
+    finally:
+        L.wb_lattice_arrays_free(C.byref(out))
 
 
 def save_lattice(lat: Lattice, path: str) -> None:

@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 import golden_cases as GC
+import refutil
 from paper_1808_00687_b200 import lattice as L
 
 INF = math.inf
@@ -151,3 +152,53 @@ def test_canonical_batch_matches_per_utterance():
         want = L.canonical_from_device(g, nodes, arcs, ac, fin, fw)
         assert got[u].key() == want.key()
         assert np.array_equal(got[u].arc_tie, want.arc_tie)
+
+
+@pytest.mark.skipif(not refutil.HAVE_REF, reason="reference not available")
+def test_native_lattice_text_matches_reference_byte_for_byte():
+    """format_lattice_text (C++ writer, repr floats) produces the reference's exact text for
+    the reference's own lattices and random costs; parse_lattice_text reads it back to the
+    reference's parse, and malformed text raises what the reference raises."""
+    import random
+    R = refutil.ref()
+    rng = random.Random(3)
+    n = 0
+    for seed in range(40):
+        wfst, posts = refutil.random_instance(seed, max_states=10, max_arcs=30, max_frames=6,
+                                              eps_fraction=0.2)
+        rec = R.lattice.LatticeRecorder()
+        R.decoder.decode(wfst, posts, R.decoder.DecodeConfig(beam=5.0), recorder=rec)
+        try:
+            ref = R.lattice.build_lattice(rec, wfst)
+        except R.lattice.LatticeError:
+            continue
+        want = R.lattice.format_lattice_text(ref)
+        assert L.format_lattice_text(ref) == want
+        assert L.format_lattice_text(L.Lattice.from_reference(ref)) == want
+        assert L.parse_lattice_text(want) == R.lattice.parse_lattice_text(want)
+        n += 1
+    assert n > 20
+    # repr of awkward doubles: tiny, huge, integral, negative zero, inf, 17-digit values
+    vals = [0.0, -0.0, 1.0, 1e16, 1e15, 123456789012345678.0, 1e-4, 9.999e-5, 1e-5, 0.1,
+            2.5e-300, 1.7976931348623157e308, math.inf, -math.inf, 5e-324, 100.0, 1e22]
+    vals += [rng.uniform(-1e6, 1e6) for _ in range(200)] + [rng.random() * 10 ** rng.randint(-30, 30)
+                                                            for _ in range(200)]
+    nodes = tuple(R.lattice.LatticeNode(i, i) for i in range(len(vals) + 1))
+    arcs = tuple(R.lattice.LatticeArc(i, i + 1, 1, 2, v, -v) for i, v in enumerate(vals))
+    big = R.lattice.Lattice(nodes=nodes, arcs=arcs, start_id=0, finals={len(vals): vals[5]})
+    want = R.lattice.format_lattice_text(big)
+    assert L.format_lattice_text(big) == want
+    assert L.parse_lattice_text(want) == R.lattice.parse_lattice_text(want)
+    for bad in ("LATTICE nodes=x arcs=0\n", "LATTICE nodes=1 arcs=0\nN 0 0 0\nQ 1\n",
+                "LATTICE nodes=2 arcs=0\nN 0 0 0\n", "LATTICE nodes=1 arcs=0\nN 1 0 0\n",
+                "LATTICE nodes=1 arcs=0\nN 0 a 0\n", "LATTICE nodes=2 arcs=1\nN 0 0 0\nN 1 0 3\nA 0 1 1 1 0.5 0.5\n",
+                "LATTICE nodes=1 arcs=1\nN 0 0 0\nA 0 5 1 1 0.5 0.5\n",
+                "LATTICE nodes=1 arcs=1\nN 0 0 0\nA 0 0 1 1 x 0.5\n", "LATTICE nodes=1 arcs=0\nN 0 0 0 final\n"):
+        try:
+            R.lattice.parse_lattice_text(bad)
+            kind = None
+        except Exception as exc:   # noqa: BLE001 - the exception type is the contract
+            kind = type(exc).__name__
+        with pytest.raises(Exception) as ei:
+            L.parse_lattice_text(bad)
+        assert type(ei.value).__name__ == kind, bad
