@@ -460,6 +460,14 @@ def main():
                     lat_stats["pruned_nodes"] += p.num_nodes
                     lat_stats["pruned_arcs"] += p.num_arcs
             e_ms = e_ev[0][0].elapsed_time(e_ev[-1][1])
+            # lattice output: the batch's pruned lattices as text through the
+            # native writer (format_lattice_text, byte-identical to the reference's)
+            from paper_1808_00687_b200.lattice import format_lattice_text
+            t0 = time.perf_counter()
+            text_bytes = sum(len(format_lattice_text(p)) for p in lats
+                             if not isinstance(p, LatticeError))
+            lat_stats["text_ms"] = 1e3 * (time.perf_counter() - t0)
+            lat_stats["text_bytes"] = text_bytes
         else:
             for k in range(args.steps):
                 flush.zero_()
@@ -596,7 +604,7 @@ def main():
             # one persistent decode kernel per step (backtrace in-kernel) + the lattice prune
             "gpu_launches": args.steps * (2 if lat_on else 1),
             "counters_per_step": {k: int(res[k].sum()) for k in
-                                  ("n_tok", "a_emit", "a_fin", "a_cas", "e_eps", "n_cand",
+                                  ("n_tok", "a_emit", "a_fin", "a_cas", "e_eps", "eps_rounds", "n_cand",
                                    "n_surv", "n_rec")},
             "phase_share": dict(zip(["stage_row", "expand", "eps_closure", "gather", "select",
                                      "flags", "compact", "other"],

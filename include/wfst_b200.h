@@ -114,6 +114,7 @@ typedef struct {
     int64_t n_rec;           /* backpointer records written */
     int64_t lat_arcs;        /* raw lattice arcs recorded (lattice mode) */
     int64_t a_cas;           /* emitting relaxations that reached a slot (not beam-skipped) */
+    int64_t eps_rounds;      /* epsilon-closure frontier rounds (summed over steps) */
     /* SM clock cycles spent per phase (CTA thread 0, measured after each phase barrier):
      * [0] cost-row staging, [1] emitting expansion, [2] epsilon closure, [3] candidate
      * gather + min/max, [4] max-active histogram/select, [5] survivor flags + chain marks,

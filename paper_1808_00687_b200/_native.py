@@ -81,7 +81,7 @@ UTT_RESULT_DTYPE = np.dtype([
     ("status", np.int32), ("capacity_flags", np.int32), ("path_flags", np.int32),
     ("best_trace", np.int64), ("n_tok", np.int64), ("a_emit", np.int64),
     ("a_fin", np.int64), ("e_eps", np.int64), ("n_cand", np.int64), ("n_surv", np.int64),
-    ("n_rec", np.int64), ("lat_arcs", np.int64), ("a_cas", np.int64),
+    ("n_rec", np.int64), ("lat_arcs", np.int64), ("a_cas", np.int64), ("eps_rounds", np.int64),
     ("phase_cycles", np.int64, (8,))])
 
 _lib = None

@@ -875,7 +875,7 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
 // up one round later, after the barrier has published it.
 struct EpsOut {
     u32 tag, e_eps;
-    int status;
+    int status, rounds;
 };
 
 template <int BLOCK, int KC>
@@ -897,6 +897,7 @@ __noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev 
     const int r = K > 1 ? cta_rank() : 0, cbase = r * ws.cap;
     Slot *slot = c.slot();
     const Slot empty = {EMPTY_KEY, 0xFFFFFFFFu, 0xFFFFFFFFu};
+    int n_rounds = 0;
     // Round k consumes the frontier pushed in round k-1 (round 0: by expand) from buffer k & 1
     // and pushes into the other; each CTA of a cluster lane works its own frontier region and
     // the round ends at a lane barrier, after which every CTA reads every CTA's count.
@@ -909,7 +910,7 @@ __noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev 
             total += *peer(&sh.nfr[par], o);
             ovf |= *peer(&sh.overflow, o);
         }
-        if (total == 0) break;
+        if (total == 0) { n_rounds = rounds; break; }
         // a candidate overflow leaves frontier states without a candidate index: the step
         // has failed (WB_CAP_CANDIDATES), stop before following stale indices
         if (ovf) { status = wb_cap(WB_CAP_CANDIDATES); break; }
@@ -998,7 +999,7 @@ __noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev 
         }
         lane_sync(K);
     }
-    return EpsOut{tag_cur, e_eps, status};
+    return EpsOut{tag_cur, e_eps, status, n_rounds};
 }
 
 __device__ __forceinline__ int bucket_of(double cst, double best, double scale) {
@@ -1340,66 +1341,58 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
     int4 *tinfo = c.tok_info(nxt);
     double *tcost = c.tok_cost(nxt);
     u32 *pend = c.front(0) + cbase;
-    u32 *tokidx = c.front(1) + cbase;  // survivor -> next-token slot (frontier buffers are free here)
     {
-        // E1: indices from the flags only (ballot ranks within warp segments)
+        // E: one pass over each warp's segment, 32 candidates at a time: ballot ranks give
+        // every kept candidate its record index (left in its flag word for epsilon winners
+        // that trace through it) and every survivor its next-token slot; the token and the
+        // record are written in the same pass.  The candidate arrays are read coalesced, the
+        // loads issued before the ballots.
+        const int4 *__restrict__ rng_ = c.cand_rng() + cbase;
         int ra = (int)sh.wa[w], rb = (int)sh.wb[w] + surv_before;
         const u32 lt = lanemask_lt();
         for (int i0 = lo; i0 < hi; i0 += 32) {
-            int i = i0 + l;
-            u32 f = i < hi ? vca[i] : 0u;
-            bool keep = f != 0u, surv = (f & F_SURV) != 0u;
-            u32 mk = __ballot_sync(FULL, keep), ms = __ballot_sync(FULL, surv);
-            if (i < hi) {
-                ca[i] = keep ? (u32)(base + (u64)(ra + __popc(mk & lt))) : CA_NONE;
-                tokidx[i] = surv ? (u32)(rb + __popc(ms & lt)) : CA_NONE;
+            const int i = i0 + l;
+            const bool in = i < hi;
+            u32 f = 0u, a = 0u, p = 0u, st = 0u;
+            int4 rg = make_int4(0, 0, 0, 0);
+            u64 k = 0;
+            if (in) {
+                f = vca[i];
+                a = carc[i];
+                p = cpay[i];
+                st = cst[i];
+                rg = rng_[i];
+                k = ckey[i];
             }
+            const bool keep = f != 0u, surv = (f & F_SURV) != 0u;
+            const u32 mk = __ballot_sync(FULL, keep), ms = __ballot_sync(FULL, surv);
+            const u32 rec = (u32)(base + (u64)(ra + __popc(mk & lt)));
+            const u32 tj = (u32)(rb + __popc(ms & lt));
             ra += __popc(mk);
             rb += __popc(ms);
+            if (!in) continue;
+            ca[i] = keep ? rec : CA_NONE;
+            if (surv) {
+                WB_CHECK(ws, tj < (u32)ws.lcap, CHK_BOUNDS);
+                tinfo[tj] = make_int4((int)st, (int)rec, rg.y, rg.z);
+                tcost[tj] = key_cost(k);
+                if (k == mn) sh.best_tok = (int)tj;  // any minimal token will do
+                if (ws.tok_eps) ws.tok_eps[2 * c.co() + (size_t)nxt * ws.lcap + tj] = rg.x;
+            }
+            if (keep) {
+                WB_CHECK(ws, (u64)rec < ws.arena_cap, CHK_BOUNDS);
+                if (a != 0u && (p & EPS_BIT)) {
+                    const int qq = atomicAdd(&sh.n_pend, 1);
+                    pend[qq] = (u32)i;  // epsilon winner: needs its source's record index
+                } else {
+                    const u32 prev = a == 0u ? ROOT_PREV : p;
+                    c.arena()[rec] = (u64)a | ((u64)prev << 32);
+                }
+            }
         }
     }
     // epsilon winners resolve their source's record index, possibly another CTA's
-    if (g.has_eps) lane_sync(K); else __syncthreads();
-    {
-        // E2: records + next tokens, G candidates per thread with their loads in flight
-        constexpr int G = Tune<BLOCK>::GATHER;
-        const int4 *__restrict__ rng_ = c.cand_rng() + cbase;
-        for (int i0 = threadIdx.x; i0 < n_loc; i0 += BLOCK * G) {
-            u32 rec[G], tj[G], a[G], p[G];
-#pragma unroll
-            for (int q = 0; q < G; ++q) {
-                int i = i0 + q * BLOCK;
-                rec[q] = CA_NONE;
-                tj[q] = CA_NONE;
-                if (i < n_loc) {
-                    rec[q] = vca[i];
-                    tj[q] = tokidx[i];
-                    a[q] = carc[i];
-                    p[q] = cpay[i];
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < G; ++q) {
-                int i = i0 + q * BLOCK;
-                if (tj[q] != CA_NONE) {
-                    int4 rg = rng_[i];
-                    tinfo[tj[q]] = make_int4((int)cst[i], (int)rec[q], rg.y, rg.z);
-                    tcost[tj[q]] = key_cost(ckey[i]);
-                    if (ckey[i] == mn) sh.best_tok = (int)tj[q];  // any minimal token will do
-                    if (ws.tok_eps) ws.tok_eps[2 * c.co() + (size_t)nxt * ws.lcap + tj[q]] = rg.x;
-                }
-                if (rec[q] != CA_NONE) {
-                    if (a[q] != 0u && (p[q] & EPS_BIT)) {
-                        int qq = atomicAdd(&sh.n_pend, 1);
-                        pend[qq] = (u32)i;  // epsilon winner: needs its source's record index
-                    } else {
-                        u32 prev = a[q] == 0u ? ROOT_PREV : p[q];
-                        c.arena()[rec[q]] = (u64)a[q] | ((u64)prev << 32);
-                    }
-                }
-            }
-        }
-    }
+    if (g.has_eps) lane_sync(K);
 #ifdef WB_CHECKS
     // debug_epoch analogue: every slot this step touched is EMPTY again (no relaxation of
     // this step can leak into the next); registration counters are cleared for the next step
@@ -1409,7 +1402,7 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
         ws.chk_seen[c.so() + st] = 0u;
     }
 #endif
-    __syncthreads();
+    if (!g.has_eps) __syncthreads();
     const int n_pend = sh.n_pend;
     for (int q = threadIdx.x; q < n_pend; q += BLOCK) {
         int i = (int)pend[q];
@@ -1901,7 +1894,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
         const long long row0 = b.row_off[u];
         int status = WB_OK;
         u32 a_emit = 0, a_fin = 0, a_cas = 0, e_eps = 0;  // per-thread counters
-        long long n_tok = 0, n_cand_tot = 0, n_surv_tot = 0, n_rec = 0;
+        long long n_tok = 0, n_cand_tot = 0, n_surv_tot = 0, n_rec = 0, eps_rounds = 0;
         int nf = T;
         if (cfg.mode == 1) {
             if (T > ws.T_cap) {  // frame list would overflow: report, do not decode
@@ -1939,6 +1932,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             tag = eo.tag;
             e_eps += eo.e_eps;
             if (eo.status) status = eo.status;
+            eps_rounds += eo.rounds;
         }
         int cur = 0;
         StepOut so = finish_step<BLOCK, KC>(cur, g, ws, cfg);
@@ -2052,6 +2046,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
                 tag = eo.tag;
                 e_eps += eo.e_eps;
                 if (eo.status) status = eo.status;
+            eps_rounds += eo.rounds;
             }
             tick<BLOCK>(2);
             so = finish_step<BLOCK, KC>(cur ^ 1, g, ws, cfg);
@@ -2183,6 +2178,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             r.a_emit = t_emit;
             r.a_fin = t_fin;
             r.a_cas = t_cas;
+            r.eps_rounds = eps_rounds;
             r.e_eps = t_eps;
             r.n_cand = n_cand_tot;
             r.n_surv = n_surv_tot;
