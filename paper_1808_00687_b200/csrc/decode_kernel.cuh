@@ -656,13 +656,24 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
                 }
                 m = warp_min_u64(m);
                 if (l == 0 && m < sh_run_min()) atomicMin(reinterpret_cast<unsigned long long *>(&SH<BLOCK>().run_min), m);
-                __syncthreads();
+                // a cluster lane's CTAs each saw their own tokens: the lane's exact minimum is
+                // the minimum over the CTAs (run_min is not written again this step)
+                lane_sync(KC);
+                if (KC > 1) {
+                    u64 lm = sh_run_min();
+                    for (int q = 1; q < KC; ++q) {
+                        const u64 o = *(volatile u64 *)&peer(&SH<BLOCK>(), (r + q) & (KC - 1))->run_min;
+                        lm = o < lm ? o : lm;
+                    }
+                    if (threadIdx.x == 0) SH<BLOCK>().x_run_min = lm;
+                    __syncthreads();
+                }
             }
         }
         // the final cutoff key when the exact minimum is known (EMPTY_KEY: running bound)
         u64 exact_thr = EMPTY_KEY;
         if (exact) {
-            const u64 rm = sh_run_min();
+            const u64 rm = KC > 1 ? SH<BLOCK>().x_run_min : sh_run_min();
             if (rm != EMPTY_KEY) exact_thr = cost_key(__dadd_rn(key_cost(rm), beam));
         }
         const u32 s0 = (u32)__cvta_generic_to_shared(stage);
@@ -886,7 +897,11 @@ __noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev 
     // beam skip as in expand: with non-negative weights every candidate of this step costs at
     // least the emitting minimum, and run_min is an upper bound of it (this CTA's minimum), so
     // run_min + beam is at or above the step's final cutoff
-    const u64 rm = sh.run_min;
+    u64 rm = sh.run_min;
+    for (int q = 1; q < KC; ++q) {   // the lane's minimum (expand ended with a lane barrier)
+        const u64 o = *(volatile u64 *)&peer(&sh, (cta_rank() + q) & (KC - 1))->run_min;
+        rm = o < rm ? o : rm;
+    }
     const bool skip_on = g.nonneg && ws.beam_skip && beam < INFINITY && rm != EMPTY_KEY;
     const u64 thr = skip_on ? cost_key(__dadd_rn(key_cost(rm), beam)) : EMPTY_KEY;
     u32 tag_cur = tag_in, e_eps = 0;
