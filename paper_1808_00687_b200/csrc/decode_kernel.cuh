@@ -185,6 +185,7 @@ struct Smem {
     long long x_sum;    // this CTA's partial sum of a cluster reduction
     int x_n, x_flags;   // this CTA's candidates this step; bit 0 overflow, bit 1 keys in global
     int x_gn;           // rank 0: boundary-bucket members collected from the lane's CTAs
+    u32 x_gmask;        // rank 0: CTAs whose candidate flags live in global memory this step
     int x_stream;       // this CTA timed out waiting for a streamed cost row (cluster lanes)
     long long chk_off;  // checked build: this step's offset in the lane's claim log
     int x_ck, x_cs;     // kept / surviving candidates of this CTA (compaction bases)
@@ -1223,22 +1224,34 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
             }
         }
     }
-    block_minmax<BLOCK>(mn, mx);
     // lane-wide: min / max, candidate count, overflow, where each CTA keeps its flags
     int n_all = n_loc, flags = (sh.overflow ? 1 : 0) | (in_smem ? 0 : 2) | (sh.x_stream ? 4 : 0);
     u32 glob_mask = in_smem ? 0u : 1u << r;   // CTAs whose flags live in global memory
-    if (K > 1) {
-        if (threadIdx.x == 0) { sh.x_mn = mn; sh.x_mx = mx; sh.x_n = n_loc; sh.x_flags = flags; }
+    if (K == 1) {
+        block_minmax<BLOCK>(mn, mx);
+    } else {
+        // warps fold into this CTA's header with shared-memory atomics (reset at the step
+        // start), one lane barrier, then every CTA reads every CTA's values through DSMEM
+        mn = warp_min_u64(mn);
+        mx = warp_max_u64(mx);
+        if ((threadIdx.x & 31) == 0) {
+            if (mn != EMPTY_KEY) atomicMin(reinterpret_cast<unsigned long long *>(&sh.x_mn), mn);
+            if (mx != 0ull) atomicMax(reinterpret_cast<unsigned long long *>(&sh.x_mx), mx);
+        }
+        if (threadIdx.x == 0) { sh.x_n = n_loc; sh.x_flags = flags; }
         lane_sync(K);
+        mn = *(volatile u64 *)&sh.x_mn;
+        mx = *(volatile u64 *)&sh.x_mx;
         for (int q = 1; q < K; ++q) {
             const int o = (r + q) & (K - 1);
             const Smem<BLOCK> *po = peer(&sh, o);
-            const u64 a = po->x_mn, b = po->x_mx;
+            const u64 a = *(volatile const u64 *)&po->x_mn, b = *(volatile const u64 *)&po->x_mx;
             mn = a < mn ? a : mn;
             mx = b > mx ? b : mx;
-            n_all += po->x_n;
-            flags |= po->x_flags;
-            if (po->x_flags & 2) glob_mask |= 1u << o;
+            n_all += *(volatile const int *)&po->x_n;
+            const int fo = *(volatile const int *)&po->x_flags;
+            flags |= fo;
+            if (fo & 2) glob_mask |= 1u << o;
         }
     }
     int status = (flags & 4) ? wb_cap(WB_CAP_STREAM) : (flags & 1) ? wb_cap(WB_CAP_CANDIDATES) : WB_OK;
@@ -1391,7 +1404,10 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
                 WB_CHECK(ws, tj < (u32)ws.lcap, CHK_BOUNDS);
                 tinfo[tj] = make_int4((int)st, (int)rec, rg.y, rg.z);
                 tcost[tj] = key_cost(k);
-                if (k == mn) sh.best_tok = (int)tj;  // any minimal token will do
+                if (k == mn) {   // any minimal token will do; every CTA of the lane gets it
+                    sh.best_tok = (int)tj;
+                    for (int q = 1; q < K; ++q) peer(&sh, (r + q) & (K - 1))->best_tok = (int)tj;
+                }
                 if (ws.tok_eps) ws.tok_eps[2 * c.co() + (size_t)nxt * ws.lcap + tj] = rg.x;
             }
             if (keep) {
@@ -1926,6 +1942,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             sh.overflow = 0;
             sh.nfr[0] = sh.nfr[1] = 0;
             sh.x_stream = 0;
+            sh.x_mn = EMPTY_KEY; sh.x_mx = 0; sh.x_n = 0; sh.x_flags = 0; sh.x_gmask = 0;
             if (rank == 0) {
                 u64 k0 = cost_key(0.0);
                 __stcg(reinterpret_cast<ulonglong2 *>(&c.slot()[g.start]),
@@ -2001,12 +2018,9 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
                 sh.n_cand = 0; sh.nfr[0] = sh.nfr[1] = 0; sh.overflow = 0; sh.n_log = 0;
                 sh.run_min = EMPTY_KEY;
                 sh.next_chunk = BLOCK / 32;
-                // the pilot needs one minimal live token; in a cluster lane only the CTA that
-                // wrote it (in the last compaction) has one
-                for (int q = 1; q < K && sh.best_tok < 0; ++q)
-                    sh.best_tok = peer(&sh, (rank + q) & (K - 1))->best_tok;
+                // rank 0's lane accumulators of this step's prune (read after many barriers)
+                sh.x_mn = EMPTY_KEY; sh.x_mx = 0; sh.x_n = 0; sh.x_flags = 0; sh.x_gmask = 0;
             }
-            __syncthreads();
             // Pilot of the beam skip (expand_emitting): warp 0 evaluates the arcs of a cheapest
             // live token against the row in global memory while the other warps stage it.
             const bool pilot = row_in_smem && pilot_on && sh.best_tok >= 0 && sh.best_tok < n_live;
