@@ -134,7 +134,7 @@ inline void py_repr(double x, std::string &out) {
             out.push_back('.');
             out.append(digits, 1, std::string::npos);
         }
-        char eb[8];
+        char eb[16];
         std::snprintf(eb, sizeof eb, "e%c%02d", ex < 0 ? '-' : '+', ex < 0 ? -ex : ex);
         out += eb;
     }
