@@ -91,19 +91,23 @@ def _load_graph(path, isyms, osyms):
         return parse_wfst_text(fh.read(), isyms, osyms)
 
 
-def _load_inputs(args):
+def _load_inputs(args, batch: bool = False):
     isyms, osyms = _load_symbols(args.isyms), _load_symbols(args.osyms)
     graph = _load_graph(args.graph, isyms, osyms)
     if args.save_csr:
         save_wfst_binary(graph, args.save_csr)
-    posts = [load_posteriors(p, strict=args.strict_posteriors) for p in args.posts]
+    if args.device is not None:
+        import torch
+        torch.cuda.set_device(args.device)
+    if batch:   # POST1 files read natively into one page-locked table (decode consumes it)
+        from .posteriors import PosteriorBatch
+        posts = PosteriorBatch(args.posts, strict=args.strict_posteriors)
+    else:
+        posts = [load_posteriors(p, strict=args.strict_posteriors) for p in args.posts]
     if args.workers < 1:
         raise ValueError(f"workers must be >= 1, got {args.workers}")
     if args.group_size < 1:
         raise ValueError(f"group_size must be >= 1, got {args.group_size}")
-    if args.device is not None:
-        import torch
-        torch.cuda.set_device(args.device)
     return graph, posts, osyms
 
 
@@ -123,9 +127,9 @@ def _words(labels, cost, osyms) -> str:
 
 
 def cmd_decode(args) -> int:
-    graph, posts, osyms = _load_inputs(args)
+    graph, posts, osyms = _load_inputs(args, batch=True)
     cfg = _config(args)
-    recorders = [LatticeRecorder() for _ in posts] if args.lattice_out else None
+    recorders = [LatticeRecorder() for _ in range(len(posts))] if args.lattice_out else None
     results = decode_batch(graph, posts, cfg, mode=cfg.mode, recorder=recorders)
     code = EXIT_OK
     for i, r in enumerate(results):
