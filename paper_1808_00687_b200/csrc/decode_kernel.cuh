@@ -81,7 +81,6 @@ struct WorkDev {
     u32 *qtag;            // [slots][S]   epsilon frontier dedup tags
     u32 *tag_ctr;         // [slots]
     u32 *cand_state;      // [slots][cap]
-    int4 *cand_rng;       // [slots][cap] {eps_lo, emit_lo, emit_hi, 0}
     u32 *cand_arc, *cand_pay;
     u64 *cand_key;        // [slots][cap] (used when a step overflows shared memory)
     u32 *cand_ca;         // [slots][cap]
@@ -357,7 +356,6 @@ struct Lane {
     __device__ __forceinline__ u32 *cand_of() const { return ws.cand_of + so(); }
     __device__ __forceinline__ u32 *qtag() const { return ws.qtag + so(); }
     __device__ __forceinline__ u32 *cand_state() const { return ws.cand_state + co(); }
-    __device__ __forceinline__ int4 *cand_rng() const { return ws.cand_rng + co(); }
     __device__ __forceinline__ u32 *cand_arc() const { return ws.cand_arc + co(); }
     __device__ __forceinline__ u32 *cand_pay() const { return ws.cand_pay + co(); }
     __device__ __forceinline__ u64 *cand_key() const { return ws.cand_key + co(); }
@@ -403,7 +401,6 @@ __device__ __forceinline__ int warp_append(bool first, u32 d, int4 rng, bool pus
         WB_CHECK(ws, loc >= ws.cap || (idx >= 0 && idx < ws.lcap), CHK_BOUNDS);
         if (loc < ws.cap) {
             c.cand_state()[idx] = d;
-            c.cand_rng()[idx] = make_int4(rng.x, rng.y, rng.z, 0);
             if (g.has_eps && rng.x < rng.y) {
                 c.cand_of()[d] = (u32)idx;
                 pf = push;
@@ -1375,7 +1372,6 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
         // that trace through it) and every survivor its next-token slot; the token and the
         // record are written in the same pass.  The candidate arrays are read coalesced, the
         // loads issued before the ballots.
-        const int4 *__restrict__ rng_ = c.cand_rng() + cbase;
         int ra = (int)sh.wa[w], rb = (int)sh.wb[w] + surv_before;
         const u32 lt = lanemask_lt();
         for (int i0 = lo; i0 < hi; i0 += 32) {
@@ -1389,10 +1385,13 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
                 a = carc[i];
                 p = cpay[i];
                 st = cst[i];
-                rg = rng_[i];
                 k = ckey[i];
             }
             const bool keep = f != 0u, surv = (f & F_SURV) != 0u;
+            // a survivor's {eps_lo, emit_lo, emit_hi} is the second half of its winning arc's
+            // record (the arc ends in this state; its first half was read by expand, so the
+            // sector is in cache) -- no per-candidate range array
+            if (surv) rg = a == 0u ? g.start_rng : __ldg(&g.arcs[2 * (size_t)(a - 1u) + 1]);
             const u32 mk = __ballot_sync(FULL, keep), ms = __ballot_sync(FULL, surv);
             const u32 rec = (u32)(base + (u64)(ra + __popc(mk & lt)));
             const u32 tj = (u32)(rb + __popc(ms & lt));
@@ -1948,7 +1947,6 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
                 __stcg(reinterpret_cast<ulonglong2 *>(&c.slot()[g.start]),
                        make_ulonglong2(k0, (u64)0u | ((u64)ROOT_PREV << 32)));
                 c.cand_state()[0] = (u32)g.start;
-                c.cand_rng()[0] = g.start_rng;
                 if (g.has_eps) c.cand_of()[g.start] = 0u;
                 sh.n_cand = 1;
                 if (g.has_eps && g.start_rng.x < g.start_rng.y) {
