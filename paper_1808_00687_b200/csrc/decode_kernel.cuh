@@ -1181,7 +1181,8 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
     // P1: gather slot contents (batched loads), reset slots, min / max
     if (threadIdx.x == 0) sh.best_tok = -1;
     u64 mn = EMPTY_KEY, mx = 0;
-    constexpr int G1 = Tune<BLOCK>::GATHER_P1;
+    // a cluster CTA holds ~n/K candidates: keep all of a thread's slot exchanges in flight
+    constexpr int G1 = KC > 1 ? 4 : Tune<BLOCK>::GATHER_P1;
     for (int i0 = threadIdx.x; i0 < n_loc; i0 += BLOCK * G1) {
         u32 st[G1];
         Slot v[G1];
