@@ -515,6 +515,7 @@ def main():
             p_ms = float(t.item())
         e2e_post = {"value": frames_all * args.steps / (p_ms / 1e3), "unit": "frames/s",
                     "ms_per_step": p_ms / args.steps,
+                    "host_timeline_ms": getattr(dec, "last_stream_ms", None),
                     "note": "posterior matrices in; host numpy log (rows in frame blocks, "
                             "all host cores) streamed into the running kernel"}
 

@@ -390,6 +390,8 @@ class BatchDecoder:
         posteriors.py:109-110), gathered into a compacted table indexed by search step.
         Bit-identical to ``decode_host`` on ``cost_table``."""
         import os
+        import time
+        t_start = time.perf_counter()
         import threading
         from concurrent.futures import ThreadPoolExecutor
         from .posteriors import PosteriorBatch, cost_rows
@@ -440,6 +442,7 @@ class BatchDecoder:
         self._last_max_active = cfg.max_active
         N.flush_destroy()
         L = self._L
+        t_setup = time.perf_counter()
         # producers: row blocks in block-major order; each utterance's ready count advances
         # over its contiguous finished prefix.  They start BEFORE the launch: when launches are
         # serialised (CUDA_LAUNCH_BLOCKING=1, ncu, compute-sanitizer) wb_decode_stream returns
@@ -450,7 +453,7 @@ class BatchDecoder:
         # block 0 of every utterance is short (the kernel starts as soon as it is published),
         # later blocks are block_frames long: fewer, larger numpy calls keep the producers
         # off the GIL (measured on the 16-core host: 32-frame blocks 174 ms, 128-frame blocks
-        # 49 ms for config 2's 64 x 1000 rows)
+        # 49 ms for config 2's 64 x 1000 rows; blocks doubling from 16 frames were slower)
         first = max(1, min(32, block_frames))
 
         def bounds(u, b):
@@ -490,22 +493,37 @@ class BatchDecoder:
         tasks = [(u, b) for b in range(max(nblk) if nblk else 0) for u in range(n) if b < nblk[u]]
         nw = workers or int(os.environ.get("WB_PRODUCERS", 0)) or len(os.sched_getaffinity(0))
         ex = ThreadPoolExecutor(nw)
+        futs: list = []
+
+        def submit_all():   # in block order; a helper thread, so the launch is not delayed
+            for u, b in tasks:
+                futs.append(ex.submit(work, u, b))
+        submitter = threading.Thread(target=submit_all, daemon=True)
         try:
-            futs = [ex.submit(work, u, b) for u, b in tasks]
+            submitter.start()
             N.check(L.wb_decode_stream(self._h, n, costs.ctypes.data, off.ctypes.data,
                                        T.ctypes.data, L1, blank.ctypes.data, C.byref(ncfg), cap,
                                        ready.ctypes.data, crow.ctypes.data if compact else None,
                                        None), "decode")
+            t_launch = time.perf_counter()
+            submitter.join()
             for f in futs:
                 f.result()
         finally:
+            submitter.join()
             ex.shutdown(wait=True)
             ready[:] = total  # every row is written (or the kernel must not wait forever)
+        t_rows = time.perf_counter()
         res = np.zeros(n, dtype=N.UTT_RESULT_DTYPE)
         ol = np.zeros((n, cap), dtype=np.int32)
         il = np.zeros((n, cap), dtype=np.int32)
         N.check(L.wb_decode_finish(self._h, res.ctypes.data, ol.ctypes.data, il.ctypes.data),
                 "decode")
+        # host-side timeline of the last streaming decode (ms since the call): setup done,
+        # kernel launched, every cost row published, results back
+        self.last_stream_ms = {k: round(1e3 * (v - t_start), 2) for k, v in (
+            ("setup", t_setup), ("launched", t_launch), ("rows_published", t_rows),
+            ("finished", time.perf_counter()))}
         bad = res["status"] != N.WB_OK
         if bad.any():   # a capacity ran out: grow exactly that one and decode again
             if _attempt >= 16:
