@@ -334,6 +334,11 @@ int wb_check_report(wb_decoder_t d, int32_t n_lanes, int64_t *first_violation);
 int wb_claim_log(wb_decoder_t d, int32_t lane, int32_t n_steps, int32_t *queue_len,
                  uint16_t *groups, int64_t groups_cap, int64_t *n_logged);
 
+/* Utterance lanes of a decoder (persistent lanes decoding concurrently; fewer than the SMs when
+ * a large graph's per-lane dense arrays would not fit) and the largest cluster size its
+ * candidate workspace allows. */
+int wb_decoder_lanes(wb_decoder_t d, int32_t *lanes, int32_t *max_cluster);
+
 /* CTAs per utterance lane (thread-block cluster size) of the last decode launch. */
 int wb_last_launch(wb_decoder_t d, int32_t *cluster_ctas);
 

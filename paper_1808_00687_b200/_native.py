@@ -96,7 +96,7 @@ EXPORTED = ("wb_last_error", "wb_version", "wb_device_count", "wb_graph_create",
             "wb_lattice_split", "wb_decode_stream", "wb_decode_finish", "wb_wfst_parse_text",
             "wb_parsed_wfst_free", "wb_gather_rows", "wb_post1_info", "wb_post1_read", "wb_last_launch",
             "wb_checks_enabled", "wb_check_report", "wb_claim_log", "wb_lattice_format_text",
-            "wb_lattice_parse_text", "wb_text_free")
+            "wb_lattice_parse_text", "wb_text_free", "wb_decoder_lanes")
 
 
 _checked_lib = None
@@ -140,6 +140,7 @@ def _open(path):
                                  C.c_int32, C.c_void_p, C.c_int64, C.c_int32]
     L.wb_gather_rows.restype = None
     L.wb_last_launch.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
+    L.wb_decoder_lanes.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
     L.wb_lattice_format_text.argtypes = [C.POINTER(LatticeArrays), C.POINTER(C.c_void_p),
                                          C.POINTER(C.c_int64)]
     L.wb_lattice_parse_text.argtypes = [C.c_char_p, C.c_int64, C.POINTER(LatticeArrays)]

@@ -100,48 +100,8 @@ __device__ __forceinline__ Slot cas_slot(Slot *p, const Slot &expect, const Slot
     return o;
 }
 
-// Fire-and-forget reductions (REDG): the issuing warp does not wait for the L2 round trip.
-__device__ __forceinline__ void red_min_u64(u64 *p, u64 v) {
-    asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(p), "l"(v));
-}
-__device__ __forceinline__ void red_max_u64(u64 *p, u64 v) {
-    asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(p), "l"(v));
-}
-__device__ __forceinline__ void red_min_u32(u32 *p, u32 v) {
-    asm volatile("red.relaxed.gpu.global.min.u32 [%0], %1;" ::"l"(p), "r"(v));
-}
-__device__ __forceinline__ void red_add_u32(u32 *p, u32 v) {
-    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v));
-}
-__device__ __forceinline__ void red_add_u64(u64 *p, u64 v) {
-    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v));
-}
-
 __device__ __forceinline__ bool slot_better(u64 key, u32 arcp1, const Slot &cur) {
     return key < cur.key || (key == cur.key && arcp1 < cur.arcp1);
-}
-
-// Min-recombination under the (cost, src, arc) total order with equal keys rejected
-// (_relax, decoder.py:121-135; StateSlots.relax, parallel.py:106-128).
-// Returns true when this candidate was installed; *first = slot was empty before,
-// *decreased = the slot's cost strictly dropped (so epsilon successors must be re-relaxed).
-__device__ __forceinline__ bool relax_slot(Slot *p, u64 key, u32 arcp1, u32 pay, bool *first,
-                                           bool *decreased) {
-    Slot cur = ld_slot(p);
-    Slot want;
-    want.key = key;
-    want.arcp1 = arcp1;
-    want.pay = pay;
-    while (slot_better(key, arcp1, cur)) {
-        Slot prev = cas_slot(p, cur, want);
-        if (prev.key == cur.key && prev.arcp1 == cur.arcp1 && prev.pay == cur.pay) {
-            *first = cur.key == EMPTY_KEY;
-            *decreased = key < cur.key;
-            return true;
-        }
-        cur = prev;
-    }
-    return false;
 }
 
 // Arc-record load.  With WB_ARC_EVICT_FIRST the line is marked evict-first in L2 (a random

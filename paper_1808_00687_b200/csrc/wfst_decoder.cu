@@ -416,10 +416,28 @@ int wb_decoder_create(wb_graph_t g, const wb_decoder_opts *o, wb_decoder_t *out)
     d->num_sms = prop.multiProcessorCount;
     d->block = opts.block_threads;
     d->cluster = opts.cluster_ctas;
-    // one persistent lane per SM (the kernel's shared-memory candidate store fills an SM)
-    d->slots = opts.max_utts_in_flight > 0 ? opts.max_utts_in_flight : d->num_sms;
     d->cap = opts.cand_capacity > 0 ? opts.cand_capacity : std::min(g->S, 1 << 18);
     d->cap = std::max(1, std::min(d->cap, g->S));
+    // one persistent lane per SM (the kernel's shared-memory candidate store fills an SM) --
+    // unless the dense per-state arrays of that many lanes do not fit in device memory (a
+    // large graph: S x 24 B per lane): then fewer lanes, each a cluster of 2 or 4 CTAs, so the
+    // SMs still fill
+    d->slots = opts.max_utts_in_flight > 0 ? opts.max_utts_in_flight : d->num_sms;
+    if (opts.max_utts_in_flight <= 0) {
+        size_t free_b = 0, total_b = 0;
+        CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+        double budget = 0.75 * (double)free_b;
+        if (const char *mb = std::getenv("WB_MEM_BUDGET_GB")) budget = std::atof(mb) * 1e9;
+        const double per_lane = (double)g->S * (sizeof(Slot) + (g->has_eps ? 2 * sizeof(u32) : 0)) +
+                                (double)sizeof(u64) * (4 << 20);   // dense slots (+ eps maps), default arena
+        const double per_cta = (double)d->cap * 96.0;               // candidate / token / frontier regions
+        auto fits = [&](int lanes, int k) { return lanes * per_lane + lanes * k * per_cta <= budget; };
+        int lanes = d->num_sms, k = 1;
+        while (k <= 4 && !fits(lanes = std::max(1, d->num_sms / k), k)) k *= 2;   // smallest K that fits
+        if (k > 4)
+            while (lanes > 1 && !fits(lanes, 4)) --lanes;
+        d->slots = lanes;
+    }
     // cluster lanes: when the lanes leave SMs idle, a lane may be a cluster of up to 4 CTAs
     // (8 on request), each with its own candidate / token / frontier region
     d->kmax = std::max(1, opts.cluster_ctas);
@@ -538,6 +556,13 @@ int wb_claim_log(wb_decoder_t d, int32_t lane, int32_t n_steps, int32_t *queue_l
         CUDA_TRY(cudaMemcpy(groups, d->chk_log + (size_t)lane * d->chk_log_cap,
                             sizeof(uint16_t) * n, cudaMemcpyDeviceToHost));
     *n_logged = n;
+    return WB_OK;
+}
+
+int wb_decoder_lanes(wb_decoder_t d, int32_t *lanes, int32_t *max_cluster) {
+    if (!d || !lanes || !max_cluster) return set_err(WB_ERR_VALUE, "null argument");
+    *lanes = d->slots;
+    *max_cluster = d->kmax;
     return WB_OK;
 }
 

@@ -285,6 +285,12 @@ class BatchDecoder:
             raise ValueError("the claim log overflowed (raise WB_CHECK_LOG)")
         return q, groups[:got.value]
 
+    def lanes(self) -> tuple[int, int]:
+        """(utterance lanes, largest cluster size the workspace allows)."""
+        a, b = C.c_int32(), C.c_int32()
+        N.check(self._L.wb_decoder_lanes(self._h, C.byref(a), C.byref(b)), "lanes", self._L)
+        return int(a.value), int(b.value)
+
     def last_cluster_ctas(self) -> int:
         """CTAs per utterance lane (thread-block cluster size) of the last launch."""
         k = C.c_int32()

@@ -108,3 +108,20 @@ def test_cluster_tie_heavy_radix(cuda):
     out = dec.decode_host(*_table(posts), cfg, "fsd")
     assert [_fields(r) for r in out.decode_results()] == _oracle(g, posts, cfg)
     assert (out.results["path_flags"] & N.WB_PATH_RADIX).any()
+
+
+def test_memory_budget_trades_lanes_for_clusters(cuda, monkeypatch):
+    """When the dense per-state arrays of one lane per SM would not fit (a large graph), the
+    decoder takes fewer lanes and fills the SMs with clusters; results are unchanged."""
+    g = synth.random_wfst(12, 200_000, 600_000, 30, eps_fraction=0.03, final_fraction=0.05)
+    posts = [synth.random_posteriors(60 + k, 40, 30) for k in range(90)]
+    cfg = P.DecodeConfig(beam=10.0, max_active=500, mode="fsd")
+    want = BatchDecoder(g, 0).decode_host(*_table(posts), cfg, "fsd").decode_results()
+    # one lane: 200k states x 24 B + a 32 MB arena ~ 37 MB; 148 lanes would need 5.5 GB
+    monkeypatch.setenv("WB_MEM_BUDGET_GB", "3.5")
+    dec = BatchDecoder(g, 0)
+    lanes, kmax = dec.lanes()
+    assert lanes <= 74 and kmax >= 2 and lanes * kmax <= 148
+    out = dec.decode_host(*_table(posts), cfg, "fsd")
+    assert dec.last_cluster_ctas() >= 2
+    assert out.decode_results() == want

@@ -72,3 +72,52 @@ def test_gloo_world2_gather_matches_single_process():
     posts = [synth.random_posteriors(i, 5 + 3 * i, 10) for i in range(9)]
     want = _oracle_decode(g, posts, DecodeConfig(beam=8.0, max_active=30, mode="fsd"))
     assert out[0] == want and out[1] == want
+
+
+def _gpu_worker(rank, world, port, q):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path[:0] = [root, os.path.join(root, "tests")]
+    import torch
+    import torch.distributed as dist
+    from paper_1808_00687_b200 import synth
+    from paper_1808_00687_b200.decoder import DecodeConfig
+    from paper_1808_00687_b200.shard import decode_sharded
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)   # one GPU here: both ranks decode on it (independent kernels)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = synth.random_wfst(3, 3000, 9000, 20, eps_fraction=0.05, final_fraction=0.1)
+        posts = [synth.random_posteriors(50 + i, 20 + 9 * i, 20) for i in range(11)]
+        cfg = DecodeConfig(beam=9.0, max_active=200, mode="fsd")
+        got = decode_sharded(g, posts, cfg)   # the real device decoder on each rank's shard
+        q.put((rank, [tuple(r.__dict__.values()) if hasattr(r, "__dict__") else r for r in got]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gloo_world2_device_decode_gather(cuda):
+    """Two ranks (processes) shard the utterances, each decodes its share with the B200
+    decoder, and the gloo gather gives every rank the full batch -- equal to the oracle."""
+    import socket
+    from oracle import oracle as O
+    from paper_1808_00687_b200 import synth
+    from paper_1808_00687_b200.posteriors import cost_table
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    g = synth.random_wfst(3, 3000, 9000, 20, eps_fraction=0.05, final_fraction=0.1)
+    posts = [synth.random_posteriors(50 + i, 20 + 9 * i, 20) for i in range(11)]
+    want = [O.decode(g, cost_table(p), p.rows[:, 0], beam=9.0, max_active=200,
+                     mode="fsd").astuple() for p in posts]
+    assert out[0] == want and out[1] == want
