@@ -545,6 +545,10 @@ class BatchDecoder:
                                                 C.byref(nf)), "lattice")
                     need_out = max(nn.value, na.value, nf.value)
                 self._grow(flags, lattice_out_need=need_out, max_frames=maxT)
+            if batch is not None:
+                # the batch's rows are costs now (converted in place): retry from the table
+                return self.decode_host(costs, off, T, blank, cfg, mode, cap, lattice,
+                                        lattice_beam)
             return self.decode_posteriors(posts_list, cfg, mode, cap, lattice, lattice_beam,
                                           block_frames, workers, _attempt + 1)
         self.check_report(n)

@@ -253,3 +253,16 @@ def test_posterior_batch_from_post1_files(cuda, tmp_path, mode):
         o = O.decode(g, P.cost_table(m), m.rows[:, m.blank_col], beam=10.0, max_active=300,
                      mode=mode)
         assert _fields(r) == o.astuple()
+
+
+def test_posterior_batch_capacity_retry(cuda, tmp_path):
+    """A PosteriorBatch's rows are converted in place; when a capacity overflows, the retry
+    decodes the converted table (not the rows a second time) and the results are exact."""
+    from paper_1808_00687_b200.decoder import BatchDecoder
+    from paper_1808_00687_b200.posteriors import PosteriorBatch
+    g = synth.random_wfst(62, 2000, 7000, 20, eps_fraction=0.05, final_fraction=0.1)
+    mats = [synth.random_posteriors(600 + k, 50, 20) for k in range(4)]
+    cfg = P.DecodeConfig(beam=9.0, max_active=150, mode="fsd")
+    tiny = BatchDecoder(g, 0, cand_capacity=16, arena_capacity=1024)
+    got = tiny.decode_posteriors(PosteriorBatch(mats), cfg).decode_results()
+    assert got == P.decode_batch(g, mats, cfg)
