@@ -462,10 +462,10 @@ def main():
             e_ms = e_ev[0][0].elapsed_time(e_ev[-1][1])
             # lattice output: the batch's pruned lattices as text through the
             # native writer (format_lattice_text, byte-identical to the reference's)
-            from paper_1808_00687_b200.lattice import format_lattice_text
+            from paper_1808_00687_b200.lattice import format_lattices_text
             t0 = time.perf_counter()
-            text_bytes = sum(len(format_lattice_text(p)) for p in lats
-                             if not isinstance(p, LatticeError))
+            text_bytes = sum(len(t) for t in format_lattices_text(
+                [p for p in lats if not isinstance(p, LatticeError)]))
             lat_stats["text_ms"] = 1e3 * (time.perf_counter() - t0)
             lat_stats["text_bytes"] = text_bytes
         else:

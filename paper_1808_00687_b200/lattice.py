@@ -629,6 +629,19 @@ def format_lattice_text(lat: Lattice) -> str:
         L.wb_text_free(ptr)
 
 
+def format_lattices_text(lats, workers: int | None = None) -> list[str]:
+    """``format_lattice_text`` of many lattices on host threads (the native writer runs
+    without the GIL)."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    lats = list(lats)
+    n = workers or min(len(lats), len(os.sched_getaffinity(0))) or 1
+    if n <= 1:
+        return [format_lattice_text(x) for x in lats]
+    with ThreadPoolExecutor(n) as ex:
+        return list(ex.map(format_lattice_text, lats))
+
+
 def parse_lattice_text(text: str) -> Lattice:
     """Inverse of ``format_lattice_text`` (native reader); ``LatticeError`` for malformed
     text, ``ValueError`` for a bad number, as the reference raises them."""
@@ -658,7 +671,7 @@ def load_lattice(path: str) -> Lattice:
 
 
 __all__ = ["COST_EPS", "EMPTY_LATTICE", "Lattice", "LatticeArc", "LatticeError", "LatticeNode",
-           "LatticeRecorder", "PipelinedLatticeBuilder", "StepRecord", "build_lattice", "replay", "canonical_batch", "canonical_from_device", "format_lattice_text",
+           "LatticeRecorder", "PipelinedLatticeBuilder", "StepRecord", "build_lattice", "replay", "canonical_batch", "canonical_from_device", "format_lattice_text", "format_lattices_text",
            "lattice_best_path", "load_lattice", "parse_lattice_text", "prune_lattice", "prune_lattices",
            "split_lattice",
            "save_lattice"]
