@@ -169,7 +169,7 @@ struct Smem {
     u32 wa[NW + 1], wb[NW + 1];
     u64 r0[NW], r1[NW];
     long long rl[NW];
-    int n_cand, n_front, overflow, utt, tag_round, ng, thr_bucket, thr_below, n_pend;
+    int n_cand, overflow, utt, ng, thr_bucket, thr_below, n_pend;
     int flag, lat_bad;  // lattice sweeps: change flag / output-pool overflow
     int n_log;          // relaxations logged this step (lattice mode)
     u64 run_min;        // smallest emitting relaxation key seen so far this step
@@ -181,12 +181,12 @@ struct Smem {
     // after a cluster barrier
     int nfr[2];         // epsilon frontier entries pushed for round parity 0 / 1
     u64 x_mn, x_mx;     // this CTA's candidate key min / max (prune)
-    long long x_sum;    // this CTA's partial sum of a cluster reduction
     int x_n, x_flags;   // this CTA's candidates this step; bit 0 overflow, bit 1 keys in global
     int x_gn;           // rank 0: boundary-bucket members collected from the lane's CTAs
-    u32 x_gmask;        // rank 0: CTAs whose candidate flags live in global memory this step
     int x_stream;       // this CTA timed out waiting for a streamed cost row (cluster lanes)
     long long chk_off;  // checked build: this step's offset in the lane's claim log
+    u32 ls_flag[8];     // lane barrier: epoch of the last barrier each peer CTA arrived at
+    u32 ls_epoch;       // lane barriers passed by this CTA
     int x_ck, x_cs;     // kept / surviving candidates of this CTA (compaction bases)
     u64 x_run_min;      // this CTA's exact emitting minimum (expand)
     long long x_cnt[4]; // per-CTA counters summed at the utterance end
@@ -238,7 +238,7 @@ __device__ __forceinline__ void tick(int ph) {
     }
 }
 
-// ------------------------------------------------------------------ cluster lanes
+// ------------------------------------------------------------------ cluster lanes (see below)
 // With K > 1 an utterance lane is a thread-block cluster: the K CTAs (on K SMs of one GPC)
 // split every per-step phase and meet at cluster barriers; per-CTA partial results are read
 // by the others straight from their shared memory (DSMEM, mapa).  K == 1 is the plain CTA.
@@ -247,18 +247,24 @@ __device__ __forceinline__ int cta_rank() {
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
     return (int)r;
 }
-// Every thread of every CTA of the lane; release/acquire at cluster scope, so global and
-// shared writes before it are visible to all CTAs of the lane after it.
-__device__ __forceinline__ void lane_sync(int K) {
-    if (K > 1)
-        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    else
-        __syncthreads();
+// The hardware cluster barrier with acquire semantics (barrier.cluster.wait) invalidates the
+// whole L1 (CCTL.IVALL): spilled registers, cached arc records and token data all miss
+// afterwards.  Used once, at kernel start; the per-phase barriers are lane_sync below.
+__device__ __forceinline__ void cluster_sync_full() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 // The same shared-memory object in CTA `rank` of this cluster (generic address into DSMEM).
 template <class T>
 __device__ __forceinline__ T *peer(T *p, int rank) {
     return cooperative_groups::this_cluster().map_shared_rank(p, (unsigned)rank);
+}
+
+// Loads of global data another CTA of the lane wrote in an earlier phase: L2 (the per-phase
+// lane barrier does not invalidate this SM's L1).  Plain loads with one CTA per lane.
+template <int KC, class T>
+__device__ __forceinline__ T ldx(const T *p) {
+    if constexpr (KC > 1) return __ldcg(p);
+    else return *p;
 }
 
 // ------------------------------------------------------------------ checked build
@@ -280,6 +286,33 @@ enum : int {
 __device__ __noinline__ void check_fail(const WorkDev &ws, int code, int line) {
     atomicCAS(&ws.chk_err[blockIdx.x >> ws.kshift], 0ull,
               ((unsigned long long)code << 32) | (unsigned)line);
+}
+
+// Barrier of every thread of every CTA of a lane.  With K > 1: a flag handshake through
+// distributed shared memory between the CTAs' thread 0s, bracketed by CTA barriers, instead of
+// barrier.cluster (whose acquire invalidates L1).  `global`: each thread first releases its
+// global-memory writes (fence.release, MEMBAR.GPU without an L1 invalidation); the readers of
+// such data in other CTAs load it from L2 (ldx).  Shared-memory data needs no fence: it is
+// read in place through DSMEM after the handshake.
+template <int BLOCK>
+__device__ __forceinline__ void lane_sync(int K, bool global = true) {
+    if (K == 1) {
+        __syncthreads();
+        return;
+    }
+    if (global) asm volatile("fence.release.cluster;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Smem<BLOCK> &sh = SH<BLOCK>();
+        const u32 e = ++sh.ls_epoch;
+        const int r = cta_rank();
+        for (int q = 0; q < K; ++q)
+            if (q != r) *(volatile u32 *)&peer(&sh, q)->ls_flag[r] = e;
+        for (int q = 0; q < K; ++q)
+            if (q != r)
+                while ((int)(*(volatile u32 *)&sh.ls_flag[q] - e) < 0) { }
+    }
+    __syncthreads();
 }
 
 // ------------------------------------------------------------------ block primitives
@@ -457,8 +490,8 @@ __device__ __forceinline__ void pilot_min(int bt, int cur, const double *row, co
                                           const WorkDev &ws) {
     const Lane c{ws};
     const int l = threadIdx.x & 31;
-    const int4 ti = c.tok_info(cur)[bt];
-    const double tc = c.tok_cost(cur)[bt];
+    const int4 ti = __ldcg(&c.tok_info(cur)[bt]);   // possibly written by another CTA of the lane
+    const double tc = __ldcg(&c.tok_cost(cur)[bt]);
     u64 m = EMPTY_KEY;
     for (int a = ti.z + l; a < ti.w; a += 32) {
         const int4 r = ld_arc(&g.arcs[2 * a]);
@@ -622,7 +655,7 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
 #pragma unroll
                   for (int q = 0; q < 2; ++q) {
                     const int t = (chunk_of(ch0 + q * NW) << 5) + l;
-                    tcs[q] = (ch0 + q * NW < nchunks && t < n_live) ? tcost[t] : INFINITY;
+                    tcs[q] = (ch0 + q * NW < nchunks && t < n_live) ? ldx<KC>(&tcost[t]) : INFINITY;
                   }
 #pragma unroll
                   for (int q = 0; q < 2; ++q) {
@@ -631,7 +664,7 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
                     const bool pass = tc < bound && t != bt;
                     if (!__any_sync(FULL, pass)) continue;
                     int4 ti = make_int4(0, 0, 0, 0);
-                    if (pass) ti = tinfo[t];
+                    if (pass) ti = ldx<KC>(&tinfo[t]);
                     const int deg = pass ? ti.w - ti.z : 0;
                     const int incl = warp_incl_scan(deg);
                     const int total = __shfl_sync(FULL, incl, 31);
@@ -656,7 +689,7 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
                 if (l == 0 && m < sh_run_min()) atomicMin(reinterpret_cast<unsigned long long *>(&SH<BLOCK>().run_min), m);
                 // a cluster lane's CTAs each saw their own tokens: the lane's exact minimum is
                 // the minimum over the CTAs (run_min is not written again this step)
-                lane_sync(KC);
+                lane_sync<BLOCK>(KC, false);   // run_min: shared memory only
                 if (KC > 1) {
                     u64 lm = sh_run_min();
                     for (int q = 1; q < KC; ++q) {
@@ -706,7 +739,7 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
             const int t = (ch << 5) + l;
             int4 ti = make_int4(0, 0, 0, 0);
             double tc = 0.0;
-            if (t < n_live) { ti = tinfo[t]; tc = tcost[t]; }
+            if (t < n_live) { ti = ldx<KC>(&tinfo[t]); tc = ldx<KC>(&tcost[t]); }
             const bool in_pass = !ma_on || ((tc <= split) == (pass == 0));
             const int deg = (t < n_live && in_pass) ? ti.w - ti.z : 0;
 #ifdef WB_CHECKS
@@ -802,7 +835,7 @@ __noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const 
         int t = (ch << 5) + l;
         int4 ti = make_int4(0, 0, 0, 0);
         double tc = 0.0;
-        if (t < n_live) { ti = tinfo[t]; tc = tcost[t]; }
+        if (t < n_live) { ti = ldx<KC>(&tinfo[t]); tc = ldx<KC>(&tcost[t]); }
         int deg = t < n_live ? ti.w - ti.z : 0;
 #ifdef WB_CHECKS
         if (t < n_live) claim_token<BLOCK>(ws, t, r * NW + w);
@@ -950,7 +983,7 @@ __noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev 
                 uu = fin[i];
                 const int4 fe = frin[i];
                 Slot us = ld_slot(&slot[uu]);
-                ui = fe.x >= 0 ? (u32)fe.x : min(c.cand_of()[uu], (u32)ws.lcap - 1u);
+                ui = fe.x >= 0 ? (u32)fe.x : min(ldx<KC>(&c.cand_of()[uu]), (u32)ws.lcap - 1u);
                 lo = fe.y;
                 deg = fe.z - fe.y;
                 ucost = key_cost(us.key);
@@ -1010,7 +1043,7 @@ __noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev 
                 }
             }
         }
-        lane_sync(K);
+        lane_sync<BLOCK>(K);
     }
     return EpsOut{tag_cur, e_eps, status, n_rounds};
 }
@@ -1042,7 +1075,7 @@ __noinline__ __device__ Thr select_threshold(int n_loc, int max_active, double b
     constexpr int K = KC;
     const int r = K > 1 ? cta_rank() : 0;
     Smem<BLOCK> &s0 = K > 1 ? *peer(&sh, 0) : sh;   // rank 0's header (itself when K == 1)
-    if (K > 1) lane_sync(K);                         // every CTA's histogram is complete
+    if (K > 1) lane_sync<BLOCK>(K, false);                         // every CTA's histogram is complete
     if (r == 0) {
         if (threadIdx.x == 0) sh.thr_bucket = -1;   // stays -1: max-active does not bind
         u32 loc[PER];
@@ -1076,7 +1109,7 @@ __noinline__ __device__ Thr select_threshold(int n_loc, int max_active, double b
         }
         if (threadIdx.x == 0) sh.x_gn = 0;   // boundary members collected below
     }
-    lane_sync(K);
+    lane_sync<BLOCK>(K, false);
     const int bstar = s0.thr_bucket;
     if (bstar < 0) return Thr{-1, 0, 0};  // at most max_active candidates within the beam
     if (r == 0 && threadIdx.x == 0) sh.pflags |= WB_PATH_SELECT;
@@ -1092,7 +1125,7 @@ __noinline__ __device__ Thr select_threshold(int n_loc, int max_active, double b
                 s0.u.g.st[q] = cst[j];
             }
         }
-        lane_sync(K);
+        lane_sync<BLOCK>(K, false);
         if (r == 0) {
             const int m = sh.x_gn;
             for (int j = threadIdx.x; j < m; j += BLOCK) {
@@ -1106,7 +1139,7 @@ __noinline__ __device__ Thr select_threshold(int n_loc, int max_active, double b
                 if (rank == rk - 1) { sh.thr_key = kj; sh.thr_state = sj; }
             }
         }
-        lane_sync(K);
+        lane_sync<BLOCK>(K, false);
         // rank 0 writes thr_key / thr_state again only in the next step's select, many lane
         // barriers after these reads
         return Thr{bstar, s0.thr_key, s0.thr_state};
@@ -1130,7 +1163,7 @@ __noinline__ __device__ Thr select_threshold(int n_loc, int max_active, double b
             const u32 d = in_key ? (u32)((k >> shift) & 0xFF) : ((st >> shift) & 0xFF);
             atomicAdd(&sh.u.hist[d], 1u);
         }
-        lane_sync(K);
+        lane_sync<BLOCK>(K, false);
         if (r == 0 && threadIdx.x == 0) {
             u32 acc = 0;
             int d = 0;
@@ -1143,12 +1176,12 @@ __noinline__ __device__ Thr select_threshold(int n_loc, int max_active, double b
             sh.thr_below = (int)acc;
             sh.ng = d;
         }
-        lane_sync(K);
+        lane_sync<BLOCK>(K, false);
         rk -= s0.thr_below;
         const u32 d = (u32)s0.ng;
         if (in_key) { kpre |= (u64)d << shift; kmask |= 0xFFull << shift; }
         else { spre |= d << shift; smask |= 0xFFu << shift; }
-        lane_sync(K);   // rank 0 rewrites thr_below / ng for the next digit
+        lane_sync<BLOCK>(K, false);   // rank 0 rewrites thr_below / ng for the next digit
     }
     return Thr{bstar, kpre, spre};
 }
@@ -1237,7 +1270,7 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
             if (mx != 0ull) atomicMax(reinterpret_cast<unsigned long long *>(&sh.x_mx), mx);
         }
         if (threadIdx.x == 0) { sh.x_n = n_loc; sh.x_flags = flags; }
-        lane_sync(K);
+        lane_sync<BLOCK>(K);
         mn = *(volatile u64 *)&sh.x_mn;
         mx = *(volatile u64 *)&sh.x_mx;
         for (int q = 1; q < K; ++q) {
@@ -1254,7 +1287,7 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
     }
     int status = (flags & 4) ? wb_cap(WB_CAP_STREAM) : (flags & 1) ? wb_cap(WB_CAP_CANDIDATES) : WB_OK;
     tick<BLOCK>(3);
-    if (n_all == 0) { lane_sync(K); return StepOut{0, 0, status, 0}; }
+    if (n_all == 0) { lane_sync<BLOCK>(K); return StepOut{0, 0, status, 0}; }
     const double best = key_cost(mn);
     const double cutoff = __dadd_rn(best, cfg.beam);  // cutoff = best + beam (decoder.py:186)
 
@@ -1311,7 +1344,7 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
         if (!g.has_eps) continue;
         u32 v = (u32)(cbase + i);
         for (;;) {
-            u32 a = c.cand_arc()[v], p = c.cand_pay()[v];
+            u32 a = ldx<KC>(&c.cand_arc()[v]), p = ldx<KC>(&c.cand_pay()[v]);
             if (a == 0u || !(p & EPS_BIT)) break;
             u32 uix = p & ~EPS_BIT;
             u32 old = atomicOr(flag_of(uix), F_MARK);
@@ -1319,7 +1352,7 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
             v = uix;
         }
     }
-    lane_sync(K);
+    lane_sync<BLOCK>(K);
     tick<BLOCK>(5);
 
     // P4: order-preserving compaction of kept candidates (arena records) and survivors
@@ -1344,7 +1377,7 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
         if (l < NW) { sh.wa[l] = ia - va; sh.wb[l] = ib - vb; }
         if (l == 31) { sh.wa[NW] = ia; sh.wb[NW] = ib; sh.x_ck = ia; sh.x_cs = ib; }
     }
-    lane_sync(K);
+    lane_sync<BLOCK>(K, false);
     int keep_before = 0, surv_before = 0, n_keep = (int)sh.wa[NW], n_surv = (int)sh.wb[NW];
     for (int q = 1; q < K; ++q) {
         const int o = (r + q) & (K - 1);
@@ -1358,7 +1391,7 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
     {
         const u64 used = sh.arena_used + (u64)n_keep;
         if (used > ws.arena_cap || used >= (u64)EPS_BIT) {
-            lane_sync(K);
+            lane_sync<BLOCK>(K);
             return StepOut{0, 0, wb_cap(WB_CAP_ARENA), n_all};
         }
     }
@@ -1423,7 +1456,7 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
         }
     }
     // epsilon winners resolve their source's record index, possibly another CTA's
-    if (g.has_eps) lane_sync(K);
+    if (g.has_eps) lane_sync<BLOCK>(K);
 #ifdef WB_CHECKS
     // debug_epoch analogue: every slot this step touched is EMPTY again (no relaxation of
     // this step can leak into the next); registration counters are cleared for the next step
@@ -1441,7 +1474,7 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
         const u32 src = *(volatile u32 *)flag_of(p & ~EPS_BIT);
         c.arena()[vca[i]] = (u64)a | ((u64)src << 32);
     }
-    lane_sync(K);   // next tokens / records complete in every CTA of the lane
+    lane_sync<BLOCK>(K);   // next tokens / records complete in every CTA of the lane
     tick<BLOCK>(6);
     return StepOut{n_surv, n_keep, status, n_all};
 }
@@ -1904,13 +1937,18 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
     const int rank = K > 1 ? cta_rank() : 0;
     const int slot_id = (int)c.lane();
     u32 tag = ws.tag_ctr[slot_id];
+    if (K > 1) {   // lane-barrier flags are zero in every CTA before any peer writes one
+        if (threadIdx.x < 8) sh.ls_flag[threadIdx.x] = 0u;
+        if (threadIdx.x == 0) sh.ls_epoch = 0u;
+        cluster_sync_full();
+    }
     const bool row_in_smem = ws.row_in_smem != 0;
     const bool pilot_on = g.nonneg && cfg.beam < INFINITY && ws.beam_skip && ws.stage_off;
     double *srow = s_row<BLOCK>();
 
     for (;;) {
         if (rank == 0 && threadIdx.x == 0) sh.utt = (int)atomicAdd(ws.utt_ctr, 1u);
-        lane_sync(K);
+        lane_sync<BLOCK>(K);
         const int u = K > 1 ? peer(&sh, 0)->utt : sh.utt;
         if (u >= b.n) break;
         if (threadIdx.x < 8) sh.pc[threadIdx.x] = 0;
@@ -1942,7 +1980,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             sh.overflow = 0;
             sh.nfr[0] = sh.nfr[1] = 0;
             sh.x_stream = 0;
-            sh.x_mn = EMPTY_KEY; sh.x_mx = 0; sh.x_n = 0; sh.x_flags = 0; sh.x_gmask = 0;
+            sh.x_mn = EMPTY_KEY; sh.x_mx = 0; sh.x_n = 0; sh.x_flags = 0;
             if (rank == 0) {
                 u64 k0 = cost_key(0.0);
                 __stcg(reinterpret_cast<ulonglong2 *>(&c.slot()[g.start]),
@@ -1957,7 +1995,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
                 }
             }
         }
-        lane_sync(K);
+        lane_sync<BLOCK>(K);
         if (g.has_eps) {
             EpsOut eo = epsilon_closure<BLOCK, KC>(g, ws, tag, cfg.beam);
             tag = eo.tag;
@@ -1980,7 +2018,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
         int steps_run = 0, died_at = -1;
         long long expanded = 0;
         for (int s = 0; s < nf && status == WB_OK; ++s) {
-            const int f = cfg.mode == 1 ? c.frames()[s] : s;
+            const int f = cfg.mode == 1 ? ldx<KC>(&c.frames()[s]) : s;
             const int ridx = b.crow_off ? s : f;  // compacted rows are indexed by search step
             const double *grow = b.costs + (size_t)((b.crow_off ? b.crow_off[u] : row0) + ridx) * b.L1;
             const double *row = grow;
@@ -2012,13 +2050,17 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
                     if (threadIdx.x == 0) { sh.x_stream = 1; sh.ready_seen = 0; }
                 }
             }
+#ifdef WB_PROBE
+            __syncthreads();
+            tick<BLOCK>(7);   // probe build: loop overhead / row wait before the staging phase
+#endif
             int neg = !row_in_smem;  // acoustic costs of this row all >= 0? (checked while staging)
             if (threadIdx.x == 0) {
                 sh.n_cand = 0; sh.nfr[0] = sh.nfr[1] = 0; sh.overflow = 0; sh.n_log = 0;
                 sh.run_min = EMPTY_KEY;
                 sh.next_chunk = BLOCK / 32;
-                // rank 0's lane accumulators of this step's prune (read after many barriers)
-                sh.x_mn = EMPTY_KEY; sh.x_mx = 0; sh.x_n = 0; sh.x_flags = 0; sh.x_gmask = 0;
+                // this CTA's prune accumulators (peers read them after the prune's barrier)
+                sh.x_mn = EMPTY_KEY; sh.x_mx = 0; sh.x_n = 0; sh.x_flags = 0;
             }
             // Pilot of the beam skip (expand_emitting): warp 0 evaluates the arcs of a cheapest
             // live token against the row in global memory while the other warps stage it.
@@ -2041,7 +2083,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             if (ws.row_prefetch && s + 1 < nf) {
                 // the next step's row into L2 while this step searches (its staging then hits
                 // L2 instead of DRAM): one 128-byte line per thread
-                const int fn = cfg.mode == 1 ? c.frames()[s + 1] : s + 1;
+                const int fn = cfg.mode == 1 ? ldx<KC>(&c.frames()[s + 1]) : s + 1;
                 const double *nrow = b.costs + (size_t)(row0 + fn) * b.L1;
                 for (int q = threadIdx.x * 16; q < b.L1; q += BLOCK * 16)
                     asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + q));
@@ -2054,12 +2096,12 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             a_emit += ec.a_emit;
             a_fin += ec.a_fin;
             a_cas += ec.a_cas;
-            lane_sync(K);   // every CTA's relaxations have landed in the lane's slots
+            lane_sync<BLOCK>(K);   // every CTA's relaxations have landed in the lane's slots
 #ifdef WB_CHECKS
             {   // every live token of the step was expanded by exactly one group
                 u32 *cl = ws.chk_claim + c.lane() * ws.lcap;
                 for (int t = threadIdx.x + rank * BLOCK; t < n_live; t += BLOCK * K) {
-                    WB_CHECK(ws, cl[t] == 1u, CHK_CLAIM);
+                    WB_CHECK(ws, ldx<KC>(&cl[t]) == 1u, CHK_CLAIM);
                     cl[t] = 0u;
                 }
                 if (rank == 0 && threadIdx.x == 0 && s <= ws.T_cap)
@@ -2097,7 +2139,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
         }
 #ifdef WB_CHECKS
         if (status == WB_OK) {   // the whole slot array is clean between utterances
-            lane_sync(K);
+            lane_sync<BLOCK>(K);
             const Slot *sl = c.slot();
             for (long long q = threadIdx.x + (long long)rank * BLOCK; q < ws.S; q += (long long)BLOCK * K)
                 WB_CHECK(ws, ld_slot(&sl[q]).key == EMPTY_KEY, CHK_STALE_UTT);
@@ -2106,7 +2148,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
         if (status != WB_OK) {
             // a failed step may leave slots beyond the candidate capacity dirty: restore the
             // lane's whole slot array so later utterances on this lane start clean
-            lane_sync(K);
+            lane_sync<BLOCK>(K);
             Slot *sl = c.slot();
             for (long long q = threadIdx.x + (long long)rank * BLOCK; q < ws.S; q += (long long)BLOCK * K)
                 st_slot_empty(&sl[q]);
@@ -2120,7 +2162,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             if (threadIdx.x == 0) {
                 sh.x_cnt[0] = t_emit; sh.x_cnt[1] = t_fin; sh.x_cnt[2] = t_cas; sh.x_cnt[3] = t_eps;
             }
-            lane_sync(K);
+            lane_sync<BLOCK>(K, false);
             if (rank == 0)
                 for (int q = 1; q < K; ++q) {
                     const Smem<BLOCK> *po = peer(&sh, q);
@@ -2143,16 +2185,16 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             u32 st = 0xFFFFFFFFu;
             int idx = -1;
             for (int t = threadIdx.x; t < n_live; t += BLOCK) {
-                int s = tinfo[t].x;
+                int s = ldx<KC>(&tinfo[t]).x;
                 double fw = __ldg(&g.final_w[s]);
                 if (fw == INFINITY) continue;
-                u64 kk = cost_key(__dadd_rn(tcost[t], fw));
+                u64 kk = cost_key(__dadd_rn(ldx<KC>(&tcost[t]), fw));
                 if (kk < k || (kk == k && (u32)s < st)) { k = kk; st = (u32)s; idx = t; }
             }
             best_t = block_argmin_tok<BLOCK>(k, st, idx);
             if (best_t >= 0) {
                 reached = 1;
-                best_cost = __dadd_rn(tcost[best_t], __ldg(&g.final_w[tinfo[best_t].x]));
+                best_cost = __dadd_rn(ldx<KC>(&tcost[best_t]), __ldg(&g.final_w[ldx<KC>(&tinfo[best_t]).x]));
             }
         }
         if (best_t < 0) {
@@ -2160,12 +2202,12 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             u32 st = 0xFFFFFFFFu;
             int idx = -1;
             for (int t = threadIdx.x; t < n_live; t += BLOCK) {
-                u64 kk = cost_key(tcost[t]);
-                u32 s = (u32)tinfo[t].x;
+                u64 kk = cost_key(ldx<KC>(&tcost[t]));
+                u32 s = (u32)ldx<KC>(&tinfo[t]).x;
                 if (kk < k || (kk == k && s < st)) { k = kk; st = s; idx = t; }
             }
             best_t = block_argmin_tok<BLOCK>(k, st, idx);
-            if (best_t >= 0) best_cost = tcost[best_t];
+            if (best_t >= 0) best_cost = ldx<KC>(&tcost[best_t]);
         }
         if (cfg.lattice) {
             const int fstep = died_at < 0 ? steps_run : died_at;
@@ -2188,9 +2230,9 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             r.search_steps = steps_run;
             r.reached_final = reached;
             r.died_at_step = died_at;
-            r.final_state = best_t >= 0 ? tinfo[best_t].x : -1;
+            r.final_state = best_t >= 0 ? ldx<KC>(&tinfo[best_t]).x : -1;
             r.final_step = died_at < 0 ? steps_run : died_at;
-            r.best_trace = best_t >= 0 ? (long long)(u32)tinfo[best_t].y : -1;
+            r.best_trace = best_t >= 0 ? (long long)(u32)ldx<KC>(&tinfo[best_t]).y : -1;
             if (status == WB_OK)  // a failed utterance's tokens / arena are not a valid chain
                 backtrace(g, c.arena(), r.best_trace, sh.arena_used, b.olab + (size_t)u * b.lab_cap,
                           b.ilab + (size_t)u * b.lab_cap, b.lab_cap, &r.n_olabels, &r.n_ilabels);
@@ -2218,7 +2260,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
     }
     if (rank == 0 && threadIdx.x == 0) ws.tag_ctr[slot_id] = tag;
     // no CTA of a cluster may exit while another can still read its shared memory
-    if (K > 1) lane_sync(K);
+    if (K > 1) lane_sync<BLOCK>(K, false);
 }
 
 }  // namespace wb

@@ -43,7 +43,9 @@ while time.time() < t_end:
                          blank_threshold=float(rng.choice([0.98, 0.5])))
     lattice = rng.random() < 0.5
     lb = float(rng.choice([0.0, 1.0, 4.0, np.inf]))
-    dec = BatchDecoder(g, 0)
+    # WB_STRESS_CLUSTER=1: random cluster size per batch (lattice batches run one CTA per lane)
+    K = int(rng.choice([1, 2, 4, 8])) if os.environ.get("WB_STRESS_CLUSTER") == "1" else 0
+    dec = BatchDecoder(g, 0, cluster_ctas=K)
     costs = [P.cost_table(p) for p in posts]
     T = np.asarray([len(c) for c in costs], np.int32)
     off = np.zeros(n, np.int64)
