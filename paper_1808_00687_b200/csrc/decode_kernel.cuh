@@ -189,7 +189,10 @@ struct Smem {
     u32 ls_epoch;       // lane barriers passed by this CTA
     int x_ck, x_cs;     // kept / surviving candidates of this CTA (compaction bases)
     u64 x_run_min;      // this CTA's exact emitting minimum (expand)
-    long long x_cnt[4]; // per-CTA counters summed at the utterance end
+    // per-utterance counters kept out of the step loop's registers (with the 64-register
+    // budget every value live across the phase calls was spilled around each call)
+    unsigned long long cnt[4];  // a_emit, a_fin, a_cas, e_eps: warp-aggregated shared atomics
+    long long acc[5];           // thread 0: tokens expanded, candidates, survivors, records, eps rounds
     double tok_lo, tok_hi;  // cost range of the current live tokens (from the last prune)
     float ma_frac;          // max-active early cutoff: split point in [tok_lo, tok_hi]
     u64 ma_thr;             // its bound key for the step
@@ -337,6 +340,15 @@ __device__ __forceinline__ void block_minmax(u64 &mn, u64 &mx) {
     __syncthreads();
 }
 
+template <int BLOCK>
+__device__ __forceinline__ void count_add(int q, u32 v) {
+    v = __reduce_add_sync(FULL, v);   // one shared atomic per warp
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&SH<BLOCK>().cnt[q], (unsigned long long)v);
+}
+template <int BLOCK>
+__device__ __forceinline__ void acc_add(int q, long long v) {
+    if (threadIdx.x == 0) SH<BLOCK>().acc[q] += v;
+}
 template <int BLOCK>
 __device__ __forceinline__ long long block_sum(long long v) {
     Smem<BLOCK> &sh = SH<BLOCK>();
@@ -1952,6 +1964,8 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
         const int u = K > 1 ? peer(&sh, 0)->utt : sh.utt;
         if (u >= b.n) break;
         if (threadIdx.x < 8) sh.pc[threadIdx.x] = 0;
+        if (threadIdx.x < 4) sh.cnt[threadIdx.x] = 0ull;
+        if (threadIdx.x < 5) sh.acc[threadIdx.x] = 0ll;
         if (threadIdx.x == 0) {
             sh.t_mark = clock64(); sh.arena_used = 0; sh.ready_seen = 0; sh.run_min = EMPTY_KEY;
             sh.pflags = ws.stage_off ? WB_PATH_PREFETCH : 0;
@@ -1962,8 +1976,6 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
         const int T = b.T[u];
         const long long row0 = b.row_off[u];
         int status = WB_OK;
-        u32 a_emit = 0, a_fin = 0, a_cas = 0, e_eps = 0;  // per-thread counters
-        long long n_tok = 0, n_cand_tot = 0, n_surv_tot = 0, n_rec = 0, eps_rounds = 0;
         int nf = T;
         if (cfg.mode == 1) {
             if (T > ws.T_cap) {  // frame list would overflow: report, do not decode
@@ -1999,24 +2011,23 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
         if (g.has_eps) {
             EpsOut eo = epsilon_closure<BLOCK, KC>(g, ws, tag, cfg.beam);
             tag = eo.tag;
-            e_eps += eo.e_eps;
+            count_add<BLOCK>(3, eo.e_eps);
             if (eo.status) status = eo.status;
-            eps_rounds += eo.rounds;
+            acc_add<BLOCK>(4, eo.rounds);
         }
         int cur = 0;
         StepOut so = finish_step<BLOCK, KC>(cur, g, ws, cfg);
-        n_cand_tot += so.n_cand;
+        acc_add<BLOCK>(1, so.n_cand);
         if (so.status) status = so.status;
-        n_rec += so.n_keep;
+        acc_add<BLOCK>(3, so.n_keep);
         long long lat_arcs = 0;
         if (cfg.lattice && status == WB_OK) {
             const int rs = record_lattice_step<BLOCK>(0, cur, so.n_surv, 0, 0, nullptr, 0, g, ws);
             if (rs) status = rs;
         }
         int n_live = so.n_surv;
-        n_surv_tot += n_live;
+        acc_add<BLOCK>(2, n_live);
         int steps_run = 0, died_at = -1;
-        long long expanded = 0;
         for (int s = 0; s < nf && status == WB_OK; ++s) {
             const int f = cfg.mode == 1 ? ldx<KC>(&c.frames()[s]) : s;
             const int ridx = b.crow_off ? s : f;  // compacted rows are indexed by search step
@@ -2089,13 +2100,14 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
                     asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + q));
             }
             tick<BLOCK>(0);
-            expanded += n_live;
-            n_tok += n_live;
-            ExpandCounts ec = expand_emitting<BLOCK, KC>(n_live, cur, row, g, ws, cfg.beam, row_nonneg, pilot,
-                                                    cfg.max_active);
-            a_emit += ec.a_emit;
-            a_fin += ec.a_fin;
-            a_cas += ec.a_cas;
+            acc_add<BLOCK>(0, n_live);
+            {
+                ExpandCounts ec = expand_emitting<BLOCK, KC>(n_live, cur, row, g, ws, cfg.beam, row_nonneg,
+                                                             pilot, cfg.max_active);
+                count_add<BLOCK>(0, ec.a_emit);
+                count_add<BLOCK>(1, ec.a_fin);
+                count_add<BLOCK>(2, ec.a_cas);
+            }
             lane_sync<BLOCK>(K);   // every CTA's relaxations have landed in the lane's slots
 #ifdef WB_CHECKS
             {   // every live token of the step was expanded by exactly one group
@@ -2114,21 +2126,21 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             if (g.has_eps) {
                 EpsOut eo = epsilon_closure<BLOCK, KC>(g, ws, tag, cfg.beam);
                 tag = eo.tag;
-                e_eps += eo.e_eps;
+                count_add<BLOCK>(3, eo.e_eps);
                 if (eo.status) status = eo.status;
-            eps_rounds += eo.rounds;
+                acc_add<BLOCK>(4, eo.rounds);
             }
             tick<BLOCK>(2);
             so = finish_step<BLOCK, KC>(cur ^ 1, g, ws, cfg);
-            n_cand_tot += so.n_cand;
+            acc_add<BLOCK>(1, so.n_cand);
             if (so.status) status = so.status;
-            n_rec += so.n_keep;
+            acc_add<BLOCK>(3, so.n_keep);
             steps_run++;
             if (so.n_surv == 0) {
                 died_at = s;
                 break;
             }
-            n_surv_tot += so.n_surv;
+            acc_add<BLOCK>(2, so.n_surv);
             if (cfg.lattice && status == WB_OK) {
                 const int rs = record_lattice_step<BLOCK>(s + 1, cur ^ 1, so.n_surv, cur, n_live, grow,
                                                           b.L1, g, ws);
@@ -2153,25 +2165,17 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             for (long long q = threadIdx.x + (long long)rank * BLOCK; q < ws.S; q += (long long)BLOCK * K)
                 st_slot_empty(&sl[q]);
         }
-        long long t_emit = block_sum<BLOCK>(a_emit);
-        long long t_fin = block_sum<BLOCK>(a_fin);
-        long long t_cas = block_sum<BLOCK>(a_cas);
-        long long t_eps = block_sum<BLOCK>(e_eps);
+        if (K > 1) lane_sync<BLOCK>(K, false); else __syncthreads();
+        long long t_emit = (long long)sh.cnt[0], t_fin = (long long)sh.cnt[1];
+        long long t_cas = (long long)sh.cnt[2], t_eps = (long long)sh.cnt[3];
         int pflags = sh.pflags;
-        if (K > 1) {   // rank 0 reports the lane: sum the other CTAs' counters
-            if (threadIdx.x == 0) {
-                sh.x_cnt[0] = t_emit; sh.x_cnt[1] = t_fin; sh.x_cnt[2] = t_cas; sh.x_cnt[3] = t_eps;
+        if (K > 1 && rank == 0) {   // rank 0 reports the lane: sum the other CTAs' counters
+            for (int q = 1; q < K; ++q) {
+                const Smem<BLOCK> *po = peer(&sh, q);
+                t_emit += (long long)po->cnt[0]; t_fin += (long long)po->cnt[1];
+                t_cas += (long long)po->cnt[2]; t_eps += (long long)po->cnt[3];
+                pflags |= po->pflags;
             }
-            lane_sync<BLOCK>(K, false);
-            if (rank == 0)
-                for (int q = 1; q < K; ++q) {
-                    const Smem<BLOCK> *po = peer(&sh, q);
-                    t_emit += po->x_cnt[0]; t_fin += po->x_cnt[1]; t_cas += po->x_cnt[2];
-                    t_eps += po->x_cnt[3];
-                    pflags |= po->pflags;
-                }
-        } else {
-            __syncthreads();
         }
         if (rank != 0) continue;   // the lane's last writes are visible to rank 0 (lane_sync)
         // ---- final transition / death fallback (decoder.py:252-273, 327-333)
@@ -2226,7 +2230,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             memset(&r, 0, sizeof(r));
             for (int q = 0; q < 8; ++q) r.phase_cycles[q] = sh.pc[q];
             r.total_cost = best_cost;
-            r.tokens_expanded = expanded;
+            r.tokens_expanded = sh.acc[0];
             r.search_steps = steps_run;
             r.reached_final = reached;
             r.died_at_step = died_at;
@@ -2244,15 +2248,15 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             r.status = status & 0xFF;
             r.capacity_flags = capf;
             r.path_flags = pflags;
-            r.n_tok = n_tok;
+            r.n_tok = sh.acc[0];
             r.a_emit = t_emit;
             r.a_fin = t_fin;
             r.a_cas = t_cas;
-            r.eps_rounds = eps_rounds;
+            r.eps_rounds = sh.acc[4];
             r.e_eps = t_eps;
-            r.n_cand = n_cand_tot;
-            r.n_surv = n_surv_tot;
-            r.n_rec = n_rec;
+            r.n_cand = sh.acc[1];
+            r.n_surv = sh.acc[2];
+            r.n_rec = sh.acc[3];
             r.lat_arcs = lat_arcs;
             res[u] = r;
         }
