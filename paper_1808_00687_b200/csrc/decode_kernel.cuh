@@ -59,6 +59,16 @@ __host__ __device__ constexpr int wb_cap(int cause) { return WB_ERR_CAPACITY | (
 #ifndef WB_MINB_256
 #define WB_MINB_256 1
 #endif
+// The step's phase functions are compiled into the kernel body: as separate calls, every
+// value live across a call was spilled around it under the 64-register budget and the
+// callees read the kernel parameters through generic pointers (config 2: 97.3 ms as calls,
+// 87.2 ms inlined).  WB_PHASE_NOINLINE restores the calls (experiments).
+#ifdef WB_PHASE_NOINLINE
+#define WB_PHASE_FN __noinline__
+#else
+#define WB_PHASE_FN __forceinline__
+#endif
+
 template <int BLOCK> struct Tune {
     static constexpr int MINB = BLOCK == 512 ? WB_MINB_512 : BLOCK == 256 ? WB_MINB_256 : 1;
     static constexpr bool R64 = BLOCK * MINB >= 1024;  // 64-register budget
@@ -81,7 +91,7 @@ struct WorkDev {
     u32 *qtag;            // [slots][S]   epsilon frontier dedup tags
     u32 *tag_ctr;         // [slots]
     u32 *cand_state;      // [slots][cap]
-    u32 *cand_arc, *cand_pay;
+    u64 *cand_ap;       // candidate winner (arc + 1) | payload << 32: a slot's high word
     u64 *cand_key;        // [slots][cap] (used when a step overflows shared memory)
     u32 *cand_ca;         // [slots][cap]
     u32 *front;           // [slots][2][cap] frontier states / pending record list
@@ -202,6 +212,9 @@ struct Smem {
     u64 arena_used;    // records of the lane's current utterance
     long long pc[8];   // phase cycle counters (thread 0)
     long long t_mark;  // last phase boundary (thread 0)
+#ifdef WB_PROBE
+    long long spin_acc, spin_ph[8];  // probe build: lane-barrier wait cycles of thread 0 per phase
+#endif
     union {
         u32 hist[NB];
         struct {
@@ -238,6 +251,10 @@ __device__ __forceinline__ void tick(int ph) {
         long long t = clock64();
         sh.pc[ph] += t - sh.t_mark;
         sh.t_mark = t;
+#ifdef WB_PROBE
+        sh.spin_ph[ph] += sh.spin_acc;
+        sh.spin_acc = 0;
+#endif
     }
 }
 
@@ -311,9 +328,15 @@ __device__ __forceinline__ void lane_sync(int K, bool global = true) {
         const int r = cta_rank();
         for (int q = 0; q < K; ++q)
             if (q != r) *(volatile u32 *)&peer(&sh, q)->ls_flag[r] = e;
+#ifdef WB_PROBE
+        const long long t0 = clock64();
+#endif
         for (int q = 0; q < K; ++q)
             if (q != r)
                 while ((int)(*(volatile u32 *)&sh.ls_flag[q] - e) < 0) { }
+#ifdef WB_PROBE
+        sh.spin_acc += clock64() - t0;
+#endif
     }
     __syncthreads();
 }
@@ -401,8 +424,7 @@ struct Lane {
     __device__ __forceinline__ u32 *cand_of() const { return ws.cand_of + so(); }
     __device__ __forceinline__ u32 *qtag() const { return ws.qtag + so(); }
     __device__ __forceinline__ u32 *cand_state() const { return ws.cand_state + co(); }
-    __device__ __forceinline__ u32 *cand_arc() const { return ws.cand_arc + co(); }
-    __device__ __forceinline__ u32 *cand_pay() const { return ws.cand_pay + co(); }
+    __device__ __forceinline__ u64 *cand_ap() const { return ws.cand_ap + co(); }
     __device__ __forceinline__ u64 *cand_key() const { return ws.cand_key + co(); }
     __device__ __forceinline__ u32 *cand_ca() const { return ws.cand_ca + co(); }
     __device__ __forceinline__ u32 *front(int k) const { return ws.front + 2 * co() + (size_t)k * ws.lcap; }
@@ -610,7 +632,7 @@ __device__ __forceinline__ void claim_token(const WorkDev &ws, int t, int group)
 #endif
 
 template <int BLOCK, int KC>
-__noinline__ __device__ ExpandCounts expand_emitting(int n_live, int cur, const double *row,
+WB_PHASE_FN __device__ ExpandCounts expand_emitting(int n_live, int cur, const double *row,
                                                      const GraphDev &g, const WorkDev &ws,
                                                      double beam, bool row_nonneg, bool piloted,
                                                      int max_active) {
@@ -933,7 +955,7 @@ struct EpsOut {
 };
 
 template <int BLOCK, int KC>
-__noinline__ __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev &ws, u32 tag_in,
+WB_PHASE_FN __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev &ws, u32 tag_in,
                                                double beam) {
     Smem<BLOCK> &sh = SH<BLOCK>();
     const Lane c{ws};
@@ -1077,7 +1099,7 @@ struct Thr {
 };
 
 template <int BLOCK, int KC>
-__noinline__ __device__ Thr select_threshold(int n_loc, int max_active, double best, double cutoff,
+WB_PHASE_FN __device__ Thr select_threshold(int n_loc, int max_active, double best, double cutoff,
                                              double scale, const u64 *ckey, const u32 *cst,
                                              const WorkDev &ws) {
     Smem<BLOCK> &sh = SH<BLOCK>();
@@ -1207,7 +1229,7 @@ struct StepOut {
 };
 
 template <int BLOCK, int KC>
-__noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const WorkDev &ws,
+WB_PHASE_FN __device__ StepOut finish_step(int nxt, const GraphDev &g, const WorkDev &ws,
                                             const CfgDev &cfg) {
     Smem<BLOCK> &sh = SH<BLOCK>();
     const Lane c{ws};
@@ -1221,7 +1243,7 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
     u32 *ca = in_smem ? s_ca<BLOCK>(ws) : c.cand_ca() + cbase;
     volatile u32 *vca = ca;
     u32 *cst = c.cand_state() + cbase;
-    u32 *carc = c.cand_arc() + cbase, *cpay = c.cand_pay() + cbase;
+    u64 *cap = c.cand_ap() + cbase;
 
     // P1: gather slot contents (batched loads), reset slots, min / max
     if (threadIdx.x == 0) sh.best_tok = -1;
@@ -1249,8 +1271,7 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
             int i = i0 + q * BLOCK;
             if (i < n_loc) {
                 ckey[i] = v[q].key;
-                carc[i] = v[q].arcp1;
-                cpay[i] = v[q].pay;
+                cap[i] = (u64)v[q].arcp1 | ((u64)v[q].pay << 32);
                 ca[i] = 0u;
                 if (!ws.xchg_gather) st_slot_empty(&c.slot()[st[q]]);
 #ifdef WB_CHECKS
@@ -1356,7 +1377,8 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
         if (!g.has_eps) continue;
         u32 v = (u32)(cbase + i);
         for (;;) {
-            u32 a = ldx<KC>(&c.cand_arc()[v]), p = ldx<KC>(&c.cand_pay()[v]);
+            const u64 ap = ldx<KC>(&c.cand_ap()[v]);
+            u32 a = (u32)ap, p = (u32)(ap >> 32);
             if (a == 0u || !(p & EPS_BIT)) break;
             u32 uix = p & ~EPS_BIT;
             u32 old = atomicOr(flag_of(uix), F_MARK);
@@ -1428,8 +1450,9 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
             u64 k = 0;
             if (in) {
                 f = vca[i];
-                a = carc[i];
-                p = cpay[i];
+                const u64 ap = cap[i];
+                a = (u32)ap;
+                p = (u32)(ap >> 32);
                 st = cst[i];
                 k = ckey[i];
             }
@@ -1482,7 +1505,8 @@ __noinline__ __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wo
     const int n_pend = sh.n_pend;
     for (int q = threadIdx.x; q < n_pend; q += BLOCK) {
         int i = (int)pend[q];
-        u32 a = carc[i], p = cpay[i];
+        const u64 ap = cap[i];
+        const u32 a = (u32)ap, p = (u32)(ap >> 32);
         const u32 src = *(volatile u32 *)flag_of(p & ~EPS_BIT);
         c.arena()[vca[i]] = (u64)a | ((u64)src << 32);
     }
@@ -1964,6 +1988,10 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
         const int u = K > 1 ? peer(&sh, 0)->utt : sh.utt;
         if (u >= b.n) break;
         if (threadIdx.x < 8) sh.pc[threadIdx.x] = 0;
+#ifdef WB_PROBE
+        if (threadIdx.x < 8) sh.spin_ph[threadIdx.x] = 0;
+        if (threadIdx.x == 0) sh.spin_acc = 0;
+#endif
         if (threadIdx.x < 4) sh.cnt[threadIdx.x] = 0ull;
         if (threadIdx.x < 5) sh.acc[threadIdx.x] = 0ll;
         if (threadIdx.x == 0) {
@@ -2061,10 +2089,6 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
                     if (threadIdx.x == 0) { sh.x_stream = 1; sh.ready_seen = 0; }
                 }
             }
-#ifdef WB_PROBE
-            __syncthreads();
-            tick<BLOCK>(7);   // probe build: loop overhead / row wait before the staging phase
-#endif
             int neg = !row_in_smem;  // acoustic costs of this row all >= 0? (checked while staging)
             if (threadIdx.x == 0) {
                 sh.n_cand = 0; sh.nfr[0] = sh.nfr[1] = 0; sh.overflow = 0; sh.n_log = 0;
@@ -2229,6 +2253,11 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             wb_utt_result r;
             memset(&r, 0, sizeof(r));
             for (int q = 0; q < 8; ++q) r.phase_cycles[q] = sh.pc[q];
+#ifdef WB_PROBE
+            // probe build: phases 0-6 report thread 0's lane-barrier wait, 7 the total
+            for (int q = 0; q < 7; ++q) r.phase_cycles[7] += sh.pc[q];
+            for (int q = 0; q < 7; ++q) r.phase_cycles[q] = sh.spin_ph[q];
+#endif
             r.total_cost = best_cost;
             r.tokens_expanded = sh.acc[0];
             r.search_steps = steps_run;

@@ -56,7 +56,8 @@ struct wb_decoder_s {
     u64 arena_cap = 0;
     Slot *slot = nullptr;
     u32 *cand_of = nullptr, *qtag = nullptr, *tag_ctr = nullptr;
-    u32 *cand_state = nullptr, *cand_arc = nullptr, *cand_pay = nullptr, *cand_ca = nullptr;
+    u32 *cand_state = nullptr, *cand_ca = nullptr;
+    u64 *cand_ap = nullptr;
     u64 *cand_key = nullptr;
     u32 *front = nullptr;
     int4 *frng = nullptr;
@@ -209,7 +210,7 @@ static void free_decoder(wb_decoder_s *d) {
     void *chk[] = {d->chk_claim, d->chk_seen, d->chk_err, d->chk_log, d->chk_steps};
     for (void *p : chk) cudaFree(p);
     void *ptrs[] = {d->slot, d->cand_of, d->qtag, d->tag_ctr, d->cand_state,
-                    d->cand_arc, d->cand_pay, d->cand_key, d->cand_ca, d->front, d->frng, d->tok_info,
+                    d->cand_ap, d->cand_key, d->cand_ca, d->front, d->frng, d->tok_info,
                     d->tok_cost, d->frames, d->arena, d->counters, d->h_costs, d->h_blank,
                     d->h_off, d->h_crow, d->h_T, d->h_res, d->h_lab, d->tok_eps, d->sbits, d->snode,
                     d->ln_state, d->ln_out, d->ln_flag, d->la_src, d->la_dst, d->la_arc,
@@ -452,8 +453,7 @@ int wb_decoder_create(wb_graph_t g, const wb_decoder_opts *o, wb_decoder_t *out)
     DA(qtag, g->has_eps ? slots * S : 1);
     DA(tag_ctr, slots);
     DA(cand_state, cslots * cap);
-    DA(cand_arc, cslots * cap);
-    DA(cand_pay, cslots * cap);
+    DA(cand_ap, cslots * cap);
     DA(cand_key, cslots * cap);
     DA(cand_ca, cslots * cap);
     DA(front, cslots * 2 * cap);
@@ -674,8 +674,7 @@ static int decode_impl(wb_decoder_t d, int32_t n, const double *costs, const int
     WorkDev wd;
     std::memset(&wd, 0, sizeof(wd));
     wd.slot = d->slot; wd.cand_of = d->cand_of; wd.qtag = d->qtag; wd.tag_ctr = d->tag_ctr;
-    wd.cand_state = d->cand_state; wd.cand_arc = d->cand_arc;
-    wd.cand_pay = d->cand_pay; wd.cand_key = d->cand_key; wd.cand_ca = d->cand_ca;
+    wd.cand_state = d->cand_state; wd.cand_ap = d->cand_ap; wd.cand_key = d->cand_key; wd.cand_ca = d->cand_ca;
     wd.front = d->front; wd.frng = d->frng; wd.tok_info = d->tok_info; wd.tok_cost = d->tok_cost;
     wd.frames = d->frames;
     wd.arena = d->arena; wd.arena_cap = d->arena_cap;
