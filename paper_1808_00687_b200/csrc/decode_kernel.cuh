@@ -764,20 +764,26 @@ WB_PHASE_FN __device__ ExpandCounts expand_emitting(int n_live, int cur, const d
             ma_thr = mb;
             __syncthreads();
         }
-        // warps claim 32-token chunks dynamically (first chunk = warp id), so no warp idles at
-        // the closing barrier while another still has two chunks to go
-        for (int lc = w; lc < nchunks;) {
+        // warps claim work units dynamically (first unit = warp id): 32-token chunks, except
+        // that the last NW chunks are claimed as 8-token quarters, so the warps run out of work
+        // within about a quarter chunk of each other at the closing barrier
+        const int nbig = max(0, nchunks - NW);
+        const int nunits = nbig + 4 * (nchunks - nbig);
+        for (int lc = w; lc < nunits;) {
             int ch_claim = 0;
-            if (l == 0) ch_claim = atomicAdd(&SH<BLOCK>().next_chunk, 1);  // used after this chunk
-            const int ch = chunk_of(lc);
-            const int t = (ch << 5) + l;
+            if (l == 0) ch_claim = atomicAdd(&SH<BLOCK>().next_chunk, 1);  // used after this unit
+            const int qv = lc - nbig;
+            const int ch = chunk_of(lc < nbig ? lc : nbig + (qv >> 2));
+            const int tlo = lc < nbig ? 0 : (qv & 3) << 3;   // the unit's first token in the chunk
+            const int t = (ch << 5) + tlo + l;
             int4 ti = make_int4(0, 0, 0, 0);
             double tc = 0.0;
-            if (t < n_live) { ti = ldx<KC>(&tinfo[t]); tc = ldx<KC>(&tcost[t]); }
+            if (t < n_live && (lc < nbig || l < 8)) { ti = ldx<KC>(&tinfo[t]); tc = ldx<KC>(&tcost[t]); }
             const bool in_pass = !ma_on || ((tc <= split) == (pass == 0));
-            const int deg = (t < n_live && in_pass) ? ti.w - ti.z : 0;
+            const bool mine = t < n_live && (lc < nbig || l < 8) && in_pass;
+            const int deg = mine ? ti.w - ti.z : 0;
 #ifdef WB_CHECKS
-            if (t < n_live && in_pass) claim_token<BLOCK>(ws, t, r * NW + w);
+            if (mine) claim_token<BLOCK>(ws, t, r * NW + w);
 #endif
             a_emit += deg;
             const int incl = warp_incl_scan(deg);
@@ -826,7 +832,7 @@ WB_PHASE_FN __device__ ExpandCounts expand_emitting(int n_live, int cur, const d
                         const long long e = base + __popc(m & lanemask_lt());
                         if (act && e < ws.rlog_cap)
                             ws.rlog[(size_t)blockIdx.x * ws.rlog_cap + e] =
-                                make_int4((ch << 5) + k, arc, rec.x, rec.y);
+                                make_int4((ch << 5) + tlo + k, arc, rec.x, rec.y);
                     }
                 }
                 bool first = false, dec = false;
