@@ -68,6 +68,13 @@ __host__ __device__ constexpr int wb_cap(int cause) { return WB_ERR_CAPACITY | (
 #else
 #define WB_PHASE_FN __forceinline__
 #endif
+// the lattice recorder's step and trim functions (lattice mode only): inlined as well
+// (config 3: 529 -> 518 ms); WB_LATTICE_NOINLINE restores the calls
+#ifdef WB_LATTICE_NOINLINE
+#define WB_LATTICE_FN __noinline__
+#else
+#define WB_LATTICE_FN __forceinline__
+#endif
 
 template <int BLOCK> struct Tune {
     static constexpr int MINB = BLOCK == 512 ? WB_MINB_512 : BLOCK == 256 ? WB_MINB_256 : 1;
@@ -1595,7 +1602,7 @@ __device__ __forceinline__ bool surv_bit(const u32 *bits, u32 s) {
 // survivors(k).  The raw lattice is a pure function of these sets, so no per-relaxation
 // recorder is needed.  Node / arc indices are utterance-global positions in this lane's pool.
 template <int BLOCK>
-__noinline__ __device__ int record_lattice_step(int k, int nxt, int n_surv, int prv, int n_prev,
+WB_LATTICE_FN __device__ int record_lattice_step(int k, int nxt, int n_surv, int prv, int n_prev,
                                                 const double *grow, int L1,
                                                 const GraphDev &g, const WorkDev &ws) {
     Smem<BLOCK> &sh = SH<BLOCK>();
@@ -1751,7 +1758,7 @@ __noinline__ __device__ int record_lattice_step(int k, int nxt, int n_surv, int 
 constexpr unsigned char LF_FWD = 1, LF_BWD = 2;
 
 template <int BLOCK>
-__noinline__ __device__ void trim_lattice(int u, int K, int reached, int final_state,
+WB_LATTICE_FN __device__ void trim_lattice(int u, int K, int reached, int final_state,
                                           const GraphDev &g, const WorkDev &ws) {
     const int final_step = K;  // the last node step with nodes is the winner's step
     Smem<BLOCK> &sh = SH<BLOCK>();
