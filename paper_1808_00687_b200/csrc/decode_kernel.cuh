@@ -191,6 +191,8 @@ struct Smem {
     int n_log;          // relaxations logged this step (lattice mode)
     u64 run_min;        // smallest emitting relaxation key seen so far this step
     int best_tok;       // a live token of minimal cost (its arcs seed run_min); -1 = unknown
+    u64 best_rng;       // its emitting arc range emit_hi << 32 | emit_lo (one 64-bit store)
+    u64 best_key;       // its cost key (the step's minimum)
     int next_chunk;     // expand: next unclaimed 32-token chunk (warps claim chunks dynamically)
     int ready_seen;     // streaming: last ready count read for the current utterance
     int pflags;         // WB_PATH_* bits of the current utterance (thread 0 writes)
@@ -529,12 +531,12 @@ __device__ __forceinline__ bool finish_relax(Slot *p, const Slot &want, Slot pre
 template <int BLOCK>
 __device__ __forceinline__ void pilot_min(int bt, int cur, const double *row, const GraphDev &g,
                                           const WorkDev &ws) {
-    const Lane c{ws};
     const int l = threadIdx.x & 31;
-    const int4 ti = __ldcg(&c.tok_info(cur)[bt]);   // possibly written by another CTA of the lane
-    const double tc = __ldcg(&c.tok_cost(cur)[bt]);
+    // the token's arc range and cost as the compaction recorded them with best_tok
+    const u64 br = *(volatile u64 *)&SH<BLOCK>().best_rng;
+    const double tc = key_cost(SH<BLOCK>().best_key);
     u64 m = EMPTY_KEY;
-    for (int a = ti.z + l; a < ti.w; a += 32) {
+    for (int a = (int)(u32)br + l; a < (int)(u32)(br >> 32); a += 32) {
         const int4 r = ld_arc(&g.arcs[2 * a]);
         const double ac = row[r.y];
         if (ac != INFINITY) {
@@ -1486,8 +1488,17 @@ WB_PHASE_FN __device__ StepOut finish_step(int nxt, const GraphDev &g, const Wor
                 tinfo[tj] = make_int4((int)st, (int)rec, rg.y, rg.z);
                 tcost[tj] = key_cost(k);
                 if (k == mn) {   // any minimal token will do; every CTA of the lane gets it
-                    sh.best_tok = (int)tj;
-                    for (int q = 1; q < K; ++q) peer(&sh, (r + q) & (K - 1))->best_tok = (int)tj;
+                    // with its arc range (one store: concurrent minimal tokens cannot mix
+                    // ranges) and its arcs pulled into L2 for the next step's pilot
+                    const u64 br = ((u64)(u32)rg.z << 32) | (u32)rg.y;
+                    for (int q = 0; q < K; ++q) {
+                        Smem<BLOCK> *po = q == 0 ? &sh : peer(&sh, (r + q) & (K - 1));
+                        po->best_tok = (int)tj;
+                        *(volatile u64 *)&po->best_rng = br;
+                        po->best_key = k;
+                    }
+                    for (int a2 = rg.y; a2 < rg.z; a2 += 4)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(&g.arcs[2 * (size_t)a2]));
                 }
                 if (ws.tok_eps) ws.tok_eps[2 * c.co() + (size_t)nxt * ws.lcap + tj] = rg.x;
             }
