@@ -2113,6 +2113,10 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
                     if (threadIdx.x == 0) { sh.x_stream = 1; sh.ready_seen = 0; }
                 }
             }
+#ifdef WB_PROBE_STAGE
+            __syncthreads();
+            tick<BLOCK>(7);   // probe build: loop top (frame id, row address) vs staging + pilot
+#endif
             int neg = !row_in_smem;  // acoustic costs of this row all >= 0? (checked while staging)
             if (threadIdx.x == 0) {
                 sh.n_cand = 0; sh.nfr[0] = sh.nfr[1] = 0; sh.overflow = 0; sh.n_log = 0;
@@ -2131,10 +2135,23 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             if (row_in_smem) {
                 const int t0 = pilot ? (int)threadIdx.x - 32 : (int)threadIdx.x;
                 const int nt = pilot ? BLOCK - 32 : BLOCK;
-                for (int q = t0; q >= 0 && q < b.L1; q += nt) {
-                    const double v = __ldg(&grow[q]);
-                    neg |= v < 0.0;
-                    srow[q] = v;
+                // 8 loads in flight per thread before the stores (one memory round trip for
+                // rows up to 8 x BLOCK columns instead of one per column a thread stages)
+                for (int q0 = t0; q0 >= 0 && q0 < b.L1; q0 += 8 * nt) {
+                    double v[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int q = q0 + i * nt;
+                        v[i] = q < b.L1 ? __ldg(&grow[q]) : 0.0;
+                    }
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int q = q0 + i * nt;
+                        if (q < b.L1) {
+                            neg |= v[i] < 0.0;
+                            srow[q] = v[i];
+                        }
+                    }
                 }
                 row = srow;
             }
