@@ -488,9 +488,12 @@ def main():
         e2e = {"value": frames_all * args.steps / (e_ms / 1e3), "unit": "frames/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": e_ms / args.steps,
-               "input_path": ("pinned host cost table read zero-copy by the kernel (one staged "
-                              "row per search step, overlapped with the search)" if zero_copy
-                              else "pinned host cost table copied H2D, then decode")}
+               "input_path": {1: "pinned host cost table read zero-copy by the kernel (one staged "
+                                 "row per search step, overlapped with the search)",
+                              2: "pinned host cost table copied H2D by the copy engine in step-range "
+                                 "chunks (8, 16, then 32 steps of every utterance) while the kernel "
+                                 "decodes; the kernel polls per-utterance ready counts"}.get(
+                                     zero_copy, "pinned host cost table copied H2D, then decode")}
 
     # ---------------- e2e from posterior matrices (decode_batch's path): frame_costs
     # (numpy -log, bit-exactness needs the host's own log) on host threads, streamed into the

@@ -259,9 +259,12 @@ int wb_lattice_pruned_totals(wb_decoder_t d, int32_t *n_utts, int64_t *n_nodes, 
 int wb_lattice_pruned_fetch(wb_decoder_t d, int64_t *meta, int32_t *nodes, uint32_t *arcs,
                             double *arc_ac, uint32_t *finals, double *final_w);
 
-/* Host->device bytes of the last WB_MEM_HOST wb_decode call and whether its cost table was
- * read zero-copy (page-locked host memory, one staged row per search step: the transfer
- * overlaps the search and LSD reads only the non-blank rows).  Pageable tables are copied. */
+/* Host->device bytes of the last WB_MEM_HOST wb_decode call and how its cost table moved:
+ * zero_copy 1 = read zero-copy by the kernel (page-locked host memory, one staged row per
+ * search step; LSD reads only the non-blank rows); 2 = page-locked FSD table of equal-length
+ * utterances at a common stride, copied by the copy engine in step-range chunks while the
+ * kernel decodes (the kernel polls per-utterance ready counts); 0 = copied before the decode
+ * (pageable memory). */
 int wb_last_transfer(wb_decoder_t d, int64_t *h2d_bytes, int32_t *zero_copy);
 
 /*

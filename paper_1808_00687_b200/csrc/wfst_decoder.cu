@@ -76,6 +76,14 @@ struct wb_decoder_s {
     int *h_lab = nullptr;
     size_t h_off_n = 0, h_T_n = 0, h_res_n = 0, h_lab_n = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // H2D pipeline of a page-locked FSD cost table: step-range chunks on a copy stream, each
+    // followed by the per-utterance ready counts the kernel polls (see decode_impl)
+    cudaStream_t copy_st = nullptr;
+    cudaEvent_t cev_a = nullptr, cev_b = nullptr, cev_c = nullptr;
+    int *dma_ready = nullptr;          // device [n] ready counters
+    size_t dma_ready_n = 0;
+    int *dma_counts = nullptr;         // page-locked host [chunks][n] counts to publish
+    size_t dma_counts_n = 0;
     size_t bytes = 0;
     long long last_h2d = 0;   // bytes moved host -> device by the last WB_MEM_HOST call
     int last_zero_copy = 0;
@@ -207,6 +215,11 @@ int wb_graph_device_bytes(wb_graph_t g, int64_t *bytes) {
 }  // extern "C"
 
 static void free_decoder(wb_decoder_s *d) {
+    if (d->copy_st) cudaStreamSynchronize(d->copy_st);
+    cudaFree(d->dma_ready);
+    cudaFreeHost(d->dma_counts);
+    for (cudaEvent_t ev : {d->cev_a, d->cev_b, d->cev_c}) if (ev) cudaEventDestroy(ev);
+    if (d->copy_st) cudaStreamDestroy(d->copy_st);
     void *chk[] = {d->chk_claim, d->chk_seen, d->chk_err, d->chk_log, d->chk_steps};
     for (void *p : chk) cudaFree(p);
     void *ptrs[] = {d->slot, d->cand_of, d->qtag, d->tag_ctr, d->cand_state,
@@ -613,6 +626,7 @@ static int decode_impl(wb_decoder_t d, int32_t n, const double *costs, const int
     wb_utt_result *dres = results;
     int *dol = olabels, *dil = ilabels;
     const int lcap = std::max(label_cap, 1);
+    bool dma = false;   // H2D pipeline of the cost table (below)
     if (host) {
         int maxT = 0;
         long long rows = 0;
@@ -656,7 +670,63 @@ static int decode_impl(wb_decoder_t d, int32_t n, const double *costs, const int
             }
             ready_dev = (const int *)pr.devicePointer;
         }
-        if (ncost && !zc)
+        // H2D pipeline (FSD, page-locked table, every utterance T rows at a common stride): the
+        // copy engine moves step-range chunks of all utterances into device memory while the
+        // kernel runs, publishing per-utterance ready counts after each chunk; the kernel reads
+        // its rows from HBM instead of staging each one over PCIe.  WB_H2D_PIPELINE=0: off.
+        const char *dp = std::getenv("WB_H2D_PIPELINE");
+        if (zc && !ready && cfg->mode == 0 && n > 0 && !(dp && dp[0] == '0')) {
+            const long long T0 = num_frames[0], stride = n > 1 ? row_offset[1] - row_offset[0] : T0;
+            dma = T0 > 0 && stride >= T0;
+            for (int i = 0; i < n && dma; ++i)
+                dma = num_frames[i] == T0 && row_offset[i] == row_offset[0] + (long long)i * stride;
+        }
+        if (dma) {
+            const int T0 = num_frames[0];
+            const long long stride = n > 1 ? row_offset[1] - row_offset[0] : T0;
+            // chunk boundaries in steps: 8, 16, then 32-step chunks (the first rows land fast)
+            std::vector<int> cut{0};
+            for (int c = 8; cut.back() < T0; c = std::min(32, c * 2)) cut.push_back(std::min(T0, cut.back() + c));
+            const size_t nch = cut.size() - 1;
+            if (!d->copy_st) {
+                CUDA_TRY(cudaStreamCreateWithFlags(&d->copy_st, cudaStreamNonBlocking));
+                CUDA_TRY(cudaEventCreateWithFlags(&d->cev_a, cudaEventDisableTiming));
+                CUDA_TRY(cudaEventCreateWithFlags(&d->cev_b, cudaEventDisableTiming));
+                CUDA_TRY(cudaEventCreateWithFlags(&d->cev_c, cudaEventDisableTiming));
+            }
+            if ((rc = grow(&d->dma_ready, d->dma_ready_n, nn))) return rc;
+            CUDA_TRY(cudaStreamSynchronize(d->copy_st));   // the host counts below are reused
+            if (d->dma_counts_n < nch * nn) {
+                cudaFreeHost(d->dma_counts);
+                d->dma_counts = nullptr;
+                d->dma_counts_n = 0;
+                CUDA_TRY(cudaMallocHost(&d->dma_counts, sizeof(int) * nch * nn));
+                d->dma_counts_n = nch * nn;
+            }
+            for (size_t k = 0; k < nch; ++k)
+                for (size_t i = 0; i < nn; ++i) d->dma_counts[k * nn + i] = cut[k + 1];
+            // the copies overwrite the device table only after the work queued before this call
+            // (a previous decode reading it) is done; the kernel starts after the counts are zero
+            CUDA_TRY(cudaEventRecord(d->cev_a, st));
+            CUDA_TRY(cudaStreamWaitEvent(d->copy_st, d->cev_a, 0));
+            CUDA_TRY(cudaMemsetAsync(d->dma_ready, 0, sizeof(int) * nn, d->copy_st));
+            CUDA_TRY(cudaEventRecord(d->cev_b, d->copy_st));
+            const size_t rowb = sizeof(double) * (size_t)num_cols, pitch = rowb * (size_t)stride;
+            for (size_t k = 0; k < nch; ++k) {
+                const size_t off = rowb * ((size_t)row_offset[0] + (size_t)cut[k]);
+                CUDA_TRY(cudaMemcpy2DAsync(reinterpret_cast<char *>(d->h_costs) + off, pitch,
+                                           reinterpret_cast<const char *>(costs) + off, pitch,
+                                           rowb * (size_t)(cut[k + 1] - cut[k]), nn,
+                                           cudaMemcpyHostToDevice, d->copy_st));
+                CUDA_TRY(cudaMemcpyAsync(d->dma_ready, d->dma_counts + k * nn, sizeof(int) * nn,
+                                         cudaMemcpyHostToDevice, d->copy_st));
+            }
+            CUDA_TRY(cudaEventRecord(d->cev_c, d->copy_st));
+            CUDA_TRY(cudaStreamWaitEvent(st, d->cev_b, 0));
+            zc = false;
+            ready_dev = d->dma_ready;
+        }
+        if (ncost && !zc && !dma)
             CUDA_TRY(cudaMemcpyAsync(d->h_costs, costs, sizeof(double) * ncost, cudaMemcpyHostToDevice, st));
         d->last_h2d = (long long)(sizeof(double) * (zc ? 0 : ncost) + sizeof(double) * rows +
                                   (sizeof(long long) + sizeof(int)) * nn);
@@ -783,7 +853,9 @@ static int decode_impl(wb_decoder_t d, int32_t n, const double *costs, const int
         bd.costs = d->h_costs;
         e = launch();
     }
-    d->last_zero_copy = zc ? 1 : 0;
+    d->last_zero_copy = zc ? 1 : dma ? 2 : 0;
+    // the call's stream completes only after the whole table copy (the next call may reuse it)
+    if (dma) CUDA_TRY(cudaStreamWaitEvent(st, d->cev_c, 0));
     if (e == cudaSuccess && prune) {
         const size_t T2 = (size_t)d->T_cap + 3;
         CUDA_TRY(cudaMemsetAsync(d->p_ctr, 0, sizeof(unsigned long long) * 4, st));

@@ -251,11 +251,13 @@ class BatchDecoder:
         N.check(self._L.wb_decoder_device_bytes(self._h, C.byref(b)))
         return int(b.value)
 
-    def last_transfer(self) -> tuple[int, bool]:
-        """(host->device bytes, zero-copy?) of the last host-buffer decode."""
+    def last_transfer(self) -> tuple[int, int]:
+        """(host->device bytes, path) of the last host-buffer decode: path 1 = cost rows read
+        zero-copy by the kernel, 2 = table copied in step-range chunks during the decode (H2D
+        pipeline), 0 = copied before the decode."""
         b, z = C.c_int64(), C.c_int32()
         N.check(self._L.wb_last_transfer(self._h, C.byref(b), C.byref(z)))
-        return int(b.value), bool(z.value)
+        return int(b.value), int(z.value)
 
     def check_report(self, n_lanes: int | None = None) -> None:
         """Checked build: raise ``DeviceCheckError`` if a device invariant failed during the

@@ -52,8 +52,10 @@ def test_medium_graph(cuda, seed):
 
 @pytest.mark.parametrize("mode", ["fsd", "lsd"])
 def test_zero_copy_pinned_matches_copy_and_oracle(cuda, mode):
-    """A page-locked cost table is read zero-copy by the kernel (one staged row per step);
-    the results equal the copy path's and the oracle's, and only searched rows cross PCIe."""
+    """A page-locked cost table: FSD (equal-length utterances at a common stride) goes through
+    the H2D pipeline (step-range chunks copied while the kernel decodes, ready counts polled),
+    LSD is read zero-copy (only searched rows cross PCIe); the results equal the copy path's
+    and the oracle's."""
     import torch
     from paper_1808_00687_b200.decoder import BatchDecoder
     g = synth.random_wfst(5, 3000, 9000, 40, eps_fraction=0.03, selfloops=mode == "lsd",
@@ -70,10 +72,14 @@ def test_zero_copy_pinned_matches_copy_and_oracle(cuda, mode):
     cfg = P.DecodeConfig(beam=9.0, max_active=200, mode=mode)
     dec = BatchDecoder(g, 0)
     zc = dec.decode_host(pinned.numpy(), off, T, blank, cfg, mode)
-    h2d, was_zc = dec.last_transfer()
-    assert was_zc
-    steps = int(zc.results["search_steps"].sum())
-    assert h2d == steps * 41 * 8 + blank.nbytes + off.nbytes + T.nbytes
+    h2d, path = dec.last_transfer()
+    if mode == "fsd":   # equal-length utterances at a common stride: the H2D pipeline
+        assert path == 2
+        assert h2d == pinned.numpy().nbytes + blank.nbytes + off.nbytes + T.nbytes
+    else:               # LSD: zero-copy, only the searched (non-blank) rows cross PCIe
+        assert path == 1
+        steps = int(zc.results["search_steps"].sum())
+        assert h2d == steps * 41 * 8 + blank.nbytes + off.nbytes + T.nbytes
     cp = dec.decode_host(pinned.numpy().copy(), off, T, blank, cfg, mode)   # pageable -> copy
     assert not dec.last_transfer()[1]
     assert zc.decode_results() == cp.decode_results()
@@ -266,3 +272,32 @@ def test_posterior_batch_capacity_retry(cuda, tmp_path):
     tiny = BatchDecoder(g, 0, cand_capacity=16, arena_capacity=1024)
     got = tiny.decode_posteriors(PosteriorBatch(mats), cfg).decode_results()
     assert got == P.decode_batch(g, mats, cfg)
+
+
+def test_h2d_pipeline_fallbacks(cuda, monkeypatch):
+    """The H2D pipeline needs equal-length FSD utterances at a common stride: ragged batches
+    and WB_H2D_PIPELINE=0 read the page-locked table zero-copy; all three paths agree."""
+    import torch
+    from paper_1808_00687_b200.decoder import BatchDecoder
+    g = synth.random_wfst(8, 2000, 6000, 30, eps_fraction=0.03, final_fraction=0.05)
+    cfg = P.DecodeConfig(beam=9.0, max_active=150, mode="fsd")
+    for name, lens in (("equal", [90] * 6), ("ragged", [90, 40, 90, 75, 90, 1])):
+        posts = [synth.random_posteriors(70 + k, t, 30) for k, t in enumerate(lens)]
+        T = np.asarray(lens, np.int32)
+        off = np.zeros(len(T), np.int64)
+        np.cumsum(T[:-1], out=off[1:])
+        pinned = torch.empty((int(T.sum()), 31), dtype=torch.float64, pin_memory=True)
+        for p, o in zip(posts, off):
+            P.cost_table(p, out=pinned.numpy()[o:o + p.num_frames])
+        blank = np.concatenate([p.rows[:, 0] for p in posts])
+        dec = BatchDecoder(g, 0)
+        r = dec.decode_host(pinned.numpy(), off, T, blank, cfg, "fsd").decode_results()
+        assert dec.last_transfer()[1] == (2 if name == "equal" else 1)
+        for p, got in zip(posts, r):
+            o = O.decode(g, P.cost_table(p), p.rows[:, 0], beam=9.0, max_active=150, mode="fsd")
+            assert _fields(got) == o.astuple()
+        if name == "equal":
+            monkeypatch.setenv("WB_H2D_PIPELINE", "0")
+            assert dec.decode_host(pinned.numpy(), off, T, blank, cfg, "fsd").decode_results() == r
+            assert dec.last_transfer()[1] == 1
+            monkeypatch.delenv("WB_H2D_PIPELINE")
