@@ -36,6 +36,25 @@ for mode in ("fsd", "lsd"):
                 r.reached_final, r.died_at_step) == o.astuple(), (mode, r, o)
     rec = P.LatticeRecorder()
     P.decode(g, posts[0], cfg, recorder=rec)
+# the H2D pipeline of a page-locked FSD table (copies enqueued before the launch)
+import numpy as np
+import torch
+from paper_1808_00687_b200.decoder import BatchDecoder
+eq = [synth.random_posteriors(90 + i, 70, 30) for i in range(4)]
+T = np.full(4, 70, np.int32)
+off = np.arange(4, dtype=np.int64) * 70
+pin = torch.empty((280, 31), dtype=torch.float64, pin_memory=True)
+for p, o in zip(eq, off):
+    P.cost_table(p, out=pin.numpy()[o:o + 70])
+blank = np.concatenate([p.rows[:, 0] for p in eq])
+dec = BatchDecoder(g, 0)
+cfg = P.DecodeConfig(beam=9.0, max_active=150, mode="fsd")
+res = dec.decode_host(pin.numpy(), off, T, blank, cfg, "fsd").decode_results()
+assert dec.last_transfer()[1] == 2, dec.last_transfer()
+for p, r in zip(eq, res):
+    o = O.decode(g, P.cost_table(p), p.rows[:, 0], beam=9.0, max_active=150, mode="fsd")
+    assert (r.total_cost, r.olabels, r.ilabels, r.search_steps, r.tokens_expanded,
+            r.reached_final, r.died_at_step) == o.astuple(), (r, o)
 print("OK")
 """ % ROOT
 
@@ -43,7 +62,8 @@ print("OK")
 def test_streaming_decode_with_blocking_launches(cuda):
     """CUDA_LAUNCH_BLOCKING=1 makes every launch return only after its kernel finished (as
     under ncu or compute-sanitizer).  The cost-row producers start before the launch, so the
-    streaming kernel still gets its rows and decode() completes with the oracle's results."""
+    streaming kernel still gets its rows and decode() completes with the oracle's results; the
+    FSD H2D pipeline's copies are all enqueued before its launch."""
     env = dict(os.environ, CUDA_LAUNCH_BLOCKING="1")
     r = subprocess.run([sys.executable, "-c", _CHILD], env=env, capture_output=True, text=True,
                        timeout=600)
