@@ -288,6 +288,10 @@ int wb_decode_stream(wb_decoder_t d, int32_t n_utts, const double *costs, const 
 void wb_gather_rows(const double *src, int64_t src_ld, const int32_t *idx, int64_t n, int32_t col0,
                     int32_t ncols, double *dst, int64_t dst_ld, int32_t dst_col0);
 int wb_decode_finish(wb_decoder_t d, wb_utt_result *results, int32_t *olabels, int32_t *ilabels);
+/* The CSR arc order of Wfst (wfst.py:182): `order` receives the permutation that sorts the arcs
+ * stably by (src, ilabel, dst, olabel, weight).  States and labels must be >= 0. */
+int wb_sort_arcs(int64_t n, const int32_t *src, const int32_t *ilabel, const int32_t *dst,
+                 const int32_t *olabel, const double *weight, int64_t *order);
 
 /*
  * parse_wfst_text (wfst.py:315-378): AT&T transducer text -> arc arrays in file order, finals

@@ -96,7 +96,7 @@ EXPORTED = ("wb_last_error", "wb_version", "wb_device_count", "wb_graph_create",
             "wb_lattice_split", "wb_decode_stream", "wb_decode_finish", "wb_wfst_parse_text",
             "wb_parsed_wfst_free", "wb_gather_rows", "wb_post1_info", "wb_post1_read", "wb_last_launch",
             "wb_checks_enabled", "wb_check_report", "wb_claim_log", "wb_lattice_format_text",
-            "wb_lattice_parse_text", "wb_text_free", "wb_decoder_lanes")
+            "wb_lattice_parse_text", "wb_text_free", "wb_decoder_lanes", "wb_sort_arcs")
 
 
 _checked_lib = None
@@ -136,6 +136,7 @@ def _open(path):
     L.wb_decode_stream.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_int32, C.c_void_p, C.POINTER(Config), C.c_int32,
                                    C.c_void_p, C.c_void_p, C.c_void_p]
+    L.wb_sort_arcs.argtypes = [C.c_int64] + [C.c_void_p] * 6
     L.wb_gather_rows.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32,
                                  C.c_int32, C.c_void_p, C.c_int64, C.c_int32]
     L.wb_gather_rows.restype = None

@@ -8,6 +8,7 @@
 //
 // Input lines are '\n' separated with ASCII whitespace (the Python shim normalises other line
 // breaks); blank lines and lines starting with '#' are skipped.
+#include <charconv>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -39,9 +40,6 @@ extern "C" {
 
 int wb_lattice_format_text(const wb_lattice_arrays *lat, char **text, int64_t *len) {
     if (!lat || !text || !len) return wb_internal_set_error(WB_ERR_VALUE, "null argument");
-    std::string out;
-    out.reserve((size_t)(lat->n_nodes * 24 + lat->n_arcs * 64 + 64));
-    out += "LATTICE nodes=" + std::to_string(lat->n_nodes) + " arcs=" + std::to_string(lat->n_arcs) + "\n";
     std::vector<double> fw((size_t)lat->n_nodes, 0.0);
     std::vector<char> is_final((size_t)lat->n_nodes, 0);
     for (int64_t k = 0; k < lat->n_finals; ++k) {
@@ -50,26 +48,52 @@ int wb_lattice_format_text(const wb_lattice_arrays *lat, char **text, int64_t *l
         is_final[nid] = 1;
         fw[nid] = lat->final_w[k];
     }
+    // one pass into a buffer sized for the longest lines: a node line <= 3 x 20 + 48 bytes,
+    // an arc line <= 4 x 20 + 2 x 32 + 8
+    const size_t cap = 64 + (size_t)lat->n_nodes * 112 + (size_t)lat->n_arcs * 160;
+    char *buf = (char *)std::malloc(cap + 1);
+    if (!buf) return wb_internal_set_error(WB_ERR_NOMEM, "lattice text buffer");
+    char *p = buf;
+    auto put = [&](const char *s) { const size_t n = std::strlen(s); std::memcpy(p, s, n); p += n; };
+    auto num = [&](long long v) { p = std::to_chars(p, p + 24, v).ptr; };
+    put("LATTICE nodes=");
+    num(lat->n_nodes);
+    put(" arcs=");
+    num(lat->n_arcs);
+    *p++ = '\n';
     for (int64_t i = 0; i < lat->n_nodes; ++i) {
-        out += "N " + std::to_string(i) + " " + std::to_string(lat->node_state[i]) + " " +
-               std::to_string(lat->node_step[i]);
+        *p++ = 'N';
+        *p++ = ' ';
+        num(i);
+        *p++ = ' ';
+        num(lat->node_state[i]);
+        *p++ = ' ';
+        num(lat->node_step[i]);
         if (is_final[i]) {
-            out += " final ";
-            pytext::py_repr(fw[i], out);
+            put(" final ");
+            p = pytext::py_repr_to(fw[i], p);
         }
-        out.push_back('\n');
+        *p++ = '\n';
     }
     for (int64_t e = 0; e < lat->n_arcs; ++e) {
-        out += "A " + std::to_string(lat->arc_from[e]) + " " + std::to_string(lat->arc_to[e]) + " " +
-               std::to_string(lat->arc_il[e]) + " " + std::to_string(lat->arc_ol[e]) + " ";
-        pytext::py_repr(lat->arc_g[e], out);
-        out.push_back(' ');
-        pytext::py_repr(lat->arc_a[e], out);
-        out.push_back('\n');
+        *p++ = 'A';
+        *p++ = ' ';
+        num(lat->arc_from[e]);
+        *p++ = ' ';
+        num(lat->arc_to[e]);
+        *p++ = ' ';
+        num(lat->arc_il[e]);
+        *p++ = ' ';
+        num(lat->arc_ol[e]);
+        *p++ = ' ';
+        p = pytext::py_repr_to(lat->arc_g[e], p);
+        *p++ = ' ';
+        p = pytext::py_repr_to(lat->arc_a[e], p);
+        *p++ = '\n';
     }
-    *text = (char *)std::malloc(out.size() + 1);
-    std::memcpy(*text, out.data(), out.size() + 1);
-    *len = (int64_t)out.size();
+    *p = '\0';
+    *text = buf;
+    *len = (int64_t)(p - buf);
     return WB_OK;
 }
 

@@ -97,47 +97,67 @@ inline bool py_float(const char *b, const char *e, double *v) {
 }
 
 // repr(float): the shortest digits that round-trip, fixed notation for decimal exponents in
-// [-4, 16), else d.ddde+XX; always a '.0' on integral fixed values.
-inline void py_repr(double x, std::string &out) {
-    if (std::isnan(x)) { out += "nan"; return; }
-    if (std::isinf(x)) { out += x > 0 ? "inf" : "-inf"; return; }
-    char buf[64];
+// [-4, 16), else d.ddde+XX; always a '.0' on integral fixed values.  Writes at p (at most 32
+// bytes) and returns the end.
+inline char *py_repr_to(double x, char *p) {
+    if (std::isnan(x)) { std::memcpy(p, "nan", 3); return p + 3; }
+    if (std::isinf(x)) {
+        if (x > 0) { std::memcpy(p, "inf", 3); return p + 3; }
+        std::memcpy(p, "-inf", 4);
+        return p + 4;
+    }
+    char buf[48];
     const auto r = std::to_chars(buf, buf + sizeof buf - 1, x, std::chars_format::scientific);
     *r.ptr = '\0';   // to_chars does not terminate; the exponent is read with atoi
-    const char *p = buf, *end = r.ptr;
-    if (*p == '-') { out.push_back('-'); ++p; }
-    const char *ep = (const char *)std::memchr(p, 'e', end - p);
-    std::string digits;
-    for (const char *q = p; q < ep; ++q)
-        if (*q != '.') digits.push_back(*q);
+    const char *q = buf, *end = r.ptr;
+    if (*q == '-') { *p++ = '-'; ++q; }
+    const char *ep = (const char *)std::memchr(q, 'e', end - q);
+    char digits[24];
+    int nd = 0;
+    for (const char *t = q; t < ep; ++t)
+        if (*t != '.') digits[nd++] = *t;
     const int ex = std::atoi(ep + 1);
-    const int nd = (int)digits.size();
     if (ex >= -4 && ex < 16) {
         if (ex >= 0) {
             if (nd <= ex + 1) {
-                out += digits;
-                out.append((size_t)(ex + 1 - nd), '0');
-                out += ".0";
+                std::memcpy(p, digits, nd);
+                p += nd;
+                for (int z = 0; z < ex + 1 - nd; ++z) *p++ = '0';
+                *p++ = '.';
+                *p++ = '0';
             } else {
-                out.append(digits, 0, (size_t)ex + 1);
-                out.push_back('.');
-                out.append(digits, (size_t)ex + 1, std::string::npos);
+                std::memcpy(p, digits, ex + 1);
+                p += ex + 1;
+                *p++ = '.';
+                std::memcpy(p, digits + ex + 1, nd - ex - 1);
+                p += nd - ex - 1;
             }
         } else {
-            out += "0.";
-            out.append((size_t)(-ex - 1), '0');
-            out += digits;
+            *p++ = '0';
+            *p++ = '.';
+            for (int z = 0; z < -ex - 1; ++z) *p++ = '0';
+            std::memcpy(p, digits, nd);
+            p += nd;
         }
     } else {
-        out.push_back(digits[0]);
+        *p++ = digits[0];
         if (nd > 1) {
-            out.push_back('.');
-            out.append(digits, 1, std::string::npos);
+            *p++ = '.';
+            std::memcpy(p, digits + 1, nd - 1);
+            p += nd - 1;
         }
-        char eb[16];
-        std::snprintf(eb, sizeof eb, "e%c%02d", ex < 0 ? '-' : '+', ex < 0 ? -ex : ex);
-        out += eb;
+        const int ax = ex < 0 ? -ex : ex;
+        *p++ = 'e';
+        *p++ = ex < 0 ? '-' : '+';
+        if (ax < 10) *p++ = '0';
+        p = std::to_chars(p, p + 8, ax).ptr;
     }
+    return p;
+}
+
+inline void py_repr(double x, std::string &out) {
+    char b[40];
+    out.append(b, py_repr_to(x, b));
 }
 
 inline std::string py_repr(double x) {

@@ -11,6 +11,7 @@
 // Input is one line per '\n' (an optional '\r' before it) with ASCII-whitespace separated
 // fields: the Python shim normalises text that uses other line breaks or Unicode whitespace
 // before calling.  Errors report the 1-based line number and a message (wb_last_error).
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -179,6 +180,40 @@ int wb_wfst_parse_text(const char *text, int64_t len, int32_t allow_negative_wei
     out->final_state = dup32(final_order);
     out->final_weight = (double *)std::malloc(sizeof(double) * std::max<size_t>(final_order.size(), 1));
     for (size_t k = 0; k < final_order.size(); ++k) out->final_weight[k] = finals[final_order[k]];
+    return WB_OK;
+}
+
+// The CSR arc order (wfst.py:182): a stable sort by (src, ilabel, dst, olabel, weight).  States
+// and labels are non-negative (checked by the caller), so (src, ilabel) and (dst, olabel) pack
+// into order-preserving 64-bit keys; equal keys keep their input order (the index breaks ties).
+int wb_sort_arcs(int64_t n, const int32_t *src, const int32_t *ilabel, const int32_t *dst,
+                 const int32_t *olabel, const double *weight, int64_t *order) {
+    if (n < 0 || (n > 0 && (!src || !ilabel || !dst || !olabel || !weight || !order)))
+        return wb_internal_set_error(WB_ERR_VALUE, "null argument");
+    struct Key {
+        uint64_t a, b;
+        double w;
+        int64_t i;
+    };
+    std::vector<Key> k((size_t)n);
+    bool sorted = true;
+    for (int64_t i = 0; i < n; ++i) {
+        k[i] = Key{((uint64_t)(uint32_t)src[i] << 32) | (uint32_t)ilabel[i],
+                   ((uint64_t)(uint32_t)dst[i] << 32) | (uint32_t)olabel[i], weight[i], i};
+        if (i && sorted) {
+            const Key &x = k[i - 1], &y = k[i];
+            sorted = x.a < y.a || (x.a == y.a && (x.b < y.b || (x.b == y.b && !(y.w < x.w))));
+        }
+    }
+    if (!sorted)
+        std::sort(k.begin(), k.end(), [](const Key &x, const Key &y) {
+            if (x.a != y.a) return x.a < y.a;
+            if (x.b != y.b) return x.b < y.b;
+            if (x.w < y.w) return true;
+            if (y.w < x.w) return false;
+            return x.i < y.i;
+        });
+    for (int64_t i = 0; i < n; ++i) order[i] = k[i].i;
     return WB_OK;
 }
 

@@ -646,10 +646,8 @@ def parse_lattice_text(text: str) -> Lattice:
     """Inverse of ``format_lattice_text`` (native reader); ``LatticeError`` for malformed
     text, ``ValueError`` for a bad number, as the reference raises them."""
     from . import _native as N
-    from .wfst import _ODD_BREAKS
-    if not text.isascii() or _ODD_BREAKS.search(text):
-        text = "\n".join(" ".join(line.split()) for line in text.splitlines())
-    data = text.encode("utf-8")
+    from .wfst import _native_text
+    data = _native_text(text)
     out = N.LatticeArrays()
     L = N.load()
     rc = L.wb_lattice_parse_text(data, len(data), C.byref(out))

@@ -18,7 +18,6 @@ from __future__ import annotations
 
 import ctypes as C
 import math
-import re
 from dataclasses import dataclass
 
 import numpy as np
@@ -186,8 +185,8 @@ class Wfst:
                 raise WfstError("final weight array must have one entry per state")
             if np.isnan(fw).any():
                 raise WfstError("a final weight is NaN")
-        # sort key (src, ilabel, dst, olabel, weight) -- wfst.py:182; lexsort is stable
-        order = np.lexsort((w, ol, dst, il, src))
+        # sort key (src, ilabel, dst, olabel, weight) -- wfst.py:182, stable
+        order = _arc_order(src, il, dst, ol, w)
         self.num_states = S
         self.start = int(start)
         self.dst = np.ascontiguousarray(dst[order], dtype=np.int32)
@@ -421,8 +420,39 @@ def _cycle_weight(cyc, u, v, wt) -> float:
     return total
 
 
-_ODD_BREAKS = re.compile("[\u000b\u000c\u001c-\u001f\u0085\u00a0\u1680\u2000-\u200a\u2028\u2029"
-                         "\u202f\u205f\u3000]|\r(?!\n)")
+def _arc_order(src, il, dst, ol, w) -> np.ndarray:
+    """Permutation sorting the arcs stably by (src, ilabel, dst, olabel, weight): the native
+    packed-key sort (a no-op check when the input is already in order), else np.lexsort."""
+    n = len(src)
+    if n >= 4096:
+        try:
+            from . import _native as N
+            L = N.load()
+        except Exception:   # no library (a CPU-only checkout): numpy
+            L = None
+        if L is not None:
+            arrs = [np.ascontiguousarray(a, dtype=t) for a, t in
+                    ((src, np.int32), (il, np.int32), (dst, np.int32), (ol, np.int32), (w, np.float64))]
+            order = np.empty(n, np.int64)
+            N.check(L.wb_sort_arcs(n, *(a.ctypes.data for a in arrs), order.ctypes.data), "sort arcs")
+            return order
+    return np.lexsort((w, ol, dst, il, src))
+
+
+# ASCII bytes the native tokenizers do not treat as Python does (vertical tab, form feed, the
+# \x1c-\x1f separators, a lone carriage return); any non-ASCII text is normalised too
+_ODD_ASCII = (b"\x0b", b"\x0c", b"\x1c", b"\x1d", b"\x1e", b"\x1f")
+
+
+def _native_text(text: str) -> bytes:
+    """``text`` as the native tokenizers read it: '\\n' lines with ASCII-space fields exactly
+    where Python's ``splitlines`` / ``split`` would find them."""
+    if text.isascii():
+        data = text.encode("ascii")
+        if not any(c in data for c in _ODD_ASCII) and data.count(b"\r") == data.count(b"\r\n"):
+            return data
+    return "\n".join(" ".join(line.split()) for line in text.splitlines()).encode("utf-8")
+
 
 
 def parse_wfst_text(text: str, isyms: SymbolTable | None = None,
@@ -436,10 +466,7 @@ def parse_wfst_text(text: str, isyms: SymbolTable | None = None,
     ``SymbolError`` as the reference does."""
     from . import _native as N
     L = N.load()
-    if not text.isascii() or _ODD_BREAKS.search(text):
-        # Python line breaks and Unicode whitespace the native tokenizer does not know
-        text = "\n".join(" ".join(line.split()) for line in text.splitlines())
-    data = text.encode("utf-8")
+    data = _native_text(text)   # Python line breaks / Unicode whitespace normalised
     tabs = [t.format().encode("utf-8") if t is not None else None for t in (isyms, osyms)]
     out = N.ParsedWfst()
     rc = L.wb_wfst_parse_text(data, len(data), int(bool(allow_negative_weights)),
