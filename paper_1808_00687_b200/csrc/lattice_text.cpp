@@ -102,7 +102,9 @@ void wb_text_free(char *text) { std::free(text); }
 int wb_lattice_parse_text(const char *text, int64_t len, wb_lattice_arrays *out) {
     if (!text || !out || len < 0) return wb_internal_set_error(WB_ERR_VALUE, "null argument");
     std::memset(out, 0, sizeof(*out));
-    std::vector<std::string> lines;
+    // lines and fields as [begin, end) ranges into `text`: no per-line allocation
+    struct Tok { const char *b, *e; };
+    std::vector<Tok> lines;
     for (const char *p = text, *end = text + len; p < end;) {
         const char *eol = (const char *)std::memchr(p, '\n', end - p);
         if (!eol) eol = end;
@@ -110,65 +112,78 @@ int wb_lattice_parse_text(const char *text, int64_t len, wb_lattice_arrays *out)
         p = eol + 1;
         while (b < e && is_ws(*b)) ++b;
         while (e > b && is_ws(e[-1])) --e;
-        if (b < e && *b != '#') lines.emplace_back(b, e);
+        if (b < e && *b != '#') lines.push_back(Tok{b, e});
     }
     if (lines.empty()) return WB_OK;   // EMPTY_LATTICE
+    auto str = [](Tok t) { return std::string(t.b, t.e); };
     auto lat_err = [](const std::string &m) { return wb_internal_set_error(WB_ERR_LATTICE, m.c_str()); };
-    auto fields_of = [](const std::string &s) {
-        std::vector<std::string> f;
-        for (size_t i = 0; i < s.size();) {
-            while (i < s.size() && is_ws(s[i])) ++i;
-            size_t j = i;
-            while (j < s.size() && !is_ws(s[j])) ++j;
-            if (j > i) f.emplace_back(s, i, j - i);
-            i = j;
+    constexpr int MAXF = 8;
+    auto fields_of = [](Tok s, Tok *f) {   // returns the field count (fields beyond MAXF uncounted past MAXF + 1)
+        int n = 0;
+        for (const char *p = s.b; p < s.e;) {
+            while (p < s.e && is_ws(*p)) ++p;
+            const char *q = p;
+            while (q < s.e && !is_ws(*q)) ++q;
+            if (q > p) {
+                if (n < MAXF) f[n] = Tok{p, q};
+                if (++n > MAXF) return n;
+            }
+            p = q;
         }
-        return f;
+        return n;
+    };
+    auto eq = [](Tok t, const char *w) {
+        const size_t n = std::strlen(w);
+        return (size_t)(t.e - t.b) == n && std::memcmp(t.b, w, n) == 0;
     };
     // int() / float() failures surface as the ValueError Python raises
-    auto as_int = [](const std::string &s, long long *v) {
-        return pytext::py_int(s.data(), s.data() + s.size(), v);
+    auto as_int = [](Tok t, long long *v) { return pytext::py_int(t.b, t.e, v); };
+    auto as_float = [](Tok t, double *v) { return pytext::py_float(t.b, t.e, v); };
+    auto int_err = [&](Tok t) {
+        return wb_internal_set_error(WB_ERR_VALUE, ("invalid literal for int() with base 10: " + q(str(t))).c_str());
     };
-    auto as_float = [](const std::string &s, double *v) {
-        return pytext::py_float(s.data(), s.data() + s.size(), v);
+    auto float_err = [&](Tok t) {
+        return wb_internal_set_error(WB_ERR_VALUE, ("could not convert string to float: " + q(str(t))).c_str());
     };
-    auto int_err = [](const std::string &s) {
-        return wb_internal_set_error(WB_ERR_VALUE, ("invalid literal for int() with base 10: " + q(s)).c_str());
-    };
-    auto float_err = [](const std::string &s) {
-        return wb_internal_set_error(WB_ERR_VALUE, ("could not convert string to float: " + q(s)).c_str());
-    };
-    const std::vector<std::string> head = fields_of(lines[0]);
+    Tok head[MAXF];
+    const int nh = fields_of(lines[0], head);
     long long n_nodes = 0, n_arcs = 0;
-    if (head.size() != 3 || head[0] != "LATTICE" || head[1].rfind("nodes=", 0) != 0 ||
-        head[2].rfind("arcs=", 0) != 0 || !as_int(head[1].substr(6), &n_nodes) ||
-        !as_int(head[2].substr(5), &n_arcs))
-        return lat_err("bad lattice header " + q(lines[0]));
+    if (nh != 3 || !eq(head[0], "LATTICE") || head[1].e - head[1].b < 6 ||
+        std::memcmp(head[1].b, "nodes=", 6) != 0 || head[2].e - head[2].b < 5 ||
+        std::memcmp(head[2].b, "arcs=", 5) != 0 || !as_int(Tok{head[1].b + 6, head[1].e}, &n_nodes) ||
+        !as_int(Tok{head[2].b + 5, head[2].e}, &n_arcs))
+        return lat_err("bad lattice header " + q(str(lines[0])));
     std::vector<int32_t> st, sp;
     std::vector<int64_t> fn, af, at, tie;
     std::vector<double> fwv, ag, aa;
     std::vector<int32_t> ail, aol;
+    if (n_nodes > 0 && n_nodes < (1ll << 31)) { st.reserve(n_nodes); sp.reserve(n_nodes); }
+    if (n_arcs > 0 && n_arcs < (1ll << 31)) {
+        af.reserve(n_arcs); at.reserve(n_arcs); tie.reserve(n_arcs); ag.reserve(n_arcs);
+        aa.reserve(n_arcs); ail.reserve(n_arcs); aol.reserve(n_arcs);
+    }
+    Tok f[MAXF];
     for (size_t k = 1; k < lines.size(); ++k) {
-        const std::string &ln = lines[k];
-        const std::vector<std::string> f = fields_of(ln);
-        if (f[0] == "N") {
-            if ((f.size() != 4 && f.size() != 6) || (f.size() == 6 && f[4] != "final"))
-                return lat_err("bad node line " + q(ln));
+        const Tok ln = lines[k];
+        const int nf = fields_of(ln, f);
+        if (eq(f[0], "N")) {
+            if ((nf != 4 && nf != 6) || (nf == 6 && !eq(f[4], "final")))
+                return lat_err("bad node line " + q(str(ln)));
             long long id, s, t;
             if (!as_int(f[1], &id)) return int_err(f[1]);
-            if (id != (long long)st.size()) return lat_err("node ids must be dense and ordered; got " + q(ln));
+            if (id != (long long)st.size()) return lat_err("node ids must be dense and ordered; got " + q(str(ln)));
             if (!as_int(f[2], &s)) return int_err(f[2]);
             if (!as_int(f[3], &t)) return int_err(f[3]);
             st.push_back((int32_t)s);
             sp.push_back((int32_t)t);
-            if (f.size() == 6) {
+            if (nf == 6) {
                 double w;
                 if (!as_float(f[5], &w)) return float_err(f[5]);
                 fn.push_back(id);
                 fwv.push_back(w);
             }
-        } else if (f[0] == "A") {
-            if (f.size() != 7) return lat_err("bad arc line " + q(ln));
+        } else if (eq(f[0], "A")) {
+            if (nf != 7) return lat_err("bad arc line " + q(str(ln)));
             long long v[4];
             for (int i = 0; i < 4; ++i)
                 if (!as_int(f[1 + i], &v[i])) return int_err(f[1 + i]);
@@ -183,7 +198,7 @@ int wb_lattice_parse_text(const char *text, int64_t len, wb_lattice_arrays *out)
             ag.push_back(g);
             aa.push_back(a);
         } else {
-            return lat_err("unrecognized lattice line " + q(ln));
+            return lat_err("unrecognized lattice line " + q(str(ln)));
         }
     }
     if ((long long)st.size() != n_nodes || (long long)af.size() != n_arcs)

@@ -37,6 +37,17 @@ inline bool digit_run(const char *b, const char *e, std::string &out, const char
 
 // Python int(token) for a token without surrounding whitespace (|value| < 1e18).
 inline bool py_int(const char *b, const char *e, long long *v) {
+    {   // fast path: [sign] 1-18 plain digits
+        const char *q = b;
+        const bool ng = q < e && *q == '-';
+        if (q < e && (*q == '+' || *q == '-')) ++q;
+        if (q < e && e - q <= 18) {
+            long long x = 0;
+            const char *t = q;
+            while (t < e && is_digit(*t)) x = x * 10 + (*t++ - '0');
+            if (t == e) { *v = ng ? -x : x; return true; }
+        }
+    }
     bool neg = false;
     if (b < e && (*b == '+' || *b == '-')) neg = *b++ == '-';
     std::string digits;
@@ -60,6 +71,22 @@ inline bool ieq(const char *b, const char *e, const char *word) {
 // (digits [. [digits]] | . digits) [(e|E) [sign] digits], underscores between digits;
 // correctly rounded (strtod), like CPython.
 inline bool py_float(const char *b, const char *e, double *v) {
+    {   // fast path: no underscores, letters only as the exponent mark -> from_chars (also
+        // correctly rounded); anything it does not consume exactly takes the full path
+        bool plain = b < e;
+        for (const char *t = b; t < e && plain; ++t)
+            plain = is_digit(*t) || *t == '.' || *t == 'e' || *t == 'E' || *t == '+' || *t == '-';
+        if (plain) {
+            const char *q = b;
+            const bool ng = *q == '-';
+            if (*q == '+' || *q == '-') ++q;
+            if (q < e && *q != '+' && *q != '-') {
+                double x;
+                const auto r = std::from_chars(q, e, x, std::chars_format::general);
+                if (r.ec == std::errc() && r.ptr == e) { *v = ng ? -x : x; return true; }
+            }
+        }
+    }
     std::string s;
     if (b < e && (*b == '+' || *b == '-')) s.push_back(*b++);
     if (ieq(b, e, "inf") || ieq(b, e, "infinity")) {
