@@ -711,15 +711,21 @@ static int decode_impl(wb_decoder_t d, int32_t n, const double *costs, const int
             CUDA_TRY(cudaStreamWaitEvent(d->copy_st, d->cev_a, 0));
             CUDA_TRY(cudaMemsetAsync(d->dma_ready, 0, sizeof(int) * nn, d->copy_st));
             CUDA_TRY(cudaEventRecord(d->cev_b, d->copy_st));
+            // in the order the lanes consume them: a wave of `slots` utterances (the lanes take
+            // utterances from a queue in index order) at a time, its step chunks in turn
             const size_t rowb = sizeof(double) * (size_t)num_cols, pitch = rowb * (size_t)stride;
-            for (size_t k = 0; k < nch; ++k) {
-                const size_t off = rowb * ((size_t)row_offset[0] + (size_t)cut[k]);
-                CUDA_TRY(cudaMemcpy2DAsync(reinterpret_cast<char *>(d->h_costs) + off, pitch,
-                                           reinterpret_cast<const char *>(costs) + off, pitch,
-                                           rowb * (size_t)(cut[k + 1] - cut[k]), nn,
-                                           cudaMemcpyHostToDevice, d->copy_st));
-                CUDA_TRY(cudaMemcpyAsync(d->dma_ready, d->dma_counts + k * nn, sizeof(int) * nn,
-                                         cudaMemcpyHostToDevice, d->copy_st));
+            const size_t wave = (size_t)std::max(1, d->slots);
+            for (size_t u0 = 0; u0 < nn; u0 += wave) {
+                const size_t nu = std::min(wave, nn - u0);
+                for (size_t k = 0; k < nch; ++k) {
+                    const size_t off = rowb * ((size_t)row_offset[u0] + (size_t)cut[k]);
+                    CUDA_TRY(cudaMemcpy2DAsync(reinterpret_cast<char *>(d->h_costs) + off, pitch,
+                                               reinterpret_cast<const char *>(costs) + off, pitch,
+                                               rowb * (size_t)(cut[k + 1] - cut[k]), nu,
+                                               cudaMemcpyHostToDevice, d->copy_st));
+                    CUDA_TRY(cudaMemcpyAsync(d->dma_ready + u0, d->dma_counts + k * nn + u0,
+                                             sizeof(int) * nu, cudaMemcpyHostToDevice, d->copy_st));
+                }
             }
             CUDA_TRY(cudaEventRecord(d->cev_c, d->copy_st));
             CUDA_TRY(cudaStreamWaitEvent(st, d->cev_b, 0));
