@@ -491,8 +491,9 @@ def main():
                "input_path": {1: "pinned host cost table read zero-copy by the kernel (one staged "
                                  "row per search step, overlapped with the search)",
                               2: "pinned host cost table copied H2D by the copy engine in step-range "
-                                 "chunks (8, 16, then 32 steps of every utterance) while the kernel "
-                                 "decodes; the kernel polls per-utterance ready counts"}.get(
+                                 "chunks (8, 16, then 32 steps; one wave of lanes' utterances at a "
+                                 "time) while the kernel decodes; the kernel polls per-utterance "
+                                 "ready counts"}.get(
                                      zero_copy, "pinned host cost table copied H2D, then decode")}
 
     # ---------------- e2e from posterior matrices (decode_batch's path): frame_costs
