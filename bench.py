@@ -482,12 +482,21 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         h2d, zero_copy = dec.last_transfer()   # bytes copied + rows read zero-copy
+        # the end-to-end results are the device path's, field by field (same inputs)
+        keys = ("total_cost", "tokens_expanded", "search_steps", "reached_final", "died_at_step",
+                "final_state", "final_step", "n_olabels", "n_ilabels", "status")
+        dol = ol_d.cpu().numpy().reshape(utts, -1)
+        dil = il_d.cpu().numpy().reshape(utts, -1)
+        same = all(np.array_equal(out.results[k], res[k]) for k in keys) and all(
+            np.array_equal(out.olabels[u, :res["n_olabels"][u]], dol[u, :res["n_olabels"][u]]) and
+            np.array_equal(out.ilabels[u, :res["n_ilabels"][u]], dil[u, :res["n_ilabels"][u]])
+            for u in range(utts))
         d2h = out.results.nbytes + out.olabels.nbytes + out.ilabels.nbytes
         if lat_stats:   # trimmed lattice pools: node 8 B, arc 16 + 8 B, meta 48 B / utt
             d2h += 8 * lat_stats["nodes"] + 24 * lat_stats["arcs"] + 48 * utts
         e2e = {"value": frames_all * args.steps / (e_ms / 1e3), "unit": "frames/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": e_ms / args.steps,
+               "ms_per_step": e_ms / args.steps, "results_equal_device_path": bool(same),
                "input_path": {1: "pinned host cost table read zero-copy by the kernel (one staged "
                                  "row per search step, overlapped with the search)",
                               2: "pinned host cost table copied H2D by the copy engine in step-range "
