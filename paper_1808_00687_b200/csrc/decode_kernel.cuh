@@ -94,7 +94,8 @@ struct GraphDev {
 
 struct WorkDev {
     Slot *slot;           // [slots][S]   recombination slots (EMPTY between steps)
-    u32 *cand_of;         // [slots][S]   state -> candidate index (epsilon graphs)
+    u64 *cand_of;         // [slots][S]   state -> step stamp << 32 | candidate index (epsilon
+                          //              graphs; one store, so a reader sees both or neither)
     u32 *qtag;            // [slots][S]   epsilon frontier dedup tags
     u32 *tag_ctr;         // [slots]
     u32 *cand_state;      // [slots][cap]
@@ -207,6 +208,8 @@ struct Smem {
     u32 ls_flag[8];     // lane barrier: epoch of the last barrier each peer CTA arrived at
     u32 ls_epoch;       // lane barriers passed by this CTA
     int x_ck, x_cs;     // kept / surviving candidates of this CTA (compaction bases)
+    int x_eps_rounds;   // epsilon-closure rounds this CTA ran this step
+    u32 stamp;          // this step's stamp in cand_of (the lane's dedup tag at the step start)
     u64 x_run_min;      // this CTA's exact emitting minimum (expand)
     // per-utterance counters kept out of the step loop's registers (with the 64-register
     // budget every value live across the phase calls was spilled around each call)
@@ -430,7 +433,7 @@ struct Lane {
     __device__ __forceinline__ size_t so() const { return lane() * (size_t)ws.S; }
     __device__ __forceinline__ size_t co() const { return lane() * (size_t)ws.lcap; }
     __device__ __forceinline__ Slot *slot() const { return ws.slot + so(); }
-    __device__ __forceinline__ u32 *cand_of() const { return ws.cand_of + so(); }
+    __device__ __forceinline__ u64 *cand_of() const { return ws.cand_of + so(); }
     __device__ __forceinline__ u32 *qtag() const { return ws.qtag + so(); }
     __device__ __forceinline__ u32 *cand_state() const { return ws.cand_state + co(); }
     __device__ __forceinline__ u64 *cand_ap() const { return ws.cand_ap + co(); }
@@ -478,7 +481,7 @@ __device__ __forceinline__ int warp_append(bool first, u32 d, int4 rng, bool pus
         if (loc < ws.cap) {
             c.cand_state()[idx] = d;
             if (g.has_eps && rng.x < rng.y) {
-                c.cand_of()[d] = (u32)idx;
+                c.cand_of()[d] = ((u64)sh.stamp << 32) | (u32)idx;
                 pf = push;
             }
         } else {
@@ -993,28 +996,30 @@ WB_PHASE_FN __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev &
     Slot *slot = c.slot();
     const Slot empty = {EMPTY_KEY, 0xFFFFFFFFu, 0xFFFFFFFFu};
     int n_rounds = 0;
+    // a candidate overflow anywhere in the lane leaves frontier states without a candidate
+    // index: the step has failed (WB_CAP_CANDIDATES)
+    auto lane_overflow = [&]() {
+        int ovf = *(volatile int *)&sh.overflow;
+        for (int q = 1; q < K; ++q) ovf |= *(volatile int *)peer(&sh.overflow, (r + q) & (K - 1));
+        return ovf != 0;
+    };
     // Round k consumes the frontier pushed in round k-1 (round 0: by expand) from buffer k & 1
-    // and pushes into the other; each CTA of a cluster lane works its own frontier region and
-    // the round ends at a lane barrier, after which every CTA reads every CTA's count.
+    // and pushes into the other.  Each CTA of a cluster lane drains its own frontier region with
+    // CTA barriers (a push always goes to the pusher's region, so no CTA can create work for
+    // another); the lane meets once, after the last CTA is done.  Dedup tags are per CTA and
+    // round (tag_in + 1 + rounds * K + rank), so one CTA's push never suppresses another's.
     for (int rounds = 0;; ++rounds) {
         const int par = rounds & 1;
         const int n_front = min(sh.nfr[par], ws.cap);  // overflowed pushes were dropped (flagged)
-        int total = n_front, ovf = sh.overflow;
-        for (int q = 1; q < K; ++q) {
-            const int o = (r + q) & (K - 1);
-            total += *peer(&sh.nfr[par], o);
-            ovf |= *peer(&sh.overflow, o);
-        }
-        if (total == 0) { n_rounds = rounds; break; }
-        // a candidate overflow leaves frontier states without a candidate index: the step
-        // has failed (WB_CAP_CANDIDATES), stop before following stale indices
-        if (ovf) { status = wb_cap(WB_CAP_CANDIDATES); break; }
+        n_rounds = rounds;
+        if (n_front == 0) break;
+        // stop before following stale indices
+        if (lane_overflow()) { status = wb_cap(WB_CAP_CANDIDATES); break; }
         if (rounds >= MAX_EPS_ROUNDS) { status = wb_cap(WB_CAP_EPS_ROUNDS); break; }
         // the other buffer's count was last read before the barrier that ended the last round
         if (threadIdx.x == 0) sh.nfr[par ^ 1] = 0;
         __syncthreads();
-        const u32 tag = tag_cur + 1u;
-        tag_cur = tag;
+        const u32 tag = tag_in + 1u + (u32)rounds * (u32)K + (u32)r;
         const u32 *fin = c.front(par) + cbase;
         u32 *fout = c.front(par ^ 1) + cbase;
         const int4 *frin = c.frng(par) + cbase;
@@ -1032,7 +1037,17 @@ WB_PHASE_FN __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev &
                 uu = fin[i];
                 const int4 fe = frin[i];
                 Slot us = ld_slot(&slot[uu]);
-                ui = fe.x >= 0 ? (u32)fe.x : min(ldx<KC>(&c.cand_of()[uu]), (u32)ws.lcap - 1u);
+                if (fe.x >= 0) {
+                    ui = (u32)fe.x;
+                } else {
+                    // the state's candidate index, possibly registered by another CTA that has
+                    // not published it yet: valid once it carries this step's stamp
+                    for (;;) {
+                        const u64 co = ldx<KC>(&c.cand_of()[uu]);
+                        ui = min((u32)co, (u32)ws.lcap - 1u);
+                        if ((u32)(co >> 32) == sh.stamp || lane_overflow()) break;
+                    }
+                }
                 lo = fe.y;
                 deg = fe.z - fe.y;
                 ucost = key_cost(us.key);
@@ -1092,8 +1107,16 @@ WB_PHASE_FN __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev &
                 }
             }
         }
-        lane_sync<BLOCK>(K);
+        __syncthreads();
     }
+    // every CTA's relaxations have landed before the gather; the next step's tags start above
+    // every tag any CTA used
+    if (threadIdx.x == 0) sh.x_eps_rounds = n_rounds;
+    lane_sync<BLOCK>(K);
+    int max_rounds = n_rounds;
+    for (int q = 1; q < K; ++q)
+        max_rounds = max(max_rounds, *(volatile int *)&peer(&sh, (r + q) & (K - 1))->x_eps_rounds);
+    tag_cur = tag_in + (u32)(max_rounds + 1) * (u32)K;
     return EpsOut{tag_cur, e_eps, status, n_rounds};
 }
 
@@ -2040,6 +2063,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
 
         // ---- initial tokens: start entry + epsilon closure + prune (decoder.py:236-249)
         if (threadIdx.x == 0) {   // rank 0 holds the start entry as its candidate 0
+            sh.stamp = tag;
             sh.n_cand = 0;
             sh.overflow = 0;
             sh.nfr[0] = sh.nfr[1] = 0;
@@ -2050,7 +2074,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
                 __stcg(reinterpret_cast<ulonglong2 *>(&c.slot()[g.start]),
                        make_ulonglong2(k0, (u64)0u | ((u64)ROOT_PREV << 32)));
                 c.cand_state()[0] = (u32)g.start;
-                if (g.has_eps) c.cand_of()[g.start] = 0u;
+                if (g.has_eps) c.cand_of()[g.start] = (u64)sh.stamp << 32;
                 sh.n_cand = 1;
                 if (g.has_eps && g.start_rng.x < g.start_rng.y) {
                     c.front(0)[0] = (u32)g.start;
@@ -2120,6 +2144,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             int neg = !row_in_smem;  // acoustic costs of this row all >= 0? (checked while staging)
             if (threadIdx.x == 0) {
                 sh.n_cand = 0; sh.nfr[0] = sh.nfr[1] = 0; sh.overflow = 0; sh.n_log = 0;
+                sh.stamp = tag;   // registrations of this step (expand, closure) carry it
                 sh.run_min = EMPTY_KEY;
                 sh.next_chunk = BLOCK / 32;
                 // this CTA's prune accumulators (peers read them after the prune's barrier)

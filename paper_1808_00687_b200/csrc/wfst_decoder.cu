@@ -55,7 +55,8 @@ struct wb_decoder_s {
     int *chk_steps = nullptr;
     u64 arena_cap = 0;
     Slot *slot = nullptr;
-    u32 *cand_of = nullptr, *qtag = nullptr, *tag_ctr = nullptr;
+    u64 *cand_of = nullptr;
+    u32 *qtag = nullptr, *tag_ctr = nullptr;
     u32 *cand_state = nullptr, *cand_ca = nullptr;
     u64 *cand_ap = nullptr;
     u64 *cand_key = nullptr;
@@ -442,7 +443,7 @@ int wb_decoder_create(wb_graph_t g, const wb_decoder_opts *o, wb_decoder_t *out)
         CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
         double budget = 0.75 * (double)free_b;
         if (const char *mb = std::getenv("WB_MEM_BUDGET_GB")) budget = std::atof(mb) * 1e9;
-        const double per_lane = (double)g->S * (sizeof(Slot) + (g->has_eps ? 2 * sizeof(u32) : 0)) +
+        const double per_lane = (double)g->S * (sizeof(Slot) + (g->has_eps ? sizeof(u64) + sizeof(u32) : 0)) +
                                 (double)sizeof(u64) * (4 << 20);   // dense slots (+ eps maps), default arena
         const double per_cta = (double)d->cap * 96.0;               // candidate / token / frontier regions
         auto fits = [&](int lanes, int k) { return lanes * per_lane + lanes * k * per_cta <= budget; };
@@ -485,7 +486,8 @@ int wb_decoder_create(wb_graph_t g, const wb_decoder_opts *o, wb_decoder_t *out)
 #undef DA
     if (e == cudaSuccess) e = cudaMemset(d->slot, 0xFF, sizeof(Slot) * slots * S);
     if (e == cudaSuccess && g->has_eps) e = cudaMemset(d->qtag, 0, sizeof(u32) * slots * S);
-    if (e == cudaSuccess && g->has_eps) e = cudaMemset(d->cand_of, 0, sizeof(u32) * slots * S);
+    // stamp 0xFFFFFFFF: no step's (the lane's tags start at 0)
+    if (e == cudaSuccess && g->has_eps) e = cudaMemset(d->cand_of, 0xFF, sizeof(u64) * slots * S);
     if (e == cudaSuccess) e = cudaMemset(d->tag_ctr, 0, sizeof(u32) * slots);
 #ifdef WB_CHECKS
     if (e == cudaSuccess) e = cudaMemset(d->chk_claim, 0, sizeof(u32) * cslots * cap);
