@@ -1025,13 +1025,16 @@ WB_PHASE_FN __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev &
         const int4 *frin = c.frng(par) + cbase;
         int4 *frout = c.frng(par ^ 1) + cbase;
         int *nfout = &sh.nfr[par ^ 1];
-        const int nchunks = (n_front + 31) >> 5;
+        // a small frontier is spread over more warps (units of 8 entries): a round's latency is
+        // one pass over a unit's epsilon arcs
+        const int ush = n_front > 16 * NW ? 5 : 3, usz = 1 << ush;
+        const int nchunks = (n_front + usz - 1) >> ush;
         for (int ch = w; ch < nchunks; ch += NW) {
-            int i = (ch << 5) + l;
+            int i = (ch << ush) + l;
             u32 uu = 0, ui = 0;
             int lo = 0, deg = 0;
             double ucost = 0.0;
-            if (i < n_front) {
+            if (l < usz && i < n_front) {
                 // the entry carries the state's epsilon range (and its candidate index when the
                 // pusher knew it), so the arcs load alongside the slot
                 uu = fin[i];
