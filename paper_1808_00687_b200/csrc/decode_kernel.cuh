@@ -33,7 +33,10 @@
 
 namespace wb {
 
-constexpr int NB = 4096;             // prune histogram buckets
+#ifndef WB_NB
+#define WB_NB 2048
+#endif
+constexpr int NB = WB_NB;            // prune histogram buckets
 constexpr int GCAP = 1024;           // boundary-bucket members ranked in shared memory
 constexpr int ROW_SMEM_MAX = 16384;  // cost-row columns staged in shared memory (128 KB)
 constexpr u32 F_SURV = 1u, F_MARK = 2u, CA_NONE = 0xFFFFFFFFu;
