@@ -15,7 +15,7 @@
 //            (cost, src state, arc) total order (decoder.py:121-135).
 //   closure  frontier rounds over the epsilon arcs of improved states, epoch-tagged dedup
 //            (decoder.py:138-171; Jacobi form parallel.py:287-325).
-//   prune    exact beam + max-active cut without a sort: min/max reduce, a 4096-bucket value
+//   prune    exact beam + max-active cut without a sort: min/max reduce, a 2048-bucket value
 //            histogram in shared memory, exact (cost, state) rank inside the boundary bucket
 //            (radix-select fallback) (decoder.py:174-194).
 //   compact  candidate keys/flags live in shared memory; survivors and the epsilon-chain
