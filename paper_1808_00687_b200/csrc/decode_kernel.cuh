@@ -33,6 +33,12 @@
 
 namespace wb {
 
+#ifndef WB_EPS_UNIT_SPLIT
+#define WB_EPS_UNIT_SPLIT 8      // closure: frontiers above this many entries per warp use 32-entry units
+#endif
+#ifndef WB_EPS_UNIT_SHIFT
+#define WB_EPS_UNIT_SHIFT 3      // ... else units of 1 << this entries
+#endif
 #ifndef WB_NB
 #define WB_NB 2048
 #endif
@@ -1028,9 +1034,9 @@ WB_PHASE_FN __device__ EpsOut epsilon_closure(const GraphDev &g, const WorkDev &
         const int4 *frin = c.frng(par) + cbase;
         int4 *frout = c.frng(par ^ 1) + cbase;
         int *nfout = &sh.nfr[par ^ 1];
-        // a small frontier is spread over more warps (units of 8 entries): a round's latency is
-        // one pass over a unit's epsilon arcs
-        const int ush = n_front > 16 * NW ? 5 : 3, usz = 1 << ush;
+        // a small frontier (<= 8 entries per warp) is spread over more warps (units of 8
+        // entries): a round's latency is one pass over a unit's epsilon arcs
+        const int ush = n_front > WB_EPS_UNIT_SPLIT * NW ? 5 : WB_EPS_UNIT_SHIFT, usz = 1 << ush;
         const int nchunks = (n_front + usz - 1) >> ush;
         for (int ch = w; ch < nchunks; ch += NW) {
             int i = (ch << ush) + l;
