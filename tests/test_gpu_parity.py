@@ -301,3 +301,25 @@ def test_h2d_pipeline_fallbacks(cuda, monkeypatch):
             assert dec.decode_host(pinned.numpy(), off, T, blank, cfg, "fsd").decode_results() == r
             assert dec.last_transfer()[1] == 1
             monkeypatch.delenv("WB_H2D_PIPELINE")
+
+
+def test_h2d_pipeline_waves(cuda):
+    """More utterances than lanes: the H2D pipeline copies one wave of lanes' utterances at a
+    time (in the order the lanes take them); every utterance equals the oracle."""
+    import torch
+    from paper_1808_00687_b200.decoder import BatchDecoder
+    g = synth.random_wfst(11, 2500, 8000, 25, eps_fraction=0.05, final_fraction=0.05)
+    cfg = P.DecodeConfig(beam=9.0, max_active=120, mode="fsd")
+    posts = [synth.random_posteriors(200 + k, 60, 25) for k in range(9)]
+    T = np.full(len(posts), 60, np.int32)
+    off = np.arange(len(posts), dtype=np.int64) * 60
+    pinned = torch.empty((int(T.sum()), 26), dtype=torch.float64, pin_memory=True)
+    for p, o in zip(posts, off):
+        P.cost_table(p, out=pinned.numpy()[o:o + 60])
+    blank = np.concatenate([p.rows[:, 0] for p in posts])
+    dec = BatchDecoder(g, 0, max_utts_in_flight=2)   # 2 lanes: 5 waves
+    got = dec.decode_host(pinned.numpy(), off, T, blank, cfg, "fsd").decode_results()
+    assert dec.last_transfer()[1] == 2
+    for p, r in zip(posts, got):
+        o = O.decode(g, P.cost_table(p), p.rows[:, 0], beam=9.0, max_active=120, mode="fsd")
+        assert _fields(r) == o.astuple()
