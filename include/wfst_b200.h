@@ -78,7 +78,9 @@ typedef struct {
     int32_t max_active;      /* 0 = None */
     int32_t mode;            /* 0 = fsd, 1 = lsd */
     int32_t lattice;         /* 1 = record the raw lattice (LatticeRecorder) */
-    int32_t _pad;
+    int32_t log_rows;        /* 1 = the cost rows hold log(p) (acoustic scale 1): the decoder
+                                negates each value as it stages the row, which saves the host a
+                                pass; needs rows that fit shared memory (<= 16384 columns) */
     double lattice_beam;     /* >= 0 (lattice mode): also beam-prune the lattices on the device
                                 (stage one of prune_lattice, see wb_lattice_pruned_fetch); < 0 off */
 } wb_config;

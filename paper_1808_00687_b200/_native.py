@@ -47,7 +47,7 @@ class GraphDesc(C.Structure):
 class Config(C.Structure):
     _fields_ = [("beam", C.c_double), ("blank_threshold", C.c_double),
                 ("max_active", C.c_int32), ("mode", C.c_int32), ("lattice", C.c_int32),
-                ("_pad", C.c_int32), ("lattice_beam", C.c_double)]
+                ("log_rows", C.c_int32), ("lattice_beam", C.c_double)]
 
 
 class DecoderOpts(C.Structure):

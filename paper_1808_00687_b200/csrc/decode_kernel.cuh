@@ -139,6 +139,7 @@ struct WorkDev {
     long long S;
     int cap, T_cap, smem_cands, row_in_smem;
     int stage_off;        // dyn-smem byte offset of the per-lane arc prefetch buffers (0 = off)
+    int log_rows;         // the cost rows hold log(p): negated as they are read (rows staged)
     int beam_skip;        // expand skips relaxations provably outside the beam
     int exact_min;        // token-filtered exact emitting-minimum pass (needs a non-negative row)
     int xchg_gather;      // gather reads and resets each slot with one 128-bit atomic exchange
@@ -542,7 +543,7 @@ __device__ __forceinline__ bool finish_relax(Slot *p, const Slot &want, Slot pre
 // the step's running minimum, an upper bound of its best cost.
 template <int BLOCK>
 __device__ __forceinline__ void pilot_min(int bt, int cur, const double *row, const GraphDev &g,
-                                          const WorkDev &ws) {
+                                          const WorkDev &ws, bool neg_row = false) {
     const int l = threadIdx.x & 31;
     // the token's arc range and cost as the compaction recorded them with best_tok
     const u64 br = *(volatile u64 *)&SH<BLOCK>().best_rng;
@@ -550,7 +551,7 @@ __device__ __forceinline__ void pilot_min(int bt, int cur, const double *row, co
     u64 m = EMPTY_KEY;
     for (int a = (int)(u32)br + l; a < (int)(u32)(br >> 32); a += 32) {
         const int4 r = ld_arc(&g.arcs[2 * a]);
-        const double ac = row[r.y];
+        const double ac = neg_row ? -row[r.y] : row[r.y];
         if (ac != INFINITY) {
             const u64 k = cost_key(__dadd_rn(__dadd_rn(tc, __hiloint2double(r.w, r.z)), ac));
             m = k < m ? k : m;
@@ -1687,7 +1688,7 @@ WB_LATTICE_FN __device__ int record_lattice_step(int k, int nxt, int n_surv, int
     const double *row = grow;
     if (k > 0 && ws.row_in_smem) {
         double *srow = s_row<BLOCK>();
-        for (int q = threadIdx.x; q < L1; q += BLOCK) srow[q] = __ldg(&grow[q]);
+        for (int q = threadIdx.x; q < L1; q += BLOCK) srow[q] = ws.log_rows ? -__ldg(&grow[q]) : __ldg(&grow[q]);
         row = srow;
     }
     __syncthreads();
@@ -2168,7 +2169,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
             const bool pilot = row_in_smem && pilot_on && sh.best_tok >= 0 && sh.best_tok < n_live;
             if (pilot && threadIdx.x < 32) {
                 __syncwarp();
-                pilot_min<BLOCK>(sh.best_tok, cur, grow, g, ws);
+                pilot_min<BLOCK>(sh.best_tok, cur, grow, g, ws, ws.log_rows != 0);
             }
             if (row_in_smem) {
                 const int t0 = pilot ? (int)threadIdx.x - 32 : (int)threadIdx.x;
@@ -2181,6 +2182,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ WorkDe
                     for (int i = 0; i < 8; ++i) {
                         const int q = q0 + i * nt;
                         v[i] = q < b.L1 ? __ldg(&grow[q]) : 0.0;
+                        if (ws.log_rows) v[i] = -v[i];   // log(p) rows: the cost is -log(p)
                     }
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {

@@ -344,6 +344,7 @@ static cudaError_t launch_decode(int max_grid, int num_sms, int num_cols, cudaSt
     // WB_SMEM_CANDS caps the candidates kept in shared memory (tests force the global path)
     if (const char *sc = std::getenv("WB_SMEM_CANDS")) wd.smem_cands = std::min(wd.smem_cands, std::max(0, std::atoi(sc)));
     wd.row_in_smem = row > 0;
+    if (wd.log_rows && !wd.row_in_smem) return cudaErrorNotSupported;   // log(p) rows are negated as staged
     // per-lane arc prefetch buffers (2 x 16 B) after the staged row, when they fit
     const size_t row_r = (row + 127) & ~(size_t)127, stage = (size_t)BLOCK * 32;
     const char *pf = std::getenv("WB_PREFETCH");
@@ -797,6 +798,7 @@ static int decode_impl(wb_decoder_t d, int32_t n, const double *costs, const int
     }
     BatchDev bd{dc, doff, dT, db, num_cols, n, dol, dil, lcap, ready_dev, crow_dev};
     CfgDev cd{cfg->beam, cfg->blank_threshold, cfg->max_active, cfg->mode, cfg->lattice};
+    wd.log_rows = cfg->log_rows ? 1 : 0;
     const bool prune = cfg->lattice && cfg->lattice_beam >= 0;
     if (cfg->lattice && !(cfg->lattice_beam < 0) && std::isnan(cfg->lattice_beam))
         return set_err(WB_ERR_VALUE, "lattice_beam must be >= 0");

@@ -75,9 +75,9 @@ class SearchDied(RuntimeError):
 
 
 def _native_config(cfg, mode: str, lattice: bool = False,
-                   lattice_beam: float | None = None) -> N.Config:
+                   lattice_beam: float | None = None, log_rows: bool = False) -> N.Config:
     return N.Config(float(cfg.beam), float(cfg.blank_threshold), int(cfg.max_active or 0),
-                    0 if mode == "fsd" else 1, int(bool(lattice)), 0,
+                    0 if mode == "fsd" else 1, int(bool(lattice)), int(bool(log_rows)),
                     -1.0 if lattice_beam is None else float(lattice_beam))
 
 
@@ -446,7 +446,10 @@ class BatchDecoder:
         cap = label_capacity or (maxT + 64)
         if lattice_beam is not None and not lattice_beam >= 0:
             raise ValueError(f"lattice_beam must be >= 0, got {lattice_beam}")
-        ncfg = _native_config(cfg, mode, lattice, lattice_beam)
+        # scale 1: the rows keep log(p) and the decoder negates them as it stages each row
+        # (exact; one pass less for the producers).  WB_LOG_ROWS=0: costs on the host.
+        log_rows = float(cfg.acoustic_scale) == 1.0 and os.environ.get("WB_LOG_ROWS", "1") != "0"
+        ncfg = _native_config(cfg, mode, lattice, lattice_beam, log_rows)
         self._last_max_active = cfg.max_active
         N.flush_destroy()
         L = self._L
@@ -483,16 +486,19 @@ class BatchDecoder:
                 dst = costs[r0:r0 + hi - lo, 1:]
                 with np.errstate(divide="ignore"):
                     np.log(dst, out=dst)
-                np.multiply(dst, neg, out=dst)
-                costs[r0:r0 + hi - lo, 0] = np.inf
+                if log_rows:
+                    costs[r0:r0 + hi - lo, 0] = -np.inf
+                else:
+                    np.multiply(dst, neg, out=dst)
+                    costs[r0:r0 + hi - lo, 0] = np.inf
             else:
                 view = costs[off[u]:off[u] + T[u]]
                 if need[u] is None:
-                    cost_rows(p, np.arange(lo, hi), view, cfg.acoustic_scale)
+                    cost_rows(p, np.arange(lo, hi), view, cfg.acoustic_scale, log_only=log_rows)
                 else:
                     sel = need[u][(need[u] >= lo) & (need[u] < hi)]
                     if len(sel):
-                        cost_rows(p, sel, view, cfg.acoustic_scale)
+                        cost_rows(p, sel, view, cfg.acoustic_scale, log_only=log_rows)
             with lock:
                 done[u][b] = hi
                 while nxt[u] in done[u]:
@@ -549,6 +555,8 @@ class BatchDecoder:
                 self._grow(flags, lattice_out_need=need_out, max_frames=maxT)
             if batch is not None:
                 # the batch's rows are costs now (converted in place): retry from the table
+                if log_rows:   # (log(p) rows: the costs are their negation, exactly)
+                    np.negative(costs, out=costs)
                 return self.decode_host(costs, off, T, blank, cfg, mode, cap, lattice,
                                         lattice_beam)
             return self.decode_posteriors(posts_list, cfg, mode, cap, lattice, lattice_beam,
